@@ -1,0 +1,189 @@
+/*
+ * sslic_b200 — C ABI of the B200-native SSLIC hot path (sm_100a).
+ *
+ * Drop-in boundary for the reference's C++ SLIC interface
+ * (/root/reference/proj/include/sslic/). Every entry point below names the
+ * reference function it replaces. Plain pointers and sizes only; no torch or
+ * C++ types cross this boundary. The C++ adapter over the reference's own
+ * types is include/sslic_b200.hpp; the Python mirror is
+ * paper_1806_08741_b200/__init__.py.
+ *
+ * Conventions
+ *  - Layout is the reference's frozen layout (image.hpp:1-5): axis 0 fastest,
+ *    channels interleaved; rank 1..4 (image.hpp:25).
+ *  - Status codes mirror the reference's exception classes
+ *    (SURVEY §8b "Errors"): SSLIC_EINVAL = std::invalid_argument,
+ *    SSLIC_ELOGIC = std::logic_error, SSLIC_ERANGE = std::out_of_range.
+ *    sslic_last_error() returns the thread's last message.
+ *  - Host entry points take HOST buffers and copy; engine entry points work on
+ *    DEVICE buffers and run on the caller's CUDA stream.
+ *  - There is no CPU fallback: every compute entry point runs CUDA kernels and
+ *    fails with SSLIC_ECUDA when no sm_100 device is usable.
+ */
+#ifndef SSLIC_B200_H
+#define SSLIC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SSLIC_OK 0
+#define SSLIC_EINVAL (-1) /* std::invalid_argument (slic.hpp:52-64, image.hpp:238-249) */
+#define SSLIC_ELOGIC (-2) /* std::logic_error (slic.hpp:330-331) */
+#define SSLIC_ERANGE (-3) /* std::out_of_range (image.hpp:112-124) */
+#define SSLIC_ECUDA (-4)
+#define SSLIC_ENOMEM (-5)
+
+#define SSLIC_UNDEFINED 0xffffffffu /* LabelMap::kUndefined (image.hpp:291) */
+
+typedef enum {
+  SSLIC_U8 = 0,  /* io.hpp:67-71 uint8 volumes */
+  SSLIC_U16 = 1, /* config 3 (not readable by the reference I/O; exact in fp64) */
+  SSLIC_F32 = 2, /* io.hpp:67-71 float32 volumes */
+  SSLIC_F64 = 3  /* NDImage's own storage (image.hpp:284) */
+} sslic_dtype;
+
+/* NDImage (image.hpp:236-285) in its native storage type. */
+typedef struct {
+  int rank;          /* 1..4 */
+  int64_t dims[4];   /* extents, axis 0 fastest */
+  int channels;      /* >= 1, interleaved */
+  int dtype;         /* sslic_dtype */
+  const void* data;  /* host or device pointer (see each entry point) */
+} sslic_image;
+
+/* SlicParams (slic.hpp:34-65). */
+typedef struct {
+  int64_t grid[4];            /* S per axis, 1 <= S <= dims */
+  double weight_m;            /* m > 0 (default 10) */
+  int max_iterations;         /* 0 => 10 for rank <= 2, 5 otherwise */
+  int enforce_connectivity;   /* used by sslic_segment only */
+  int has_residual_threshold; /* std::optional<double> residual_threshold */
+  double residual_threshold;
+} sslic_params;
+
+const char* sslic_last_error(void);
+const char* sslic_version(void);
+
+/* k = prod ceil(d_a/S_a) (slic.hpp:212-216); 0 on invalid input. */
+int64_t sslic_cluster_count(int rank, const int64_t* dims, const int64_t* grid);
+int sslic_iterations_for(const sslic_params* p, int rank); /* SlicParams::iterations_for 47-50 */
+
+/* run_slic (slic.hpp:384-415). img->data is HOST memory. Outputs (host):
+ *   labels_out[N] (uint32), centers_out[k*(c+rank)], residuals_out[iterations],
+ *   *iterations_done. The reference's `workers` maps to nothing: one device. */
+int sslic_run_slic(const sslic_image* img, const sslic_params* params, int device,
+                   uint32_t* labels_out, double* centers_out, double* residuals_out,
+                   int* iterations_done);
+
+/* run_slic followed by enforce_connectivity (tools/sslic.cpp:104-108).
+ * *next_label_out = the sweep's next unused label. */
+int sslic_segment(const sslic_image* img, const sslic_params* params, int device,
+                  uint32_t* labels_out, double* centers_out, double* residuals_out,
+                  int* iterations_done, uint32_t* next_label_out);
+
+/* init_centers (slic.hpp:206-230) [+ perturb_centers (236-267) when perturb].
+ * centers_out: k*(c+rank) doubles (host). */
+int sslic_init_centers(const sslic_image* img, const sslic_params* params, int perturb,
+                       int device, double* centers_out);
+
+/* perturb_centers (slic.hpp:236-267) of a caller-given table (host, in-out). */
+int sslic_perturb_centers(const sslic_image* img, double* centers, int64_t k, int device);
+
+/* gradient_magnitude_sq (color.hpp:71-102) at n coordinates (host, n*rank). */
+int sslic_gradient_sq(const sslic_image* img, const int64_t* coords, int64_t n, int device,
+                      double* out);
+
+/* squared_distance (slic.hpp:189-200) for n (center, pixel, coord) triples,
+ * evaluated by the device's exact distance routine (host buffers). */
+int sslic_squared_distance(int channels, int rank, const int64_t* grid, double weight_m,
+                           int64_t n, const double* centers, const double* pixels,
+                           const int64_t* coords, int device, double* out);
+
+/* One assign_labels pass over the whole image (slic.hpp:275-310) with
+ * caller-owned labels/dists (host, in-out): the compat path used for the
+ * "single pass bit-exact given identical centres" gate. */
+int sslic_assign_pass(const sslic_image* img, const sslic_params* params, const double* centers,
+                      int64_t k, int device, uint32_t* labels, double* dists);
+
+/* accumulate_region over the whole image + merge (slic.hpp:315-346, 133-143).
+ * sums_out[k*(c+rank)] (double), counts_out[k]. ELOGIC on undefined labels. */
+int sslic_accumulate(const sslic_image* img, const uint32_t* labels, int64_t k, int device,
+                     double* sums_out, int64_t* counts_out);
+
+/* reduce_and_update (slic.hpp:352-372) on merged sums/counts: centers in-out,
+ * residual out. */
+int sslic_reduce_and_update(double* centers, int64_t k, int stride, const double* sums,
+                            const int64_t* counts, int device, double* residual_out);
+
+/* enforce_connectivity (connectivity.hpp:265-273). Host buffers. */
+int sslic_enforce_connectivity(int rank, const int64_t* dims, const uint32_t* labels_in,
+                               const double* centers, int channels, int64_t k,
+                               const int64_t* grid, int device, uint32_t* labels_out,
+                               uint32_t* next_label_out);
+
+/* ------------------------------------------------------------------------ */
+/* Device-resident engine: the per-iteration loop on HBM-resident data, one  */
+/* z-slab (last axis) per GPU. Used by bench.py and multi-GPU runs.          */
+/* ------------------------------------------------------------------------ */
+typedef struct sslic_engine sslic_engine;
+
+/* img->dims are the FULL image; img->data is a DEVICE pointer to planes
+ * [data_begin, data_end) of the last axis, which must cover
+ * [slab_begin-2, slab_end+2) clipped to the image (the perturbation halo).
+ * stream: cudaStream_t (NULL = legacy default). */
+int sslic_engine_create(const sslic_image* img, const sslic_params* params, int device,
+                        int64_t slab_begin, int64_t slab_end, int64_t data_begin,
+                        int64_t data_end, void* stream, sslic_engine** out);
+int sslic_engine_destroy(sslic_engine* e);
+
+/* init_centers + perturb_centers for the clusters whose initial cell centre
+ * lies in this slab (zeros elsewhere). With several slabs, sum the tables
+ * across ranks (exact: one non-zero term per entry) then commit. */
+int sslic_engine_init(sslic_engine* e);
+int sslic_engine_centers_buffer(sslic_engine* e, double** dev_ptr, int64_t* count);
+int sslic_engine_commit_centers(sslic_engine* e);
+
+/* Fused assign_labels + accumulate_region over the slab (one iteration's
+ * map phase). Per-cluster partial sums land in the int64 partials buffer
+ * (k*(c+rank+1)); sum it across ranks before sslic_engine_update. */
+int sslic_engine_assign(sslic_engine* e);
+int sslic_engine_partials(sslic_engine* e, int64_t** dev_ptr, int64_t* count);
+/* reduce_and_update on the (reduced) partials; residual kept on device. */
+int sslic_engine_update(sslic_engine* e);
+/* assign + update (single slab covering the whole image). */
+int sslic_engine_iterate(sslic_engine* e, int iterations);
+
+int sslic_engine_iterations_done(sslic_engine* e);
+/* Copies residuals of the iterations done so far (host). Synchronizes. */
+int sslic_engine_residuals(sslic_engine* e, double* host_out);
+/* Slab labels (plain uint32, tags stripped) into a DEVICE buffer. */
+int sslic_engine_labels(sslic_engine* e, uint32_t* dev_out);
+int sslic_engine_centers(sslic_engine* e, double* host_out);
+/* Number of voxels whose label was undefined at the last accumulation
+ * (the reference throws std::logic_error for any). Synchronizes. */
+int64_t sslic_engine_undefined_count(sslic_engine* e);
+/* Kernel launches issued by the engine so far (bench.py's gpu_launches). */
+int64_t sslic_engine_launch_count(sslic_engine* e);
+/* Device time (ms, CUDA events on the engine stream) of the i-th assign
+ * kernel launch since creation; *n_out = launches recorded. Synchronizes. */
+int sslic_engine_assign_ms(sslic_engine* e, int i, float* ms_out, int* n_out);
+/* Enable counting of candidate evaluations / window volumes in assign. */
+int sslic_engine_set_stats(sslic_engine* e, int on);
+/* Assignment evaluation statistics of the last assign (bench roofline):
+ * *evals = candidate evaluations actually performed, *window_evals =
+ * sum_k |W_k ∩ slab| (the algorithmic count). Synchronizes. */
+int sslic_engine_eval_stats(sslic_engine* e, double* evals, double* window_evals);
+
+/* Seeded synthetic volumes for the five BASELINE configs, generated on the
+ * device straight into HBM (planes [z_begin, z_end) of the last axis). */
+int sslic_synth_generate(int config, int rank, const int64_t* dims, int channels, int dtype,
+                         uint64_t seed, int64_t z_begin, int64_t z_end, void* dev_out,
+                         void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

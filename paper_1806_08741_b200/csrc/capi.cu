@@ -1,0 +1,699 @@
+// C ABI (include/sslic_b200.h) over the Engine. Host entry points copy host
+// buffers to the device, run the CUDA path and copy results back; every
+// failure is reported as a status code mirroring the reference's exception
+// classes, with the message in sslic_last_error().
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "connectivity.cuh"
+#include "engine.cuh"
+
+using namespace sslic_b200;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int status, const std::string& msg) {
+  g_last_error = msg;
+  return status;
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    g_last_error.clear();
+    return f();
+  } catch (const Error& e) {
+    return fail(e.status, e.what());
+  } catch (const std::bad_alloc&) {
+    return fail(SSLIC_ENOMEM, "host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(SSLIC_EINVAL, e.what());
+  }
+}
+
+size_t dtype_size(int dt) {
+  switch (dt) {
+    case SSLIC_U8: return 1;
+    case SSLIC_U16: return 2;
+    case SSLIC_F32: return 4;
+    case SSLIC_F64: return 8;
+    default: return 0;
+  }
+}
+
+int64_t pixel_count(const sslic_image& img) {
+  int64_t n = 1;
+  for (int a = 0; a < img.rank; ++a) n *= img.dims[a];
+  return n;
+}
+
+// NDImage constructor checks (image.hpp:238-249).
+void validate_image(const sslic_image* img) {
+  if (!img) throw Error(SSLIC_EINVAL, "image: null descriptor");
+  if (img->rank < 1 || img->rank > kMaxRank)
+    throw Error(SSLIC_EINVAL, "NDImage: rank must be in [1, 4]");
+  for (int a = 0; a < img->rank; ++a)
+    if (img->dims[a] < 1) throw Error(SSLIC_EINVAL, "NDImage: extents must be positive");
+  if (img->channels < 1) throw Error(SSLIC_EINVAL, "NDImage: channels must be >= 1");
+  if (dtype_size(img->dtype) == 0) throw Error(SSLIC_EINVAL, "image: unknown dtype");
+  if (!img->data) throw Error(SSLIC_EINVAL, "image: null data");
+}
+
+// SlicParams::validate (slic.hpp:52-64).
+void validate_params(const sslic_params* p, const sslic_image* img) {
+  if (!p) throw Error(SSLIC_EINVAL, "SlicParams: null");
+  for (int a = 0; a < img->rank; ++a) {
+    if (p->grid[a] < 1) throw Error(SSLIC_EINVAL, "SlicParams: grid sizes must be >= 1");
+    if (p->grid[a] > img->dims[a])
+      throw Error(SSLIC_EINVAL,
+                  "SlicParams: grid size exceeds image extent on axis " + std::to_string(a));
+  }
+  if (!(p->weight_m > 0.0)) throw Error(SSLIC_EINVAL, "SlicParams: weight_m must be positive");
+  if (p->max_iterations < 0)
+    throw Error(SSLIC_EINVAL, "SlicParams: max_iterations must be positive (or 0 for default)");
+}
+
+struct DeviceBuf {
+  void* p = nullptr;
+  cudaStream_t s = nullptr;
+  DeviceBuf(size_t bytes, cudaStream_t st) : s(st) {
+    SSLIC_CUDA_CHECK(cudaMallocAsync(&p, bytes ? bytes : 1, st));
+  }
+  ~DeviceBuf() {
+    if (p) cudaFreeAsync(p, s);
+  }
+  DeviceBuf(const DeviceBuf&) = delete;
+  DeviceBuf& operator=(const DeviceBuf&) = delete;
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+struct Stream {
+  cudaStream_t s = nullptr;
+  explicit Stream(int device) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+      throw Error(SSLIC_ECUDA, "no CUDA device available (the B200 path has no CPU fallback)");
+    if (device < 0 || device >= n) throw Error(SSLIC_EINVAL, "device index out of range");
+    SSLIC_CUDA_CHECK(cudaSetDevice(device));
+    SSLIC_CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  }
+  ~Stream() {
+    if (s) {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
+  }
+  void sync() { SSLIC_CUDA_CHECK(cudaStreamSynchronize(s)); }
+};
+
+__global__ void k_count_nonfinite(const void* data, int dtype, int64_t n, unsigned long long* out) {
+  unsigned long long bad = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    bad += isfinite(load_value(data, dtype, i)) ? 0 : 1;
+  for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
+  if ((threadIdx.x & 31) == 0 && bad) atomicAdd(out, bad);
+}
+
+// Uploads a host image; checks finiteness like the NDImage constructor.
+std::unique_ptr<DeviceBuf> upload_image(const sslic_image* img, Stream& st) {
+  const int64_t nvals = pixel_count(*img) * img->channels;
+  const size_t bytes = (size_t)nvals * dtype_size(img->dtype);
+  auto buf = std::make_unique<DeviceBuf>(bytes, st.s);
+  SSLIC_CUDA_CHECK(cudaMemcpyAsync(buf->p, img->data, bytes, cudaMemcpyHostToDevice, st.s));
+  if (img->dtype == SSLIC_F32 || img->dtype == SSLIC_F64) {
+    DeviceBuf cnt(sizeof(unsigned long long), st.s);
+    SSLIC_CUDA_CHECK(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), st.s));
+    k_count_nonfinite<<<148 * 4, 256, 0, st.s>>>(buf->p, img->dtype, nvals,
+                                                 cnt.as<unsigned long long>());
+    SSLIC_CUDA_CHECK(cudaGetLastError());
+    unsigned long long bad = 0;
+    SSLIC_CUDA_CHECK(cudaMemcpyAsync(&bad, cnt.p, sizeof(bad), cudaMemcpyDeviceToHost, st.s));
+    st.sync();
+    if (bad) throw Error(SSLIC_EINVAL, "NDImage: non-finite value");
+  }
+  return buf;
+}
+
+sslic_image device_view(const sslic_image* img, const void* dev) {
+  sslic_image v = *img;
+  v.data = dev;
+  for (int a = img->rank; a < kMaxRank; ++a) v.dims[a] = 1;
+  return v;
+}
+
+sslic_params default_params_for(const sslic_image* img, const int64_t* grid, double m) {
+  sslic_params p{};
+  for (int a = 0; a < kMaxRank; ++a) p.grid[a] = a < img->rank ? grid[a] : 1;
+  p.weight_m = m;
+  return p;
+}
+
+// The run_slic loop over a whole-image engine. Returns iterations done.
+int run_loop(Engine& e, const sslic_params* p, Stream& st) {
+  e.init(true);
+  e.commit();
+  const int iters = e.max_iterations();
+  for (int it = 0; it < iters; ++it) {
+    e.assign(true);
+    if (e.undefined_count() > 0)  // slic.hpp:330-331
+      throw Error(SSLIC_ELOGIC, "accumulate_region: pixel with undefined label");
+    e.update();
+    if (p->has_residual_threshold) {
+      double r = 0.0;
+      std::vector<double> rs(e.iterations_done());
+      e.residuals_to_host(rs.data(), e.iterations_done());
+      r = rs.back();
+      if (r <= p->residual_threshold) break;  // slic.hpp:411
+    }
+  }
+  st.sync();
+  return e.iterations_done();
+}
+
+__global__ void k_update_from_sums(int64_t k, int stride, const double* sums,
+                                   const int64_t* counts, double* centers, double* partial) {
+  const int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  double part = 0.0;
+  if (id < k && counts[id] != 0) {
+    for (int i = 0; i < stride; ++i) {
+      const double v = __ddiv_rn(sums[id * stride + i], (double)counts[id]);
+      const double d = __dsub_rn(v, centers[id * stride + i]);
+      centers[id * stride + i] = v;
+      part = __dadd_rn(part, __dmul_rn(d, d));
+    }
+  }
+  __shared__ double red[256];
+  red[threadIdx.x] = part;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] = __dadd_rn(red[threadIdx.x], red[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
+}
+
+}  // namespace
+
+struct sslic_engine {
+  std::unique_ptr<Engine> e;
+};
+
+extern "C" {
+
+const char* sslic_last_error(void) { return g_last_error.c_str(); }
+const char* sslic_version(void) { return "sslic_b200 0.1 (sm_100a)"; }
+
+int64_t sslic_cluster_count(int rank, const int64_t* dims, const int64_t* grid) {
+  if (rank < 1 || rank > kMaxRank || !dims || !grid) return 0;
+  int64_t k = 1;
+  for (int a = 0; a < rank; ++a) {
+    if (grid[a] < 1 || dims[a] < 1) return 0;
+    k *= (dims[a] + grid[a] - 1) / grid[a];
+  }
+  return k;
+}
+
+int sslic_iterations_for(const sslic_params* p, int rank) {
+  if (!p) return 0;
+  return p->max_iterations > 0 ? p->max_iterations : (rank <= 2 ? 10 : 5);
+}
+
+int sslic_run_slic(const sslic_image* img, const sslic_params* params, int device,
+                   uint32_t* labels_out, double* centers_out, double* residuals_out,
+                   int* iterations_done) {
+  return guarded([&] {
+    validate_image(img);
+    validate_params(params, img);
+    Stream st(device);
+    auto dimg = upload_image(img, st);
+    const sslic_image v = device_view(img, dimg->p);
+    const int64_t last = img->dims[img->rank - 1];
+    Engine e(v, *params, device, 0, last, 0, last, st.s);
+    const int done = run_loop(e, params, st);
+    const int64_t n = pixel_count(*img);
+    {
+      DeviceBuf lab(n * sizeof(uint32_t), st.s);
+      e.unpack_labels(lab.as<uint32_t>());
+      SSLIC_CUDA_CHECK(cudaMemcpyAsync(labels_out, lab.p, n * sizeof(uint32_t),
+                                       cudaMemcpyDeviceToHost, st.s));
+      st.sync();
+    }
+    e.copy_centers_to_host(centers_out);
+    if (residuals_out) e.residuals_to_host(residuals_out, done);
+    if (iterations_done) *iterations_done = done;
+    return SSLIC_OK;
+  });
+}
+
+int sslic_segment(const sslic_image* img, const sslic_params* params, int device,
+                  uint32_t* labels_out, double* centers_out, double* residuals_out,
+                  int* iterations_done, uint32_t* next_label_out) {
+  return guarded([&] {
+    validate_image(img);
+    validate_params(params, img);
+    Stream st(device);
+    auto dimg = upload_image(img, st);
+    const sslic_image v = device_view(img, dimg->p);
+    const int64_t last = img->dims[img->rank - 1];
+    Engine e(v, *params, device, 0, last, 0, last, st.s);
+    const int done = run_loop(e, params, st);
+    const int64_t n = pixel_count(*img);
+    DeviceBuf lab(n * sizeof(uint32_t), st.s);
+    e.unpack_labels(lab.as<uint32_t>());
+    uint32_t next = (uint32_t)e.geom().k;
+    if (params->enforce_connectivity) {
+      DeviceBuf out(n * sizeof(uint32_t), st.s);
+      next = enforce_connectivity_device(e.geom(), lab.as<uint32_t>(), e.current_centers(),
+                                         out.as<uint32_t>(), st.s);
+      SSLIC_CUDA_CHECK(cudaMemcpyAsync(labels_out, out.p, n * sizeof(uint32_t),
+                                       cudaMemcpyDeviceToHost, st.s));
+      st.sync();
+    } else {
+      SSLIC_CUDA_CHECK(cudaMemcpyAsync(labels_out, lab.p, n * sizeof(uint32_t),
+                                       cudaMemcpyDeviceToHost, st.s));
+      st.sync();
+    }
+    e.copy_centers_to_host(centers_out);
+    if (residuals_out) e.residuals_to_host(residuals_out, done);
+    if (iterations_done) *iterations_done = done;
+    if (next_label_out) *next_label_out = next;
+    return SSLIC_OK;
+  });
+}
+
+int sslic_init_centers(const sslic_image* img, const sslic_params* params, int perturb,
+                       int device, double* centers_out) {
+  return guarded([&] {
+    validate_image(img);
+    validate_params(params, img);
+    Stream st(device);
+    auto dimg = upload_image(img, st);
+    const sslic_image v = device_view(img, dimg->p);
+    const int64_t last = img->dims[img->rank - 1];
+    Engine e(v, *params, device, 0, last, 0, last, st.s, true);
+    e.init(perturb != 0);
+    e.copy_centers_to_host(centers_out);
+    return SSLIC_OK;
+  });
+}
+
+int sslic_perturb_centers(const sslic_image* img, double* centers, int64_t k, int device) {
+  return guarded([&] {
+    validate_image(img);
+    Stream st(device);
+    auto dimg = upload_image(img, st);
+    Geom g{};
+    g.rank = img->rank;
+    g.channels = img->channels;
+    g.stride = img->channels + img->rank;
+    g.dtype = img->dtype;
+    int64_t acc = 1;
+    for (int a = 0; a < kMaxRank; ++a) {
+      g.dims[a] = a < img->rank ? img->dims[a] : 1;
+      g.strides[a] = acc;
+      acc *= g.dims[a];
+      g.grid[a] = g.cells[a] = 1;
+    }
+    g.k = k;
+    g.plane = acc / g.dims[img->rank - 1];
+    g.slab_begin = g.data_begin = 0;
+    g.slab_end = g.data_end = g.dims[img->rank - 1];
+    DeviceBuf c(k * g.stride * sizeof(double), st.s);
+    SSLIC_CUDA_CHECK(cudaMemcpyAsync(c.p, centers, k * g.stride * sizeof(double),
+                                     cudaMemcpyHostToDevice, st.s));
+    if (k > 0) {
+      k_perturb_table<<<(unsigned)((k + 127) / 128), 128, 0, st.s>>>(g, dimg->p, c.as<double>());
+      SSLIC_CUDA_CHECK(cudaGetLastError());
+    }
+    SSLIC_CUDA_CHECK(cudaMemcpyAsync(centers, c.p, k * g.stride * sizeof(double),
+                                     cudaMemcpyDeviceToHost, st.s));
+    st.sync();
+    return SSLIC_OK;
+  });
+}
+
+int sslic_gradient_sq(const sslic_image* img, const int64_t* coords, int64_t n, int device,
+                      double* out) {
+  return guarded([&] {
+    validate_image(img);
+    for (int64_t i = 0; i < n; ++i)
+      for (int a = 0; a < img->rank; ++a)
+        if (coords[i * img->rank + a] < 0 || coords[i * img->rank + a] >= img->dims[a])
+          throw Error(SSLIC_ERANGE, "linear_index: coordinate outside image");
+    Stream st(device);
+    auto dimg = upload_image(img, st);
+    sslic_params p = default_params_for(img, img->dims, 10.0);
+    const sslic_image v = device_view(img, dimg->p);
+    const int64_t last = img->dims[img->rank - 1];
+    Engine e(v, p, device, 0, last, 0, last, st.s, true);
+    DeviceBuf dc(n * img->rank * sizeof(int64_t), st.s), dout(n * sizeof(double), st.s);
+    SSLIC_CUDA_CHECK(cudaMemcpyAsync(dc.p, coords, n * img->rank * sizeof(int64_t),
+                                     cudaMemcpyHostToDevice, st.s));
+    if (n > 0) {
+      k_gradient_points<<<(unsigned)((n + 127) / 128), 128, 0, st.s>>>(
+          e.geom(), dimg->p, dc.as<int64_t>(), n, dout.as<double>());
+      SSLIC_CUDA_CHECK(cudaGetLastError());
+    }
+    SSLIC_CUDA_CHECK(cudaMemcpyAsync(out, dout.p, n * sizeof(double), cudaMemcpyDeviceToHost,
+                                     st.s));
+    st.sync();
+    return SSLIC_OK;
+  });
+}
+
+int sslic_squared_distance(int channels, int rank, const int64_t* grid, double weight_m,
+                           int64_t n, const double* centers, const double* pixels,
+                           const int64_t* coords, int device, double* out) {
+  return guarded([&] {
+    if (rank < 1 || rank > kMaxRank || channels < 1)
+      throw Error(SSLIC_EINVAL, "squared_distance: center size must be channels + rank");
+    Stream st(device);
+    Geom g{};
+    g.rank = rank;
+    g.channels = channels;
+    g.stride = channels + rank;
+    for (int a = 0; a < kMaxRank; ++a) g.grid[a] = a < rank ? (int)grid[a] : 1;
+    g.m_sq = weight_m * weight_m;
+    DeviceBuf dc(n * g.stride * sizeof(double), st.s), dp(n * channels * sizeof(double), st.s),
+        dx(n * rank * sizeof(int64_t), st.s), dout(n * sizeof(double), st.s);
+    SSLIC_CUDA_CHECK(cudaMemcpyAsync(dc.p, centers, n * g.stride * sizeof(double),
+                                     cudaMemcpyHostToDevice, st.s));
+    SSLIC_CUDA_CHECK(cudaMemcpyAsync(dp.p, pixels, n * channels * sizeof(double),
+                                     cudaMemcpyHostToDevice, st.s));
+    SSLIC_CUDA_CHECK(cudaMemcpyAsync(dx.p, coords, n * rank * sizeof(int64_t),
+                                     cudaMemcpyHostToDevice, st.s));
+    if (n > 0) {
+      k_distance_points<<<(unsigned)((n + 127) / 128), 128, 0, st.s>>>(
+          g, n, dc.as<double>(), dp.as<double>(), dx.as<int64_t>(), dout.as<double>());
+      SSLIC_CUDA_CHECK(cudaGetLastError());
+    }
+    SSLIC_CUDA_CHECK(cudaMemcpyAsync(out, dout.p, n * sizeof(double), cudaMemcpyDeviceToHost,
+                                     st.s));
+    st.sync();
+    return SSLIC_OK;
+  });
+}
+
+int sslic_assign_pass(const sslic_image* img, const sslic_params* params, const double* centers,
+                      int64_t k, int device, uint32_t* labels, double* dists) {
+  return guarded([&] {
+    validate_image(img);
+    for (int a = 0; a < img->rank; ++a)
+      if (params->grid[a] < 1) throw Error(SSLIC_EINVAL, "SlicParams: grid sizes must be >= 1");
+    Stream st(device);
+    auto dimg = upload_image(img, st);
+    // The engine sizes its table from the grid; a caller table may differ in
+    // k, so build the engine with a grid whose cell count we override below.
+    const sslic_image v = device_view(img, dimg->p);
+    const int64_t last = img->dims[img->rank - 1];
+    sslic_params p = *params;
+    p.max_iterations = 1;
+    Engine e(v, p, device, 0, last, 0, last, st.s, true, k);
+    e.set_centers_host(centers);
+    e.commit();
+    const int64_t n = pixel_count(*img);
+    SSLIC_CUDA_CHECK(cudaMemcpyAsync(e.label_words(), labels, n * sizeof(uint32_t),
+                                     cudaMemcpyHostToDevice, st.s));
+    SSLIC_CUDA_CHECK(cudaMemcpyAsync(e.dists(), dists, n * sizeof(double),
+                                     cudaMemcpyHostToDevice, st.s));
+    e.assign(false);
+    SSLIC_CUDA_CHECK(cudaMemcpyAsync(labels, e.label_words(), n * sizeof(uint32_t),
+                                     cudaMemcpyDeviceToHost, st.s));
+    SSLIC_CUDA_CHECK(cudaMemcpyAsync(dists, e.dists(), n * sizeof(double),
+                                     cudaMemcpyDeviceToHost, st.s));
+    st.sync();
+    return SSLIC_OK;
+  });
+}
+
+int sslic_accumulate(const sslic_image* img, const uint32_t* labels, int64_t k, int device,
+                     double* sums_out, int64_t* counts_out) {
+  return guarded([&] {
+    validate_image(img);
+    if (k < 0) throw Error(SSLIC_EINVAL, "accumulate: k must be >= 0");
+    Stream st(device);
+    auto dimg = upload_image(img, st);
+    const sslic_image v = device_view(img, dimg->p);
+    const int64_t last = img->dims[img->rank - 1];
+    // A grid giving exactly k cells is not needed: the engine only uses k for
+    // the accumulator size, so use grid = dims (k = 1) and then resize.
+    sslic_params p = default_params_for(img, img->dims, 10.0);
+    p.max_iterations = 1;
+    Engine e(v, p, device, 0, last, 0, last, st.s, true);
+    Geom g = e.geom();
+    g.k = k;
+    const int64_t n = pixel_count(*img);
+    DeviceBuf acc((k * (g.stride + 1) + 2) * sizeof(unsigned long long), st.s);
+    DeviceBuf dl(n * sizeof(uint32_t), st.s);
+    SSLIC_CUDA_CHECK(cudaMemcpyAsync(dl.p, labels, n * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                                     st.s));
+    SSLIC_CUDA_CHECK(cudaMemsetAsync(acc.p, 0, (k * (g.stride + 1) + 2) * sizeof(unsigned long long),
+                                     st.s));
+    unsigned long long* a = acc.as<unsigned long long>();
+    k_accumulate<<<(unsigned)((n + 255) / 256), 256, 0, st.s>>>(
+        g, dimg->p, dl.as<uint32_t>(), LabelCodec{32, 0xffffffffu}, e.value_shift(), a + 2, a,
+        a + 1);
+    SSLIC_CUDA_CHECK(cudaGetLastError());
+    std::vector<long long> h(k * (g.stride + 1) + 2);
+    SSLIC_CUDA_CHECK(cudaMemcpyAsync(h.data(), acc.p, h.size() * sizeof(long long),
+                                     cudaMemcpyDeviceToHost, st.s));
+    st.sync();
+    if (h[0]) throw Error(SSLIC_ELOGIC, "accumulate_region: pixel with undefined label");
+    if (h[1]) throw Error(SSLIC_EINVAL, "accumulate: label >= k");
+    for (int64_t id = 0; id < k; ++id) {
+      const long long* r = h.data() + 2 + id * (g.stride + 1);
+      for (int i = 0; i < g.stride; ++i)
+        sums_out[id * g.stride + i] =
+            i < g.channels ? std::ldexp((double)r[i], -e.value_shift()) : (double)r[i];
+      counts_out[id] = r[g.stride];
+    }
+    return SSLIC_OK;
+  });
+}
+
+int sslic_reduce_and_update(double* centers, int64_t k, int stride, const double* sums,
+                            const int64_t* counts, int device, double* residual_out) {
+  return guarded([&] {
+    if (k < 0 || stride < 1) throw Error(SSLIC_EINVAL, "reduce_and_update: bad table shape");
+    Stream st(device);
+    DeviceBuf dc(k * stride * sizeof(double), st.s), ds(k * stride * sizeof(double), st.s),
+        dn(k * sizeof(int64_t), st.s);
+    const int nb = (int)((k + 255) / 256);
+    DeviceBuf part((nb + 1) * sizeof(double), st.s);
+    SSLIC_CUDA_CHECK(cudaMemcpyAsync(dc.p, centers, k * stride * sizeof(double),
+                                     cudaMemcpyHostToDevice, st.s));
+    SSLIC_CUDA_CHECK(cudaMemcpyAsync(ds.p, sums, k * stride * sizeof(double),
+                                     cudaMemcpyHostToDevice, st.s));
+    SSLIC_CUDA_CHECK(cudaMemcpyAsync(dn.p, counts, k * sizeof(int64_t), cudaMemcpyHostToDevice,
+                                     st.s));
+    double r = 0.0;
+    if (k > 0) {
+      k_update_from_sums<<<nb, 256, 0, st.s>>>(k, stride, ds.as<double>(), dn.as<int64_t>(),
+                                               dc.as<double>(), part.as<double>());
+      k_residual_final<<<1, 1024, 0, st.s>>>(part.as<double>(), nb, part.as<double>() + nb);
+      SSLIC_CUDA_CHECK(cudaGetLastError());
+      SSLIC_CUDA_CHECK(cudaMemcpyAsync(&r, part.as<double>() + nb, sizeof(double),
+                                       cudaMemcpyDeviceToHost, st.s));
+    }
+    SSLIC_CUDA_CHECK(cudaMemcpyAsync(centers, dc.p, k * stride * sizeof(double),
+                                     cudaMemcpyDeviceToHost, st.s));
+    st.sync();
+    if (residual_out) *residual_out = r;
+    return SSLIC_OK;
+  });
+}
+
+int sslic_enforce_connectivity(int rank, const int64_t* dims, const uint32_t* labels_in,
+                               const double* centers, int channels, int64_t k,
+                               const int64_t* grid, int device, uint32_t* labels_out,
+                               uint32_t* next_label_out) {
+  return guarded([&] {
+    if (rank < 1 || rank > kMaxRank || channels < 1 || k < 0)
+      throw Error(SSLIC_EINVAL, "enforce_connectivity: bad shape");
+    Stream st(device);
+    Geom g{};
+    g.rank = rank;
+    g.channels = channels;
+    g.stride = channels + rank;
+    int64_t acc = 1;
+    for (int a = 0; a < kMaxRank; ++a) {
+      g.dims[a] = a < rank ? dims[a] : 1;
+      g.grid[a] = a < rank ? (int)grid[a] : 1;
+      if (g.dims[a] < 1 || g.grid[a] < 1) throw Error(SSLIC_EINVAL, "bad dims/grid");
+      g.cells[a] = (int)((g.dims[a] + g.grid[a] - 1) / g.grid[a]);
+      g.strides[a] = acc;
+      acc *= g.dims[a];
+    }
+    g.k = k;
+    g.ncells = 1;
+    for (int a = 0; a < kMaxRank; ++a) g.ncells *= g.cells[a];
+    g.plane = acc / g.dims[rank - 1];
+    g.slab_begin = g.data_begin = 0;
+    g.slab_end = g.data_end = g.dims[rank - 1];
+    const int64_t n = acc;
+    DeviceBuf din(n * sizeof(uint32_t), st.s), dout(n * sizeof(uint32_t), st.s),
+        dc(k * g.stride * sizeof(double), st.s);
+    SSLIC_CUDA_CHECK(cudaMemcpyAsync(din.p, labels_in, n * sizeof(uint32_t),
+                                     cudaMemcpyHostToDevice, st.s));
+    SSLIC_CUDA_CHECK(cudaMemcpyAsync(dc.p, centers, k * g.stride * sizeof(double),
+                                     cudaMemcpyHostToDevice, st.s));
+    const uint32_t next = enforce_connectivity_device(g, din.as<uint32_t>(), dc.as<double>(),
+                                                      dout.as<uint32_t>(), st.s);
+    SSLIC_CUDA_CHECK(cudaMemcpyAsync(labels_out, dout.p, n * sizeof(uint32_t),
+                                     cudaMemcpyDeviceToHost, st.s));
+    st.sync();
+    if (next_label_out) *next_label_out = next;
+    return SSLIC_OK;
+  });
+}
+
+// ---- engine -----------------------------------------------------------------
+
+int sslic_engine_create(const sslic_image* img, const sslic_params* params, int device,
+                        int64_t slab_begin, int64_t slab_end, int64_t data_begin,
+                        int64_t data_end, void* stream, sslic_engine** out) {
+  return guarded([&] {
+    validate_image(img);
+    validate_params(params, img);
+    const int64_t last = img->dims[img->rank - 1];
+    if (slab_begin < 0 || slab_end > last || slab_begin >= slab_end)
+      throw Error(SSLIC_EINVAL, "engine: bad slab range");
+    const int64_t need_lo = slab_begin - 2 < 0 ? 0 : slab_begin - 2;
+    const int64_t need_hi = slab_end + 2 > last ? last : slab_end + 2;
+    if (data_begin > need_lo || data_end < need_hi)
+      throw Error(SSLIC_EINVAL, "engine: data planes must cover the slab plus a 2-plane halo");
+    sslic_image v = device_view(img, img->data);
+    auto h = std::make_unique<sslic_engine>();
+    h->e = std::make_unique<Engine>(v, *params, device, slab_begin, slab_end, data_begin,
+                                    data_end, static_cast<cudaStream_t>(stream));
+    *out = h.release();
+    return SSLIC_OK;
+  });
+}
+
+int sslic_engine_destroy(sslic_engine* e) {
+  return guarded([&] {
+    delete e;
+    return SSLIC_OK;
+  });
+}
+
+int sslic_engine_init(sslic_engine* e) {
+  return guarded([&] {
+    e->e->init(true);
+    return SSLIC_OK;
+  });
+}
+
+int sslic_engine_centers_buffer(sslic_engine* e, double** dev_ptr, int64_t* count) {
+  return guarded([&] {
+    *dev_ptr = e->e->current_centers();
+    *count = e->e->centers_count();
+    return SSLIC_OK;
+  });
+}
+
+int sslic_engine_commit_centers(sslic_engine* e) {
+  return guarded([&] {
+    e->e->commit();
+    return SSLIC_OK;
+  });
+}
+
+int sslic_engine_assign(sslic_engine* e) {
+  return guarded([&] {
+    e->e->assign(true);
+    return SSLIC_OK;
+  });
+}
+
+int sslic_engine_partials(sslic_engine* e, int64_t** dev_ptr, int64_t* count) {
+  return guarded([&] {
+    *dev_ptr = reinterpret_cast<int64_t*>(e->e->partials());
+    *count = e->e->partials_count();
+    return SSLIC_OK;
+  });
+}
+
+int sslic_engine_update(sslic_engine* e) {
+  return guarded([&] {
+    e->e->update();
+    return SSLIC_OK;
+  });
+}
+
+int sslic_engine_iterate(sslic_engine* e, int iterations) {
+  return guarded([&] {
+    for (int i = 0; i < iterations; ++i) {
+      e->e->assign(true);
+      e->e->update();
+    }
+    return SSLIC_OK;
+  });
+}
+
+int sslic_engine_iterations_done(sslic_engine* e) { return e ? e->e->iterations_done() : 0; }
+
+int sslic_engine_residuals(sslic_engine* e, double* host_out) {
+  return guarded([&] {
+    e->e->residuals_to_host(host_out, e->e->iterations_done());
+    return SSLIC_OK;
+  });
+}
+
+int sslic_engine_labels(sslic_engine* e, uint32_t* dev_out) {
+  return guarded([&] {
+    e->e->unpack_labels(dev_out);
+    return SSLIC_OK;
+  });
+}
+
+int sslic_engine_centers(sslic_engine* e, double* host_out) {
+  return guarded([&] {
+    e->e->copy_centers_to_host(host_out);
+    return SSLIC_OK;
+  });
+}
+
+int64_t sslic_engine_undefined_count(sslic_engine* e) {
+  int64_t v = -1;
+  guarded([&] {
+    v = e->e->undefined_count();
+    return SSLIC_OK;
+  });
+  return v;
+}
+
+int64_t sslic_engine_launch_count(sslic_engine* e) { return e ? e->e->launches() : 0; }
+
+int sslic_engine_assign_ms(sslic_engine* e, int i, float* ms_out, int* n_out) {
+  return guarded([&] {
+    if (n_out) *n_out = e->e->assign_calls();
+    if (ms_out) *ms_out = e->e->assign_ms(i);
+    return SSLIC_OK;
+  });
+}
+
+int sslic_engine_set_stats(sslic_engine* e, int on) {
+  return guarded([&] {
+    e->e->set_collect_stats(on != 0);
+    return SSLIC_OK;
+  });
+}
+
+int sslic_engine_eval_stats(sslic_engine* e, double* evals, double* window_evals) {
+  return guarded([&] {
+    e->e->eval_stats(evals, window_evals);
+    return SSLIC_OK;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,107 @@
+// Host-side engine owning the device state of one SLIC run on one slab.
+#pragma once
+
+#include <vector>
+
+#include "common.cuh"
+#include "kernels_exact.cuh"
+
+namespace sslic_b200 {
+
+enum class AssignPath { kExact = 0, kFast = 1 };
+
+class Engine {
+ public:
+  // img.data: DEVICE pointer to planes [data_begin, data_end) of the last
+  // axis (borrowed). force_dist: keep an explicit fp64 DistanceMap.
+  Engine(const sslic_image& img, const sslic_params& p, int device, int64_t slab_begin,
+         int64_t slab_end, int64_t data_begin, int64_t data_end, cudaStream_t stream,
+         bool force_dist = false, int64_t k_override = -1);
+  ~Engine();
+  Engine(const Engine&) = delete;
+  Engine& operator=(const Engine&) = delete;
+
+  // K1 on the owned clusters (zeros elsewhere).
+  void init(bool perturb);
+  // Load a caller-given centre table (host) as the current table.
+  void set_centers_host(const double* h);
+  // Anchors + candidate bins of the current table.
+  void commit();
+  // One map phase: fused assign + accumulate into partials (zeroed first).
+  void assign(bool accumulate = true);
+  // Accumulate only (labels as given).
+  void accumulate_only();
+  // reduce_and_update from partials; pushes the new table; residual on device.
+  void update();
+
+  double* current_centers() const;
+  int64_t centers_count() const { return g_.k * g_.stride; }
+  unsigned long long* partials() const { return acc_; }
+  int64_t partials_count() const { return g_.k * (g_.stride + 1); }
+  uint32_t* label_words() const { return labels_; }
+  double* dists() const { return dists_; }
+  int64_t slab_voxels() const { return (g_.slab_end - g_.slab_begin) * g_.plane; }
+  void unpack_labels(uint32_t* dev_out);
+  void copy_centers_to_host(double* h);
+  void residuals_to_host(double* h, int n);
+  int64_t undefined_count();
+  int64_t out_of_range_count();
+  void eval_stats(double* evals, double* window_evals);
+  // Device time (ms) of the i-th assign kernel launch (CUDA events on stream).
+  float assign_ms(int i);
+  int assign_calls() const { return n_assign_; }
+  void set_value_shift(int s) { shift_ = s; }
+  int value_shift() const { return shift_; }
+  void set_path(AssignPath p) { path_ = p; }
+  // Count candidate evaluations and window volumes in assign() (bench).
+  void set_collect_stats(bool on) { collect_stats_ = on; }
+  AssignPath path() const { return path_; }
+
+  const Geom& geom() const { return g_; }
+  int iterations_done() const { return iter_; }
+  int max_iterations() const { return max_iter_; }
+  bool dist_mode() const { return dist_mode_; }
+  LabelCodec codec() const { return codec_; }
+  int64_t launches() const { return launches_; }
+  cudaStream_t stream() const { return stream_; }
+  int device() const { return device_; }
+
+ private:
+  void launch_check(const char* what);
+  void launch_assign_kernel(bool accumulate);
+  void compute_shift();
+
+  Geom g_{};
+  const void* img_ = nullptr;
+  cudaStream_t stream_ = nullptr;
+  int device_ = 0;
+  int max_iter_ = 0;
+  int iter_ = 0;
+  int shift_ = 0;
+  bool dist_mode_ = false;
+  AssignPath path_ = AssignPath::kExact;
+  bool collect_stats_ = false;
+  LabelCodec codec_{32, 0xffffffffu};
+
+  double* centers_ = nullptr;  // tag mode: (max_iter+1) tables; dist mode: 2 tables
+  int n_tables_ = 0;
+  uint32_t* labels_ = nullptr;
+  double* dists_ = nullptr;
+  unsigned long long* acc_ = nullptr;
+  int* anchors_ = nullptr;
+  int* cell_of_ = nullptr;
+  int* cell_count_ = nullptr;
+  int* cell_start_ = nullptr;
+  int* cursor_ = nullptr;
+  int* items_ = nullptr;
+  void* scan_tmp_ = nullptr;
+  size_t scan_tmp_bytes_ = 0;
+  double* block_partials_ = nullptr;
+  double* residuals_ = nullptr;
+  unsigned long long* counters_ = nullptr;  // [0] undefined, [1] out-of-range, [2] evals, [3] window
+  int64_t launches_ = 0;
+  std::vector<cudaEvent_t> ev_start_, ev_stop_;
+  int n_assign_ = 0;
+};
+
+}  // namespace sslic_b200

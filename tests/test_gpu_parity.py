@@ -1,0 +1,219 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's golden
+outputs and the CPU oracle. Bit-exact for labels, centres and (where the
+reference sums in the same exact integer domain) everything else; residuals
+are compared at rtol 1e-12 because the device reduces the per-cluster squared
+displacements in a fixed tree order instead of the reference's sequential
+(k, i) order."""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, load_cases
+
+pytestmark = pytest.mark.gpu
+
+RES_RTOL = 1e-12
+
+
+def _img(s, data, dims, ch):
+    return s.NDImage(tuple(int(d) for d in dims), int(ch), data)
+
+
+@pytest.mark.parametrize("corpus", ["corpus_acceptance", "corpus_run_slic",
+                                    "corpus_connectivity"])
+def test_run_slic_matches_reference_corpus(sslic, corpus):
+    # acceptance.cpp:96-113 (C1), test_slic.cpp:376-397
+    for i, c in enumerate(load_cases(corpus)):
+        img = _img(sslic, c["data"], c["dims"], c["channels"])
+        p = sslic.SlicParams(grid=[int(g) for g in c["grid"]], weight_m=float(c["weight_m"]))
+        r = sslic.run_slic(img, p)
+        assert np.array_equal(r.labels, c["labels"]), (corpus, i)
+        assert np.array_equal(r.centers.data.reshape(-1), c["centers"].reshape(-1)), (corpus, i)
+        np.testing.assert_allclose(r.residuals, c["residuals"], rtol=RES_RTOL, atol=0)
+
+
+@pytest.mark.parametrize("corpus", ["corpus_acceptance", "corpus_connectivity"])
+def test_enforce_connectivity_matches_reference(sslic, corpus):
+    # acceptance.cpp:115-140 (C2), test_connectivity.cpp:185-216
+    for i, c in enumerate(load_cases(corpus)):
+        p = sslic.SlicParams(grid=[int(g) for g in c["grid"]], weight_m=float(c["weight_m"]))
+        t = sslic.ClusterTable(int(c["channels"]), len(c["dims"]), c["centers"])
+        out = sslic.enforce_connectivity(c["labels"], c["dims"], t, p)
+        assert np.array_equal(out, c["labels_cc"]), (corpus, i)
+
+
+def test_single_pass_bit_exact(sslic):
+    # test_slic.cpp:199-246: labels AND dists bitwise given identical centres.
+    z = np.load(os.path.join(GOLDEN, "single_pass.npz"))
+    img = _img(sslic, z["data"], z["dims"], 1)
+    p = sslic.SlicParams(grid=[6, 6])
+    t = sslic.ClusterTable(1, 2, z["centers"])
+    lab = np.full(144, sslic.UNDEFINED, np.uint32)
+    dist = np.full(144, np.inf)
+    sslic.assign_labels(img, t, p, lab, dist)
+    assert np.array_equal(lab, z["labels"])
+    assert np.array_equal(dist, z["dists"])
+
+
+def test_single_pass_random_centres_bit_exact(sslic, oracle_lib):
+    # Arbitrary (drifted, fractional) centre tables and carried-over state.
+    rng = np.random.default_rng(11)
+    for trial in range(30):
+        rank = int(rng.integers(1, 4))
+        ch = int(rng.integers(1, 4))
+        dims = rng.integers(2, 20, rank)
+        grid = np.array([rng.integers(1, d + 1) for d in dims])
+        data = rng.integers(0, 65535, int(np.prod(dims)) * ch) / 256.0
+        k = int(np.prod([(d + s - 1) // s for d, s in zip(dims, grid)]))
+        cen = np.concatenate([rng.uniform(0, 255, (k, ch)),
+                              np.stack([rng.uniform(-1, d, k) for d in dims], 1)], 1)
+        lab0 = rng.integers(0, k, int(np.prod(dims))).astype(np.uint32)
+        dist0 = rng.uniform(0, 2e4, int(np.prod(dims)))
+        exp_l, exp_d = oracle_lib.assign(data, dims, ch, cen, grid, 7.5, lab0, dist0)
+        img = _img(sslic, data, dims, ch)
+        lab, dist = lab0.copy(), dist0.copy()
+        sslic.assign_labels(img, sslic.ClusterTable(ch, rank, cen),
+                            sslic.SlicParams(grid=list(grid), weight_m=7.5), lab, dist)
+        assert np.array_equal(lab, exp_l), trial
+        assert np.array_equal(dist, exp_d), trial
+
+
+def test_configlike_native_dtypes(sslic):
+    # u8 / u16 / f32 native inputs shaped like BASELINE configs 1-5.
+    for c in load_cases("configlike"):
+        img = _img(sslic, c["data"], c["dims"], c["channels"])
+        p = sslic.SlicParams(grid=[int(g) for g in c["grid"]], weight_m=float(c["weight_m"]),
+                             max_iterations=int(c["iterations"]))
+        r, nxt = sslic.segment(img, p)
+        assert np.array_equal(r.labels, c["labels_cc"]), c["name"]
+        assert nxt >= len(c["centers"])
+        np.testing.assert_allclose(r.centers.data.reshape(-1), c["centers"].reshape(-1),
+                                   rtol=1e-12, atol=1e-12)
+
+
+def test_configlike_pre_connectivity(sslic):
+    for c in load_cases("configlike"):
+        img = _img(sslic, c["data"], c["dims"], c["channels"])
+        p = sslic.SlicParams(grid=[int(g) for g in c["grid"]], weight_m=float(c["weight_m"]),
+                             max_iterations=int(c["iterations"]))
+        r = sslic.run_slic(img, p)
+        assert np.array_equal(r.labels, c["labels"]), c["name"]
+        if c["data"].dtype.kind == "u":
+            # integer intensities: int64 sums are exact -> bitwise centres
+            assert np.array_equal(r.centers.data.reshape(-1), c["centers"].reshape(-1))
+        else:
+            # float32 intensities are summed in 2^-shift fixed point
+            np.testing.assert_allclose(r.centers.data.reshape(-1), c["centers"].reshape(-1),
+                                       rtol=1e-12, atol=1e-12)
+
+
+def test_known_answers(sslic):
+    s = sslic
+    # init_centers (test_slic.cpp:23-45)
+    t = s.init_centers(s.NDImage.zeros((100, 100), 1), s.SlicParams(grid=[50, 50]))
+    assert [tuple(np.rint(r[1:]).astype(int)) for r in t.data] == [(25, 25), (75, 25),
+                                                                   (25, 75), (75, 75)]
+    t = s.init_centers(s.NDImage.zeros((7,), 1), s.SlicParams(grid=[3]))
+    assert list(t.data[:, 1]) == [1.0, 4.0, 6.0]
+    img = s.NDImage((6, 6), 2, np.array([[x, y] for y in range(6) for x in range(6)], float))
+    t = s.init_centers(img, s.SlicParams(grid=[6, 6]))
+    assert t.data[0, 0] == 3.0 and t.data[0, 1] == 3.0
+    with pytest.raises(s.InvalidArgument):
+        s.init_centers(img, s.SlicParams(grid=[7, 6]))
+    # perturb (test_slic.cpp:65-111)
+    z = s.NDImage.zeros((5, 5), 1)
+    t = s.perturb_centers(z, s.init_centers(z, s.SlicParams(grid=[5, 5])))
+    assert tuple(t.data[0, 1:]) == (1.0, 1.0)
+    ridge = s.NDImage((5, 5), 1, [100.0 if x == 2 else 0.0 for y in range(5) for x in range(5)])
+    t = s.perturb_centers(ridge, s.init_centers(ridge, s.SlicParams(grid=[5, 5])))
+    assert tuple(t.data[0, 1:]) == (2.0, 1.0) and t.data[0, 0] == 100.0
+    tiny = s.NDImage.zeros((2, 2), 1)
+    t = s.perturb_centers(tiny, s.init_centers(tiny, s.SlicParams(grid=[1, 1])))
+    assert np.all((t.data[:, 1:] >= 0) & (t.data[:, 1:] < 2))
+    # squared_distance 0 / 100 / 25 (test_slic.cpp:113-129)
+    p = s.SlicParams(grid=[7, 5], weight_m=10.0)
+    assert s.squared_distance([10, 20, 3, 4], [10, 20], [3, 4], p) == 0.0
+    assert s.squared_distance([10, 20, 3, 4], [10, 20], [10, 4], p) == 100.0
+    assert s.squared_distance([50, 10, 5, 2, 2], [53, 14, 5], [2, 2], p) == 25.0
+    # gradient (test_color.cpp:85-106)
+    flat = s.NDImage((5, 5), 1, np.full(25, 3.5))
+    assert np.all(s.gradient_magnitude_sq(flat, [[x, y] for y in range(5)
+                                                 for x in range(5)]) == 0.0)
+    ramp = s.NDImage((5, 4), 1, [float(x) for y in range(4) for x in range(5)])
+    assert s.gradient_magnitude_sq(ramp, [2, 1]) == 1.0
+    assert s.gradient_magnitude_sq(ramp, [1, 2]) == 1.0
+    two = s.NDImage((3, 3), 2, [[float(x), 2.0 * y] for y in range(3) for x in range(3)])
+    assert s.gradient_magnitude_sq(two, [1, 1]) == 5.0
+    with pytest.raises(s.OutOfRange):
+        s.gradient_magnitude_sq(two, [3, 0])
+
+
+def test_assign_covers_window_and_ties(sslic):
+    s = sslic
+    # single cluster claims its whole window (test_slic.cpp:170-179)
+    img = s.NDImage.zeros((8, 8), 1)
+    p = s.SlicParams(grid=[8, 8])
+    lab = np.full(64, s.UNDEFINED, np.uint32)
+    dist = np.full(64, np.inf)
+    s.assign_labels(img, s.init_centers(img, p), p, lab, dist)
+    assert np.all(lab == 0)
+    # equidistant pixel keeps the lower id (test_slic.cpp:181-197)
+    img = s.NDImage.zeros((8, 1), 1)
+    p = s.SlicParams(grid=[4, 1])
+    t = s.ClusterTable(1, 2, [[0.0, 1.0, 0.0], [0.0, 5.0, 0.0]])
+    lab = np.full(8, s.UNDEFINED, np.uint32)
+    dist = np.full(8, np.inf)
+    s.assign_labels(img, t, p, lab, dist)
+    assert lab[3] == 0
+
+
+def test_accumulate_and_reduce(sslic):
+    s = sslic
+    # four constant pixels (test_slic.cpp:250-262)
+    img = s.NDImage((2, 2), 1, np.full(4, 7.0))
+    sums, counts = s.accumulate_region(img, np.zeros(4, np.uint32))
+    assert counts[0] == 4 and list(sums[0]) == [28.0, 2.0, 2.0]
+    # undefined labels are a loud error (test_slic.cpp:272-276)
+    with pytest.raises(s.LogicError):
+        s.accumulate_region(s.NDImage.zeros((2, 2), 1), np.full(4, s.UNDEFINED, np.uint32), k=1)
+    # reduce: single point and empty cluster (test_slic.cpp:304-346)
+    t = s.ClusterTable(1, 2, [[5.0, 2.0, 3.0]])
+    nt, r = s.reduce_and_update(t, [(np.array([[5.0, 2.0, 3.0]]), np.array([1]))])
+    assert list(nt.data[0]) == [5.0, 2.0, 3.0] and r == 0.0
+    t = s.ClusterTable(1, 1, [[1.0, 4.0], [9.0, 8.0]])
+    nt, r = s.reduce_and_update(t, [(np.array([[10.0, 20.0]]), np.array([1]))])
+    assert list(nt.data[0]) == [10.0, 20.0] and list(nt.data[1]) == [9.0, 8.0]
+    assert r == np.sqrt(81.0 + 256.0)
+
+
+def test_uniform_image_and_monotone(sslic, oracle_lib):
+    s = sslic
+    # uniform image converges to the init cells (test_slic.cpp:399-411)
+    r = s.run_slic(s.NDImage((40, 30), 1, np.full(1200, 9.0)), s.SlicParams(grid=[10, 10]))
+    exp = [(x // 10) + 4 * (y // 10) for y in range(30) for x in range(40)]
+    assert list(r.labels) == exp
+    # acceptance C6 (acceptance.cpp:285-302): 4 cells after connectivity
+    res, _ = s.segment(s.NDImage((100, 100), 1, np.full(10000, 42.0)),
+                       s.SlicParams(grid=[50, 50]))
+    exp = [(0 if x < 50 else 1) + (0 if y < 50 else 2) for y in range(100) for x in range(100)]
+    assert list(res.labels) == exp
+    # residual threshold (test_slic.cpp:476-490)
+    rng = np.random.default_rng(606)
+    img = s.NDImage((16, 13), 1, rng.integers(0, 65280, 208) / 256.0)
+    r = s.run_slic(img, s.SlicParams(grid=[4, 4], max_iterations=10,
+                                     residual_threshold=np.finfo(float).max))
+    assert len(r.residuals) == 1
+    r = s.run_slic(img, s.SlicParams(grid=[4, 4], max_iterations=10))
+    assert len(r.residuals) == 10
+
+
+def test_errors(sslic):
+    s = sslic
+    img = s.NDImage.zeros((8, 8), 1)
+    with pytest.raises(s.InvalidArgument):
+        s.run_slic(img, s.SlicParams(grid=[9, 8]))
+    with pytest.raises(s.InvalidArgument):
+        s.run_slic(img, s.SlicParams(grid=[4, 4], weight_m=0.0))
+    with pytest.raises(s.InvalidArgument):
+        s.run_slic(img, s.SlicParams(grid=[4, 4]), workers=0)
