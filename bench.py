@@ -214,6 +214,8 @@ def main():
     params = s.SlicParams(grid=list(grid), weight_m=m, max_iterations=max(total_iters, 1))
     eng = s.Engine(dims, ch, dtype, img.data_ptr(), params, slab=slab, data_range=drange,
                    device=local, stream=stream.cuda_stream)
+    if args.path == "exact":
+        eng.set_exact(True)
 
     def allreduce(t):
         import torch.distributed as tdist
@@ -247,6 +249,7 @@ def main():
     eng.set_stats(True)
     loop.iterate()
     evals, window = eng.eval_stats()
+    ambiguous, overflow = eng.fast_stats()
     eng.set_stats(False)
     undefined = eng.undefined_count()
     if world > 1:
@@ -292,7 +295,9 @@ def main():
         "kernel_ms": amean,
         "kernel_share_of_step": amean * args.steps / ms,
         "algorithmic": {"E_window_evals_per_voxel": E, "flops_per_voxel": fpv,
-                        "bytes_per_voxel": bpv, "evals_performed_per_voxel": evals / nvox},
+                        "bytes_per_voxel": bpv, "evals_performed_per_voxel": evals / nvox,
+                        "fp64_redecided_voxel_frac": ambiguous / nvox,
+                        "crowded_ctas": overflow},
         "hbm_gbs": achieved_gbs, "hbm_peak_gbs": hbm, "hbm_frac": achieved_gbs / hbm,
         "peak_source": f"FP32 = {sm_count} SMs x 128 x 2 x {max_mhz:.0f} MHz "
                        f"(no measured FP32 peak); HBM = MEASURED_PEAKS.json hbm_gbs",

@@ -170,6 +170,12 @@ int64_t sslic_engine_launch_count(sslic_engine* e);
 /* Device time (ms, CUDA events on the engine stream) of the i-th assign
  * kernel launch since creation; *n_out = launches recorded. Synchronizes. */
 int sslic_engine_assign_ms(sslic_engine* e, int i, float* ms_out, int* n_out);
+/* Force the exact fp64 assignment kernel (1) or allow the fast fp32-filter
+ * kernel where supported (0, default). Both produce identical labels. */
+int sslic_engine_set_exact(sslic_engine* e, int exact);
+/* Fast-path statistics of the last assign: voxels re-decided in fp64 and
+ * CTAs that took the crowded-region exact fallback. Synchronizes. */
+int sslic_engine_fast_stats(sslic_engine* e, double* ambiguous, double* overflow_blocks);
 /* Enable counting of candidate evaluations / window volumes in assign. */
 int sslic_engine_set_stats(sslic_engine* e, int on);
 /* Assignment evaluation statistics of the last assign (bench roofline):

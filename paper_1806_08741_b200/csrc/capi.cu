@@ -682,6 +682,21 @@ int sslic_engine_assign_ms(sslic_engine* e, int i, float* ms_out, int* n_out) {
   });
 }
 
+int sslic_engine_set_exact(sslic_engine* e, int exact) {
+  return guarded([&] {
+    const bool fast_ok = fast_path_supported(e->e->geom()) && !e->e->dist_mode();
+    e->e->set_path(exact || !fast_ok ? AssignPath::kExact : AssignPath::kFast);
+    return SSLIC_OK;
+  });
+}
+
+int sslic_engine_fast_stats(sslic_engine* e, double* ambiguous, double* overflow_blocks) {
+  return guarded([&] {
+    e->e->fast_stats(ambiguous, overflow_blocks);
+    return SSLIC_OK;
+  });
+}
+
 int sslic_engine_set_stats(sslic_engine* e, int on) {
   return guarded([&] {
     e->e->set_collect_stats(on != 0);

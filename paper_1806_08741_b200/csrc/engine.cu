@@ -70,9 +70,11 @@ Engine::Engine(const sslic_image& img, const sslic_params& p, int device, int64_
   labels_ = dalloc<uint32_t>(nv, s);
   SSLIC_CUDA_CHECK(cudaMemsetAsync(labels_, 0xff, nv * sizeof(uint32_t), s));
   if (dist_mode_) {
-    dists_ = dalloc<double>(nv, s);
-    // +inf = 0x7ff0000000000000: fill via a tiny kernel-free pattern trick is
-    // not possible with memset; use the unpack kernel's sibling below.
+    dists_ = dalloc<double>(nv, s);  // filled with +inf below (DistanceMap, image.hpp:323)
+  } else {
+    hist32_ = dalloc<float2>((size_t)n_tables_ * g_.k * g_.stride, s);
+    chg_ = dalloc<int>(g_.k, s);
+    SSLIC_CUDA_CHECK(cudaMemsetAsync(chg_, 0, g_.k * sizeof(int), s));
   }
   acc_ = dalloc<unsigned long long>(partials_count(), s);
   anchors_ = dalloc<int>(g_.k * kMaxRank, s);
@@ -93,7 +95,15 @@ Engine::Engine(const sslic_image& img, const sslic_params& p, int device, int64_
     launch_check("fill dists");
   }
   compute_shift();
-  path_ = fast_path_supported(g_) ? AssignPath::kFast : AssignPath::kExact;
+  if (g_.dtype == SSLIC_U8) vmax_ = 255.0;
+  if (g_.dtype == SSLIC_U16) vmax_ = 65535.0;
+  {
+    // absolute fp32 margin for the hi/lo centre split (DESIGN.md error bound)
+    const double e = vmax_ * std::ldexp(1.0, -48);
+    const double M = fast_margin(g_.channels);
+    abs_margin_ = (float)(8.0 * e * e / M + e * e + 1e-37);
+  }
+  path_ = fast_path_supported(g_) && !dist_mode_ ? AssignPath::kFast : AssignPath::kExact;
 }
 
 Engine::~Engine() {
@@ -101,7 +111,7 @@ Engine::~Engine() {
   cudaStream_t s = stream_;
   void* ptrs[] = {centers_, labels_, dists_, acc_, anchors_, cell_of_, cell_count_,
                   cell_start_, cursor_, items_, scan_tmp_, block_partials_, residuals_,
-                  counters_};
+                  counters_, hist32_, chg_};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, s);
   cudaStreamSynchronize(s);
@@ -133,6 +143,7 @@ void Engine::compute_shift() {
   int e = 0;
   if (m > 0.0) std::frexp(m, &e);  // m < 2^e
   shift_ = 40 - e;                  // |v| * 2^shift < 2^40
+  vmax_ = m;
 }
 
 double* Engine::current_centers() const {
@@ -165,6 +176,12 @@ void Engine::commit() {
   launch_check("bin_fill");
   k_bin_sort<<<blocks_for(g_.ncells, 256), 256, 0, s>>>(g_.ncells, cell_start_, items_);
   launch_check("bin_sort");
+  if (!dist_mode_) {
+    const int64_t nc = centers_count();
+    k_split32<<<blocks_for(nc, 256), 256, 0, s>>>(
+        current_centers(), hist32_ + (size_t)iter_ * g_.k * g_.stride, nc);
+    launch_check("split32");
+  }
 }
 
 void Engine::assign(bool accumulate) {
@@ -174,6 +191,7 @@ void Engine::assign(bool accumulate) {
   if (accumulate)
     SSLIC_CUDA_CHECK(cudaMemsetAsync(acc_, 0, partials_count() * sizeof(unsigned long long), s));
   SSLIC_CUDA_CHECK(cudaMemsetAsync(counters_, 0, 4 * sizeof(unsigned long long), s));
+  SSLIC_CUDA_CHECK(cudaMemsetAsync(counters_ + 5, 0, 3 * sizeof(unsigned long long), s));
   const int64_t nv = slab_voxels();
   const double* hist = dist_mode_ ? nullptr : centers_;
   if (collect_stats_) {
@@ -199,9 +217,25 @@ void Engine::launch_assign_kernel(bool accumulate) {
   const int64_t nv = slab_voxels();
   const double* hist = dist_mode_ ? nullptr : centers_;
   if (path_ == AssignPath::kFast && accumulate && !dist_mode_) {
-    launch_fast_assign(g_, img_, current_centers(), hist, anchors_, cell_start_, items_, labels_,
-                       codec_, (uint32_t)iter_, shift_, acc_, counters_,
-                       collect_stats_ ? counters_ + 2 : nullptr, s);
+    FastParams P{};
+    P.g = g_;
+    P.img = img_;
+    P.centers = current_centers();
+    P.history = hist;
+    P.hist32 = hist32_;
+    P.chg = chg_;
+    P.anchors = anchors_;
+    P.cell_start = cell_start_;
+    P.items = items_;
+    P.labels = labels_;
+    P.codec = codec_;
+    P.tag_now = (uint32_t)iter_;
+    P.shift = shift_;
+    P.acc = acc_;
+    P.counters = counters_;
+    P.eval_count = collect_stats_ ? counters_ + 2 : nullptr;
+    P.abs_margin = abs_margin_;
+    launch_fast_assign(P, s);
     launch_check("assign_fast");
     return;
   }
@@ -249,7 +283,7 @@ void Engine::update() {
   const int next_slot = dist_mode_ ? ((iter_ + 1) & 1) : iter_ + 1;
   double* new_c = centers_ + (size_t)next_slot * g_.k * g_.stride;
   const unsigned nb = blocks_for(g_.k, 256);
-  k_update<<<nb, 256, 0, s>>>(g_, shift_, acc_, old_c, new_c, block_partials_);
+  k_update<<<nb, 256, 0, s>>>(g_, shift_, acc_, old_c, new_c, block_partials_, chg_, iter_ + 1);
   launch_check("update");
   k_residual_final<<<1, 1024, 0, s>>>(block_partials_, (int)nb, residuals_ + iter_);
   launch_check("residual");
@@ -296,6 +330,14 @@ float Engine::assign_ms(int i) {
   float ms = 0.f;
   SSLIC_CUDA_CHECK(cudaEventElapsedTime(&ms, ev_start_[i], ev_stop_[i]));
   return ms;
+}
+
+void Engine::fast_stats(double* ambiguous, double* overflow_blocks) {
+  unsigned long long v[2] = {0, 0};
+  SSLIC_CUDA_CHECK(cudaMemcpyAsync(v, counters_ + 5, sizeof(v), cudaMemcpyDeviceToHost, stream_));
+  SSLIC_CUDA_CHECK(cudaStreamSynchronize(stream_));
+  *ambiguous = (double)v[0];
+  *overflow_blocks = (double)v[1];
 }
 
 void Engine::eval_stats(double* evals, double* window_evals) {

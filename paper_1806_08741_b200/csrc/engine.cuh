@@ -5,6 +5,7 @@
 
 #include "common.cuh"
 #include "kernels_exact.cuh"
+#include "kernels_fast.cuh"
 
 namespace sslic_b200 {
 
@@ -47,6 +48,8 @@ class Engine {
   int64_t undefined_count();
   int64_t out_of_range_count();
   void eval_stats(double* evals, double* window_evals);
+  // Fast path: voxels re-decided in fp64, crowded CTAs (last assign).
+  void fast_stats(double* ambiguous, double* overflow_blocks);
   // Device time (ms) of the i-th assign kernel launch (CUDA events on stream).
   float assign_ms(int i);
   int assign_calls() const { return n_assign_; }
@@ -100,6 +103,10 @@ class Engine {
   double* residuals_ = nullptr;
   unsigned long long* counters_ = nullptr;  // [0] undefined, [1] out-of-range, [2] evals, [3] window
   int64_t launches_ = 0;
+  float2* hist32_ = nullptr;  // hi/lo fp32 split of every history table
+  int* chg_ = nullptr;        // per cluster: first table index of its current centre
+  double vmax_ = 0.0;
+  float abs_margin_ = 0.f;
   std::vector<cudaEvent_t> ev_start_, ev_stop_;
   int n_assign_ = 0;
 };

@@ -412,7 +412,7 @@ static __global__ void __launch_bounds__(256) k_accumulate(Geom g, const void* i
 // bit-for-bit).
 // ---------------------------------------------------------------------------
 static __global__ void k_update(Geom g, int shift, const unsigned long long* acc, const double* old_c,
-                         double* new_c, double* block_partials) {
+                         double* new_c, double* block_partials, int* chg, int next_table) {
   const int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   double part = 0.0;
   if (id < g.k) {
@@ -420,6 +420,7 @@ static __global__ void k_update(Geom g, int shift, const unsigned long long* acc
     const long long cnt = a[g.stride];
     const double* o = old_c + id * g.stride;
     double* n = new_c + id * g.stride;
+    bool changed = false;
     if (cnt == 0) {
       for (int i = 0; i < g.stride; ++i) n[i] = o[i];
     } else {
@@ -429,9 +430,12 @@ static __global__ void k_update(Geom g, int shift, const unsigned long long* acc
         const double v = __ddiv_rn(s, dc);
         const double d = __dsub_rn(v, o[i]);
         part = __dadd_rn(part, __dmul_rn(d, d));
+        changed |= __double_as_longlong(v) != __double_as_longlong(o[i]);
         n[i] = v;
       }
     }
+    // chg[k]: first table index from which centre k is bitwise unchanged
+    if (chg && changed) chg[id] = next_table;
   }
   __shared__ double red[256];
   red[threadIdx.x] = part;
