@@ -249,7 +249,7 @@ def main():
     eng.set_stats(True)
     loop.iterate()
     evals, window = eng.eval_stats()
-    ambiguous, overflow = eng.fast_stats()
+    ambiguous, overflow, changed = eng.fast_stats()
     eng.set_stats(False)
     undefined = eng.undefined_count()
     if world > 1:
@@ -297,7 +297,8 @@ def main():
         "algorithmic": {"E_window_evals_per_voxel": E, "flops_per_voxel": fpv,
                         "bytes_per_voxel": bpv, "evals_performed_per_voxel": evals / nvox,
                         "fp64_redecided_voxel_frac": ambiguous / nvox,
-                        "crowded_ctas": overflow},
+                        "crowded_ctas": overflow,
+                        "label_changed_voxel_frac_last_iter": changed / nvox},
         "hbm_gbs": achieved_gbs, "hbm_peak_gbs": hbm, "hbm_frac": achieved_gbs / hbm,
         "peak_source": f"FP32 = {sm_count} SMs x 128 x 2 x {max_mhz:.0f} MHz "
                        f"(no measured FP32 peak); HBM = MEASURED_PEAKS.json hbm_gbs",

@@ -175,7 +175,8 @@ int sslic_engine_assign_ms(sslic_engine* e, int i, float* ms_out, int* n_out);
 int sslic_engine_set_exact(sslic_engine* e, int exact);
 /* Fast-path statistics of the last assign: voxels re-decided in fp64 and
  * CTAs that took the crowded-region exact fallback. Synchronizes. */
-int sslic_engine_fast_stats(sslic_engine* e, double* ambiguous, double* overflow_blocks);
+int sslic_engine_fast_stats(sslic_engine* e, double* ambiguous, double* overflow_blocks,
+                            double* changed);
 /* Enable counting of candidate evaluations / window volumes in assign. */
 int sslic_engine_set_stats(sslic_engine* e, int on);
 /* Assignment evaluation statistics of the last assign (bench roofline):

@@ -122,7 +122,7 @@ def lib():
         "sslic_engine_eval_stats": (C.c_int, [vp, f64p, f64p]),
         "sslic_engine_set_stats": (C.c_int, [vp, C.c_int]),
         "sslic_engine_set_exact": (C.c_int, [vp, C.c_int]),
-        "sslic_engine_fast_stats": (C.c_int, [vp, f64p, f64p]),
+        "sslic_engine_fast_stats": (C.c_int, [vp, f64p, f64p, f64p]),
         "sslic_engine_assign_ms": (C.c_int, [vp, C.c_int, C.POINTER(C.c_float),
                                              C.POINTER(C.c_int)]),
         "sslic_synth_generate": (C.c_int, [C.c_int, C.c_int, i64p, C.c_int, C.c_int, C.c_uint64,
@@ -591,9 +591,11 @@ class Engine:
         _check(lib().sslic_engine_set_exact(self.h, int(exact)))
 
     def fast_stats(self):
-        a, b = C.c_double(), C.c_double()
-        _check(lib().sslic_engine_fast_stats(self.h, C.byref(a), C.byref(b)))
-        return a.value, b.value
+        """(voxels re-decided in fp64, crowded CTAs, voxels whose label value
+        changed) of the last assign (fast path, with set_stats(True))."""
+        a, b, c = C.c_double(), C.c_double(), C.c_double()
+        _check(lib().sslic_engine_fast_stats(self.h, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
 
     def set_stats(self, on: bool = True):
         _check(lib().sslic_engine_set_stats(self.h, int(on)))

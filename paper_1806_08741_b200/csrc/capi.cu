@@ -690,9 +690,10 @@ int sslic_engine_set_exact(sslic_engine* e, int exact) {
   });
 }
 
-int sslic_engine_fast_stats(sslic_engine* e, double* ambiguous, double* overflow_blocks) {
+int sslic_engine_fast_stats(sslic_engine* e, double* ambiguous, double* overflow_blocks,
+                            double* changed) {
   return guarded([&] {
-    e->e->fast_stats(ambiguous, overflow_blocks);
+    e->e->fast_stats(ambiguous, overflow_blocks, changed);
     return SSLIC_OK;
   });
 }

@@ -77,6 +77,8 @@ Engine::Engine(const sslic_image& img, const sslic_params& p, int device, int64_
     SSLIC_CUDA_CHECK(cudaMemsetAsync(chg_, 0, g_.k * sizeof(int), s));
   }
   acc_ = dalloc<unsigned long long>(partials_count(), s);
+  sums_ = dalloc<unsigned long long>(partials_count(), s);
+  SSLIC_CUDA_CHECK(cudaMemsetAsync(sums_, 0, partials_count() * sizeof(unsigned long long), s));
   anchors_ = dalloc<int>(g_.k * kMaxRank, s);
   cell_of_ = dalloc<int>(g_.k, s);
   cell_count_ = dalloc<int>(g_.ncells + 1, s);
@@ -111,7 +113,7 @@ Engine::~Engine() {
   cudaStream_t s = stream_;
   void* ptrs[] = {centers_, labels_, dists_, acc_, anchors_, cell_of_, cell_count_,
                   cell_start_, cursor_, items_, scan_tmp_, block_partials_, residuals_,
-                  counters_, hist32_, chg_};
+                  counters_, hist32_, chg_, sums_};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, s);
   cudaStreamSynchronize(s);
@@ -267,15 +269,6 @@ void Engine::launch_assign_kernel(bool accumulate) {
   launch_check("assign_exact");
 }
 
-void Engine::accumulate_only() {
-  cudaStream_t s = stream_;
-  SSLIC_CUDA_CHECK(cudaMemsetAsync(acc_, 0, partials_count() * sizeof(unsigned long long), s));
-  SSLIC_CUDA_CHECK(cudaMemsetAsync(counters_, 0, 2 * sizeof(unsigned long long), s));
-  k_accumulate<<<blocks_for(slab_voxels(), 256), 256, 0, s>>>(g_, img_, labels_, codec_, shift_,
-                                                              acc_, counters_, counters_ + 1);
-  launch_check("accumulate");
-}
-
 void Engine::update() {
   if (iter_ >= max_iter_) throw Error(SSLIC_EINVAL, "engine: all iterations already done");
   cudaStream_t s = stream_;
@@ -283,7 +276,8 @@ void Engine::update() {
   const int next_slot = dist_mode_ ? ((iter_ + 1) & 1) : iter_ + 1;
   double* new_c = centers_ + (size_t)next_slot * g_.k * g_.stride;
   const unsigned nb = blocks_for(g_.k, 256);
-  k_update<<<nb, 256, 0, s>>>(g_, shift_, acc_, old_c, new_c, block_partials_, chg_, iter_ + 1);
+  k_update<<<nb, 256, 0, s>>>(g_, shift_, acc_, sums_, old_c, new_c, block_partials_, chg_,
+                              iter_ + 1);
   launch_check("update");
   k_residual_final<<<1, 1024, 0, s>>>(block_partials_, (int)nb, residuals_ + iter_);
   launch_check("residual");
@@ -332,12 +326,13 @@ float Engine::assign_ms(int i) {
   return ms;
 }
 
-void Engine::fast_stats(double* ambiguous, double* overflow_blocks) {
-  unsigned long long v[2] = {0, 0};
+void Engine::fast_stats(double* ambiguous, double* overflow_blocks, double* changed) {
+  unsigned long long v[3] = {0, 0, 0};
   SSLIC_CUDA_CHECK(cudaMemcpyAsync(v, counters_ + 5, sizeof(v), cudaMemcpyDeviceToHost, stream_));
   SSLIC_CUDA_CHECK(cudaStreamSynchronize(stream_));
   *ambiguous = (double)v[0];
   *overflow_blocks = (double)v[1];
+  if (changed) *changed = (double)v[2];
 }
 
 void Engine::eval_stats(double* evals, double* window_evals) {

@@ -31,7 +31,6 @@ class Engine {
   // One map phase: fused assign + accumulate into partials (zeroed first).
   void assign(bool accumulate = true);
   // Accumulate only (labels as given).
-  void accumulate_only();
   // reduce_and_update from partials; pushes the new table; residual on device.
   void update();
 
@@ -49,7 +48,7 @@ class Engine {
   int64_t out_of_range_count();
   void eval_stats(double* evals, double* window_evals);
   // Fast path: voxels re-decided in fp64, crowded CTAs (last assign).
-  void fast_stats(double* ambiguous, double* overflow_blocks);
+  void fast_stats(double* ambiguous, double* overflow_blocks, double* changed);
   // Device time (ms) of the i-th assign kernel launch (CUDA events on stream).
   float assign_ms(int i);
   int assign_calls() const { return n_assign_; }
@@ -90,7 +89,8 @@ class Engine {
   int n_tables_ = 0;
   uint32_t* labels_ = nullptr;
   double* dists_ = nullptr;
-  unsigned long long* acc_ = nullptr;
+  unsigned long long* acc_ = nullptr;   // this iteration's int64 deltas (allreduced)
+  unsigned long long* sums_ = nullptr;  // persistent exact per-cluster sums
   int* anchors_ = nullptr;
   int* cell_of_ = nullptr;
   int* cell_count_ = nullptr;

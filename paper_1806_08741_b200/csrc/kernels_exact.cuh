@@ -216,21 +216,26 @@ static __global__ void k_bin_sort(int64_t ncells, const int* cell_start, int* it
 // per-cluster int64 accumulator acc[label*(stride+1) + ...] (ClusterAccumulatorMap,
 // slic.hpp:108-149). Integer sums are exact and associative, so the result is
 // independent of the order and of the slab/GPU decomposition.
+static __device__ inline void count_undefined(bool undef, unsigned long long* undefined_count) {
+  const unsigned full = __activemask();
+  const unsigned undef_mask = __ballot_sync(full, undef);
+  if (undef_mask && (threadIdx.x & 31) == __ffs(undef_mask) - 1)
+    atomicAdd(undefined_count, (unsigned long long)__popc(undef_mask));
+}
+
+// sign = +1 adds the voxel's joint vector to cluster `label`, -1 removes it
+// (delta accumulation: exact because the sums are integers).
 static __device__ inline void warp_accumulate(const Geom& g, int shift, uint32_t label, bool valid,
-                                       const void* img, int64_t di, const int64_t* coord,
-                                       unsigned long long* acc,
-                                       unsigned long long* undefined_count) {
+                                              int sign, const void* img, int64_t di,
+                                              const int64_t* coord, unsigned long long* acc) {
   const unsigned full = __activemask();
   const int lane = threadIdx.x & 31;
-  const bool undef = valid && label == kUndefined;
-  const unsigned undef_mask = __ballot_sync(full, undef);
-  if (undef_mask && lane == __ffs(undef_mask) - 1)
-    atomicAdd(undefined_count, (unsigned long long)__popc(undef_mask));
-  unsigned todo = __ballot_sync(full, valid && !undef);
+  valid = valid && label != kUndefined;
+  unsigned todo = __ballot_sync(full, valid);
   while (todo) {
     const int leader = __ffs(todo) - 1;
     const uint32_t lab = __shfl_sync(full, label, leader);
-    const bool mine = valid && !undef && label == lab;
+    const bool mine = valid && label == lab;
     const unsigned grp = __ballot_sync(full, mine);
     unsigned long long* dst = acc + (uint64_t)lab * (g.stride + 1);
     for (int i = 0; i <= g.stride; ++i) {
@@ -239,6 +244,7 @@ static __device__ inline void warp_accumulate(const Geom& g, int shift, uint32_t
         if (i < g.channels) v = to_fixed(load_value(img, g.dtype, di + i), shift);
         else if (i < g.stride) v = coord[i - g.channels];
         else v = 1;
+        v *= sign;
       }
       for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(full, v, o);
       if (lane == leader && v != 0) atomicAdd(dst + i, (unsigned long long)v);
@@ -268,7 +274,7 @@ static __global__ void __launch_bounds__(256) k_assign_exact(
   int64_t coord[kMaxRank] = {0, 0, 0, 0};
   int64_t di = 0;
   uint32_t word = kUndefined;
-  uint32_t out_label = kUndefined;
+  uint32_t out_label = kUndefined, old_label = kUndefined;
   unsigned evals = 0;
   if (valid) {
     int64_t rem = off;
@@ -338,6 +344,7 @@ static __global__ void __launch_bounds__(256) k_assign_exact(
     }
 
     word = labels[li];
+    old_label = codec.label(word);
     double d_old;
     if (DIST) {
       d_old = dists[li];
@@ -367,7 +374,14 @@ static __global__ void __launch_bounds__(256) k_assign_exact(
     }
     out_label = codec.label(word);
   }
-  if (ACC) warp_accumulate(g, shift, out_label, valid, img, di, coord, acc, undefined_count);
+  if (ACC) {
+    // delta accumulation into the persistent integer sums: only voxels whose
+    // label value changed contribute (+ new cluster, - old cluster).
+    count_undefined(valid && out_label == kUndefined, undefined_count);
+    const bool changed = valid && out_label != old_label;
+    warp_accumulate(g, shift, out_label, changed, +1, img, di, coord, acc);
+    warp_accumulate(g, shift, old_label, changed, -1, img, di, coord, acc);
+  }
   if (eval_count) {
     unsigned s = evals;
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -402,7 +416,8 @@ static __global__ void __launch_bounds__(256) k_accumulate(Geom g, const void* i
       ok = false;
     }
   }
-  warp_accumulate(g, shift, lab, ok, img, di, coord, acc, undefined_count);
+  count_undefined(ok && lab == kUndefined, undefined_count);
+  warp_accumulate(g, shift, lab, ok, +1, img, di, coord, acc);
 }
 
 // ---------------------------------------------------------------------------
@@ -411,12 +426,16 @@ static __global__ void __launch_bounds__(256) k_accumulate(Geom g, const void* i
 // (deterministic; the reference's sequential (k, i) order is not reproduced
 // bit-for-bit).
 // ---------------------------------------------------------------------------
-static __global__ void k_update(Geom g, int shift, const unsigned long long* acc, const double* old_c,
-                         double* new_c, double* block_partials, int* chg, int next_table) {
+static __global__ void k_update(Geom g, int shift, const unsigned long long* delta,
+                                unsigned long long* sums, const double* old_c, double* new_c,
+                                double* block_partials, int* chg, int next_table) {
   const int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   double part = 0.0;
   if (id < g.k) {
-    const long long* a = reinterpret_cast<const long long*>(acc) + id * (g.stride + 1);
+    // persistent exact integer sums += this iteration's (allreduced) deltas
+    long long* a = reinterpret_cast<long long*>(sums) + id * (g.stride + 1);
+    const long long* dl = reinterpret_cast<const long long*>(delta) + id * (g.stride + 1);
+    for (int i = 0; i <= g.stride; ++i) a[i] += dl[i];
     const long long cnt = a[g.stride];
     const double* o = old_c + id * g.stride;
     double* n = new_c + id * g.stride;

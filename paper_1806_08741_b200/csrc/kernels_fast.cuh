@@ -1,14 +1,16 @@
-// K2 fast path: fused assign + accumulate for rank 2/3, 1..4 channels,
+// K2 fast path: fused assign + delta-accumulate for rank 2/3, 1..4 channels,
 // u8/u16/f32 volumes (configs 1-5). See DESIGN.md "K2".
 //
 // Work decomposition: one CTA per cell-aligned region (R_a = f_a * S_a voxels
 // per axis). The region's candidate clusters are exactly those binned in the
-// anchor cells within one cell of the region (any drift); they
-// are staged once in shared memory together with per-axis spatial tables
-// sx[j][x] = m^2 ((c_x - x)/S_x)^2 (or +inf outside cluster j's window, which
-// folds the window test into the arithmetic). Each warp sweeps 8x4x4 voxel
-// boxes (16x... in 2D), each lane 4 consecutive voxels along x, against the
-// candidates covering its box.
+// anchor cells within one cell of the region (any drift). Each
+// candidate is staged once in shared memory as one record
+//   [ (c_hi, c_hi, c_lo, c_lo) per channel | sx[RXp] | (sy,sy)[RY] | (sz,sz)[RZ] ]
+// where s_a[x] = m^2 ((c_a - x)/S_a)^2 or +inf outside the cluster's window,
+// which folds the window test into the arithmetic. Each warp sweeps 8x4x4
+// voxel boxes (8x16 in 2D), each lane 4 consecutive voxels along x, against
+// the candidates covering its box, two candidates per step with paired
+// fp32x2 arithmetic and 3-input integer min/max.
 //
 // Exactness: the bulk distance evaluations run in fp32 (hi/lo split centre
 // intensities, FMA allowed) with a rigorous error bound; the per-voxel argmin
@@ -18,11 +20,12 @@
 // squared_distance_raw (slic.hpp:156-171) and the lexicographic (D, k) rule,
 // so labels are bit-identical to the reference.
 //
-// Accumulation: warp-level aggregation of equal labels (u32 reductions; f32
-// intensities as 2^-shift fixed point split in three 16/32-bit lanes), CTA
-// shared-memory int64 slots per candidate, one global int64 atomic per
-// (cluster, component) per CTA at the end. Stale labels outside the region's
-// candidates go straight to global atomics.
+// Accumulation: the per-cluster sums are exact integers, so the kernel only
+// emits DELTAS for voxels whose label value changed (+ new cluster, - old
+// cluster); the engine keeps the running sums (k_update). Deltas are
+// warp-aggregated per label (u32 reductions; f32 intensities as 2^-shift
+// fixed point in three lanes), summed in CTA shared-memory int64 slots per
+// candidate, and flushed with one global atomic per (cluster, component).
 #pragma once
 
 #include "common.cuh"
@@ -49,10 +52,10 @@ struct FastParams {
   LabelCodec codec;
   uint32_t tag_now;
   int shift;
-  unsigned long long* acc;
-  unsigned long long* counters;  // [0] undefined, [5] ambiguous (stats), [6] overflow blocks
+  unsigned long long* acc;       // int64 deltas
+  unsigned long long* counters;  // [0] undefined, [5] fp64 re-decided, [6] crowded, [7] changed
   unsigned long long* eval_count;
-  int R[3];           // region extent per axis (3D; R[2] = 1 in 2D)
+  int R[3];           // region extent per axis (R[2] = 1 in 2D)
   int nreg[3];        // regions per axis (z counts only the slab)
   int64_t reg_z0;     // first global z plane of region row 0
   float margin;       // relative fp32 decision margin
@@ -67,44 +70,60 @@ struct BoxShape {
 struct alignas(16) FastSmem {
   int n_cand;
   int overflow;
+  int rs;  // record stride in floats
+  int pad;
   int id[kFastMaxCand];
   int anc[kFastMaxCand][3];
-  unsigned char wl[kFastThreads / 32][kFastMaxCand];
+  unsigned short wl[kFastThreads / 32][kFastMaxCand + 2];   // record offsets (floats)
+  unsigned char wj[kFastThreads / 32][kFastMaxCand + 2];    // candidate slots
 };
+
+// ---- fp32x2 (sm_100a paired FP32) --------------------------------------------
+typedef unsigned long long f2;
+__device__ __forceinline__ f2 pk2(float lo, float hi) {
+  f2 r;
+  asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void up2(f2 v, float& lo, float& hi) {
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ f2 add2(f2 a, f2 b) {
+  f2 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2 sub2(f2 a, f2 b) {
+  f2 r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
+  f2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
 
 __device__ __forceinline__ uint32_t fkey(float d, uint32_t j) {
   return (__float_as_uint(d) & ~7u) | j;
 }
 __device__ __forceinline__ float kval(uint32_t key) { return __uint_as_float(key & ~7u); }
-
-template <typename T>
-__device__ __forceinline__ float to_f(T v) { return (float)v; }
+__device__ __forceinline__ uint32_t min3u(uint32_t a, uint32_t b, uint32_t c) {
+  return min(min(a, b), c);
+}
 
 // Exact per-voxel decision over the region's candidate list (fp64, the
-// reference arithmetic). Returns the new label word and the winner's slot.
-__device__ inline uint32_t exact_region_voxel(const FastParams& P, const FastSmem& sm,
-                                              const int64_t* coord, int64_t di, uint32_t word,
-                                              bool full, int jstar, int* slot_out) {
+// reference arithmetic). full: lexicographic (D, k) argmin over all covering
+// candidates; else only the fp32-certain winner jstar is re-evaluated.
+static __device__ __noinline__ uint32_t exact_region_voxel(const FastParams& P, const FastSmem& sm,
+                                                    int64_t x, int64_t y, int64_t z, int64_t di,
+                                                    uint32_t word, bool full, int jstar) {
   const Geom& g = P.g;
+  const int64_t coord[kMaxRank] = {x, y, z, 0};
   double pix[4];
   for (int c = 0; c < g.channels; ++c) pix[c] = load_value(P.img, g.dtype, di + c);
   double best_d = kInf;
   uint32_t best_k = kUndefined;
-  int best_j = -1;
-  auto dist_of = [&](const double* ctr) {
-    double color = 0.0;
-    for (int c = 0; c < g.channels; ++c) {
-      const double d = __dsub_rn(ctr[c], pix[c]);
-      color = __dadd_rn(color, __dmul_rn(d, d));
-    }
-    double spatial = 0.0;
-    for (int a = 0; a < g.rank; ++a) {
-      const double d =
-          __ddiv_rn(__dsub_rn(ctr[g.channels + a], (double)coord[a]), (double)g.grid[a]);
-      spatial = __dadd_rn(spatial, __dmul_rn(d, d));
-    }
-    return __dadd_rn(color, __dmul_rn(g.m_sq, spatial));
-  };
   if (full) {
     for (int j = 0; j < sm.n_cand; ++j) {
       bool covered = true;
@@ -114,28 +133,102 @@ __device__ inline uint32_t exact_region_voxel(const FastParams& P, const FastSme
       }
       if (!covered) continue;
       const uint32_t kid = (uint32_t)sm.id[j];
-      const double d = dist_of(P.centers + (int64_t)kid * g.stride);
+      const double d = exact_distance(P.centers + (int64_t)kid * g.stride, pix, coord, g);
       if (d < best_d || (d == best_d && kid < best_k)) {
         best_d = d;
         best_k = kid;
-        best_j = j;
       }
     }
   } else {
-    best_j = jstar;
     best_k = (uint32_t)sm.id[jstar];
-    best_d = dist_of(P.centers + (int64_t)best_k * g.stride);
+    best_d = exact_distance(P.centers + (int64_t)best_k * g.stride, pix, coord, g);
   }
   double d_old = kInf;
   if (word != kUndefined)
-    d_old = dist_of(P.history +
-                    ((int64_t)P.codec.tag(word) * g.k + P.codec.label(word)) * g.stride);
-  if (best_j >= 0 && best_d < d_old) {
-    *slot_out = best_j;
-    return P.codec.pack(best_k, P.tag_now);
-  }
-  *slot_out = -2;  // unchanged: caller resolves the slot of the old label
+    d_old = exact_distance(
+        P.history + ((int64_t)P.codec.tag(word) * g.k + P.codec.label(word)) * g.stride, pix,
+        coord, g);
+  if (best_k != kUndefined && best_d < d_old) return P.codec.pack(best_k, P.tag_now);
   return word;
+}
+
+// Crowded region (more than kFastMaxCand candidates): generic exact scan.
+template <int RANK, int C>
+__device__ __noinline__ void crowded_region(const FastParams& P, const int64_t* org,
+                                            const int64_t* hi, int64_t zlo, int64_t zhi) {
+  const Geom& g = P.g;
+  const int RX = P.R[0], RY = P.R[1], RZ = P.R[2];
+  const int64_t nvox = (int64_t)RX * RY * (RANK == 3 ? RZ : 1);
+  for (int64_t base = 0; base < nvox; base += kFastThreads) {
+    const int64_t i = base + threadIdx.x;
+    int64_t coord[kMaxRank] = {0, 0, 0, 0};
+    coord[0] = org[0] + i % RX;
+    coord[1] = org[1] + (i / RX) % RY;
+    coord[2] = RANK == 3 ? org[2] + i / ((int64_t)RX * RY) : 0;
+    const bool valid = i < nvox && coord[0] <= hi[0] && coord[1] <= hi[1] &&
+                       (RANK == 2 || (coord[2] >= zlo && coord[2] <= zhi));
+    uint32_t lab = kUndefined, old = kUndefined;
+    int64_t di = 0;
+    if (valid) {
+      const int64_t off = coord[0] + coord[1] * g.strides[1] + coord[2] * g.strides[2];
+      const int64_t li = off - g.slab_begin * g.plane;
+      di = data_index(g, off);
+      uint32_t word = P.labels[li];
+      old = P.codec.label(word);
+      double pix[4];
+      for (int c = 0; c < C; ++c) pix[c] = load_value(P.img, g.dtype, di + c);
+      double best_d = kInf;
+      uint32_t best_k = kUndefined;
+      int64_t clo[3], chi[3], cc[3];
+      for (int a = 0; a < 3; ++a) {
+        if (a < RANK) {
+          const int64_t xc = coord[a] / g.grid[a];
+          clo[a] = xc > 0 ? xc - 1 : 0;
+          chi[a] = xc + 1 < g.cells[a] ? xc + 1 : g.cells[a] - 1;
+        } else {
+          clo[a] = chi[a] = 0;
+        }
+        cc[a] = clo[a];
+      }
+      for (;;) {
+        const int64_t cell = (cc[2] * g.cells[1] + cc[1]) * g.cells[0] + cc[0];
+        for (int it = P.cell_start[cell]; it < P.cell_start[cell + 1]; ++it) {
+          const int kid = P.items[it];
+          bool covered = true;
+          for (int a = 0; a < RANK; ++a) {
+            const int64_t dx = coord[a] - P.anchors[kid * kMaxRank + a];
+            if (dx < -g.grid[a] || dx > g.grid[a]) covered = false;
+          }
+          if (!covered) continue;
+          const double d = exact_distance(P.centers + (int64_t)kid * g.stride, pix, coord, g);
+          if (d < best_d || (d == best_d && (uint32_t)kid < best_k)) {
+            best_d = d;
+            best_k = (uint32_t)kid;
+          }
+        }
+        int a = 0;
+        for (; a < RANK; ++a) {
+          if (++cc[a] <= chi[a]) break;
+          cc[a] = clo[a];
+        }
+        if (a == RANK) break;
+      }
+      double d_old = kInf;
+      if (word != kUndefined)
+        d_old = exact_distance(
+            P.history + ((int64_t)P.codec.tag(word) * g.k + P.codec.label(word)) * g.stride, pix,
+            coord, g);
+      if (best_d < d_old) {
+        word = P.codec.pack(best_k, P.tag_now);
+        P.labels[li] = word;
+      }
+      lab = P.codec.label(word);
+    }
+    count_undefined(valid && lab == kUndefined, P.counters);
+    const bool changed = valid && lab != old;
+    warp_accumulate(g, P.shift, lab, changed, +1, P.img, di, coord, P.acc);
+    warp_accumulate(g, P.shift, old, changed, -1, P.img, di, coord, P.acc);
+  }
 }
 
 template <int RANK, int C, typename T>
@@ -143,20 +236,16 @@ __global__ void __launch_bounds__(kFastThreads) k_assign_fast(FastParams P) {
   using Box = BoxShape<RANK>;
   constexpr int kStride = C + RANK;
   constexpr int kComp = kStride + 1;
+  constexpr int kHdr = 4 * C;  // (hi, hi, lo, lo) per channel
   const Geom& g = P.g;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   FastSmem& sm = *reinterpret_cast<FastSmem*>(smem_raw);
-  const int RX = P.R[0], RY = P.R[1], RZ = P.R[2];
+  const int RX = P.R[0], RY = P.R[1], RZ = RANK == 3 ? P.R[2] : 1;
   const int RXp = (RX + 3) & ~3;
-  float* cvh = reinterpret_cast<float*>(smem_raw + sizeof(FastSmem));  // [cand][C]
-  float* cvl = cvh + kFastMaxCand * C;
-  float* sx = cvl + kFastMaxCand * C;                                   // [cand][RXp]
-  float* sy = sx + kFastMaxCand * RXp;                                  // [cand][RY]
-  float* sz = sy + kFastMaxCand * RY;                                   // [cand][RZ]
+  const int RS = (kHdr + RXp + 2 * RY + (RANK == 3 ? 2 * RZ : 0) + 3) & ~3;
+  float* rec = reinterpret_cast<float*>(smem_raw + sizeof(FastSmem));  // [cand+1][RS]
   unsigned long long* accs =
-      reinterpret_cast<unsigned long long*>(sz + kFastMaxCand * (RANK == 3 ? RZ : 1));
-  // accs may be misaligned for 8-byte access: align up
-  accs = reinterpret_cast<unsigned long long*>((reinterpret_cast<uintptr_t>(accs) + 7) & ~uintptr_t(7));
+      reinterpret_cast<unsigned long long*>(rec + (size_t)(kFastMaxCand + 1) * RS);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // ---- region ----
@@ -166,18 +255,17 @@ __global__ void __launch_bounds__(kFastThreads) k_assign_fast(FastParams P) {
   const int ryi = (int)(rb % P.nreg[1]);
   rb /= P.nreg[1];
   const int rzi = (int)rb;
-  int64_t org[3] = {(int64_t)rxi * RX, (int64_t)ryi * RY,
-                    RANK == 3 ? P.reg_z0 + (int64_t)rzi * RZ : 0};
-  int64_t hi[3];  // inclusive last coordinate of the region inside the image
-  hi[0] = min(org[0] + RX, g.dims[0]) - 1;
-  hi[1] = min(org[1] + RY, g.dims[1]) - 1;
-  hi[2] = RANK == 3 ? min(org[2] + RZ, g.dims[2]) - 1 : 0;
+  const int64_t org[3] = {(int64_t)rxi * RX, (int64_t)ryi * RY,
+                          RANK == 3 ? P.reg_z0 + (int64_t)rzi * RZ : 0};
+  const int64_t hi[3] = {min(org[0] + RX, g.dims[0]) - 1, min(org[1] + RY, g.dims[1]) - 1,
+                         RANK == 3 ? min(org[2] + RZ, g.dims[2]) - 1 : 0};
   const int64_t zlo = RANK == 3 ? max(org[2], g.slab_begin) : 0;
   const int64_t zhi = RANK == 3 ? min(hi[2], g.slab_end - 1) : 0;
 
   // ---- gather candidates (warp 0) ----
   if (warp == 0) {
     int clo[3], chi[3], nc = 1;
+#pragma unroll
     for (int a = 0; a < 3; ++a) {
       if (a < RANK) {
         const int64_t lo_a = a == 2 ? zlo : org[a];
@@ -219,99 +307,39 @@ __global__ void __launch_bounds__(kFastThreads) k_assign_fast(FastParams P) {
   }
   __syncthreads();
   const int n = sm.n_cand;
-
   if (sm.overflow) {
-    // Crowded region (heavy drift): exact generic per-voxel scan.
     if (tid == 0) atomicAdd(P.counters + 6, 1ull);
-    const int64_t nvox = (int64_t)RX * RY * (RANK == 3 ? RZ : 1);
-    for (int64_t base = 0; base < nvox; base += kFastThreads) {
-      const int64_t i = base + tid;
-      int64_t coord[kMaxRank] = {0, 0, 0, 0};
-      coord[0] = org[0] + i % RX;
-      coord[1] = org[1] + (i / RX) % RY;
-      coord[2] = RANK == 3 ? org[2] + i / ((int64_t)RX * RY) : 0;
-      const bool valid = i < nvox && coord[0] <= hi[0] && coord[1] <= hi[1] &&
-                         (RANK == 2 || (coord[2] >= zlo && coord[2] <= zhi));
-      uint32_t lab = kUndefined;
-      int64_t di = 0;
-      if (valid) {
-        const int64_t off = coord[0] + coord[1] * g.strides[1] + coord[2] * g.strides[2];
-        const int64_t li = off - g.slab_begin * g.plane;
-        di = data_index(g, off);
-        uint32_t word = P.labels[li];
-        // generic candidate scan over the 3^rank anchor-cell hood
-        double pix[4];
-        for (int c = 0; c < C; ++c) pix[c] = load_value(P.img, g.dtype, di + c);
-        double best_d = kInf;
-        uint32_t best_k = kUndefined;
-        int64_t clo[3], chi[3], cc[3];
-        for (int a = 0; a < 3; ++a) {
-          if (a < RANK) {
-            const int64_t xc = coord[a] / g.grid[a];
-            clo[a] = xc > 0 ? xc - 1 : 0;
-            chi[a] = xc + 1 < g.cells[a] ? xc + 1 : g.cells[a] - 1;
-          } else {
-            clo[a] = chi[a] = 0;
-          }
-          cc[a] = clo[a];
-        }
-        for (;;) {
-          const int64_t cell = (cc[2] * g.cells[1] + cc[1]) * g.cells[0] + cc[0];
-          for (int it = P.cell_start[cell]; it < P.cell_start[cell + 1]; ++it) {
-            const int kid = P.items[it];
-            bool covered = true;
-            for (int a = 0; a < RANK; ++a) {
-              const int64_t dx = coord[a] - P.anchors[kid * kMaxRank + a];
-              if (dx < -g.grid[a] || dx > g.grid[a]) covered = false;
-            }
-            if (!covered) continue;
-            const double d = exact_distance(P.centers + (int64_t)kid * g.stride, pix, coord, g);
-            if (d < best_d || (d == best_d && (uint32_t)kid < best_k)) {
-              best_d = d;
-              best_k = (uint32_t)kid;
-            }
-          }
-          int a = 0;
-          for (; a < RANK; ++a) {
-            if (++cc[a] <= chi[a]) break;
-            cc[a] = clo[a];
-          }
-          if (a == RANK) break;
-        }
-        double d_old = kInf;
-        if (word != kUndefined)
-          d_old = exact_distance(
-              P.history + ((int64_t)P.codec.tag(word) * g.k + P.codec.label(word)) * g.stride,
-              pix, coord, g);
-        if (best_d < d_old) {
-          word = P.codec.pack(best_k, P.tag_now);
-          P.labels[li] = word;
-        }
-        lab = P.codec.label(word);
-      }
-      warp_accumulate(g, P.shift, lab, valid, P.img, di, coord, P.acc, P.counters);
-    }
+    crowded_region<RANK, C>(P, org, hi, zlo, zhi);
     return;
   }
 
-  // ---- stage candidates: centres (hi/lo fp32), anchors, spatial tables ----
-  for (int j = tid; j < n; j += kFastThreads) {
-    const int kid = sm.id[j];
-    const double* ctr = P.centers + (int64_t)kid * g.stride;
-    for (int c = 0; c < C; ++c) {
-      const float h = __double2float_rn(ctr[c]);
-      cvh[j * C + c] = h;
-      cvl[j * C + c] = __double2float_rn(ctr[c] - (double)h);
+  // ---- stage candidate records (+ one all-inf padding record at slot n) ----
+  for (int j = tid; j <= n; j += kFastThreads) {
+    float* r = rec + (size_t)j * RS;
+    if (j < n) {
+      const int kid = sm.id[j];
+      const double* ctr = P.centers + (int64_t)kid * g.stride;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const float h = __double2float_rn(ctr[c]);
+        const float l = __double2float_rn(ctr[c] - (double)h);
+        r[4 * c] = h;
+        r[4 * c + 1] = h;
+        r[4 * c + 2] = l;
+        r[4 * c + 3] = l;
+      }
+#pragma unroll
+      for (int a = 0; a < 3; ++a) sm.anc[j][a] = a < RANK ? P.anchors[kid * kMaxRank + a] : 0;
+    } else {
+#pragma unroll
+      for (int c = 0; c < 4 * C; ++c) r[c] = 0.f;
     }
-    for (int a = 0; a < 3; ++a) sm.anc[j][a] = a < RANK ? P.anchors[kid * kMaxRank + a] : 0;
   }
-  for (int j = 0; j < n; ++j)
-    for (int i = tid; i < kComp; i += kFastThreads) accs[j * kComp + i] = 0ull;
+  for (int i = tid; i < n * kComp; i += kFastThreads) accs[i] = 0ull;
   __syncthreads();
   {
-    const int RZt = RANK == 3 ? RZ : 0;
-    const int per = RX + RY + RZt;
-    for (int e = tid; e < n * per; e += kFastThreads) {
+    const int per = RX + RY + (RANK == 3 ? RZ : 0);
+    for (int e = tid; e < (n + 1) * per; e += kFastThreads) {
       const int j = e / per;
       int r = e - j * per, a = 0;
       if (r >= RX) {
@@ -322,18 +350,28 @@ __global__ void __launch_bounds__(kFastThreads) k_assign_fast(FastParams P) {
           a = 2;
         }
       }
-      const int64_t x = org[a] + r;
-      const int kid = sm.id[j];
-      const double cpos = P.centers[(int64_t)kid * g.stride + C + a];
-      const int64_t dx = x - sm.anc[j][a];
       float v = kInf;
-      if (dx >= -g.grid[a] && dx <= g.grid[a]) {
-        const double t = (cpos - (double)x) / (double)g.grid[a];
-        v = __double2float_rn(g.m_sq * (t * t));
+      if (j < n) {
+        const int64_t x = (a == 0 ? org[0] : (a == 1 ? org[1] : org[2])) + r;
+        const int kid = sm.id[j];
+        const int an = a == 0 ? sm.anc[j][0] : (a == 1 ? sm.anc[j][1] : sm.anc[j][2]);
+        const int s = g.grid[a];
+        const int64_t dx = x - an;
+        if (dx >= -s && dx <= s) {
+          const double t = (P.centers[(int64_t)kid * g.stride + C + a] - (double)x) / (double)s;
+          v = __double2float_rn(g.m_sq * (t * t));
+        }
       }
-      if (a == 0) sx[j * RXp + r] = v;
-      else if (a == 1) sy[j * RY + r] = v;
-      else sz[j * RZ + r] = v;
+      float* rj = rec + (size_t)j * RS + kHdr;
+      if (a == 0) {
+        rj[r] = v;
+      } else if (a == 1) {
+        rj[RXp + 2 * r] = v;
+        rj[RXp + 2 * r + 1] = v;
+      } else {
+        rj[RXp + 2 * RY + 2 * r] = v;
+        rj[RXp + 2 * RY + 2 * r + 1] = v;
+      }
     }
   }
   __syncthreads();
@@ -348,12 +386,12 @@ __global__ void __launch_bounds__(kFastThreads) k_assign_fast(FastParams P) {
   const float M = P.margin;
   const float A = P.abs_margin;
   const float fscale = ldexpf(1.0f, P.shift);
+  unsigned n_changed = 0, n_redecided = 0, n_evals = 0;
 
   for (int b = warp; b < nbox; b += kFastThreads / 32) {
     const int bx = b % nbx, by = (b / nbx) % nby, bz = b / (nbx * nby);
     const int lx0 = bx * Box::X + 4 * xq, ly = by * Box::Y + yq, lz = bz * Box::Z + zq;
     const int64_t gx0 = org[0] + lx0, gy = org[1] + ly, gz = org[2] + lz;
-    // box bounds (global, clipped) for the warp's candidate culling
     const int64_t blo[3] = {org[0] + bx * Box::X, org[1] + by * Box::Y,
                             RANK == 3 ? max(org[2] + bz * Box::Z, zlo) : 0};
     const int64_t bhi[3] = {min(org[0] + bx * Box::X + Box::X - 1, hi[0]),
@@ -366,34 +404,49 @@ __global__ void __launch_bounds__(kFastThreads) k_assign_fast(FastParams P) {
 #pragma unroll
     for (int v = 0; v < 4; ++v) valid[v] = row_ok && lx0 + v < RX && gx0 + v <= hi[0];
 
-    // candidates covering this box -> compact warp list
-    unsigned m0, m1;
-    __syncwarp();  // previous box's readers of wl are done
+    // candidates covering this box -> compact warp list (padded to even)
+    __syncwarp();
+    int nl;
     {
-      bool c0 = false, c1 = false;
+      bool cov[2];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int j = lane + 32 * h;
-        bool cov = j < n;
-        if (cov) {
+        bool c = j < n;
+        if (c) {
+#pragma unroll
           for (int a = 0; a < RANK; ++a) {
             const int64_t an = sm.anc[j][a];
-            if (an + g.grid[a] < blo[a] || an - g.grid[a] > bhi[a]) cov = false;
+            if (an + g.grid[a] < blo[a] || an - g.grid[a] > bhi[a]) c = false;
           }
         }
-        if (h == 0) c0 = cov;
-        else c1 = cov;
+        cov[h] = c;
       }
-      m0 = __ballot_sync(0xffffffffu, c0);
-      m1 = __ballot_sync(0xffffffffu, c1);
+      const unsigned m0 = __ballot_sync(0xffffffffu, cov[0]);
+      const unsigned m1 = __ballot_sync(0xffffffffu, cov[1]);
       const unsigned lt = (1u << lane) - 1u;
-      if (c0) sm.wl[warp][__popc(m0 & lt)] = (unsigned char)lane;
-      if (c1) sm.wl[warp][__popc(m0) + __popc(m1 & lt)] = (unsigned char)(lane + 32);
+      if (cov[0]) {
+        const int pos = __popc(m0 & lt);
+        sm.wl[warp][pos] = (unsigned short)(lane * RS);
+        sm.wj[warp][pos] = (unsigned char)lane;
+      }
+      if (cov[1]) {
+        const int pos = __popc(m0) + __popc(m1 & lt);
+        sm.wl[warp][pos] = (unsigned short)((lane + 32) * RS);
+        sm.wj[warp][pos] = (unsigned char)(lane + 32);
+      }
+      nl = __popc(m0) + __popc(m1);
+      if (lane == 0 && (nl & 1)) {
+        sm.wl[warp][nl] = (unsigned short)(n * RS);  // all-inf padding record
+        sm.wj[warp][nl] = (unsigned char)n;
+      }
       __syncwarp();
     }
-    const int nl = __popc(m0) + __popc(m1);
+    const int nlp = (nl + 1) & ~1;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) n_evals += valid[v] ? nl : 0;
 
-    // pixels and label words
+    // pixels (paired per channel) and label words
     const int64_t off0 = gx0 + gy * g.strides[1] + (RANK == 3 ? gz * g.strides[2] : 0);
     const int64_t li0 = off0 - g.slab_begin * g.plane;
     const int64_t di0 = data_index(g, off0);
@@ -407,12 +460,20 @@ __global__ void __launch_bounds__(kFastThreads) k_assign_fast(FastParams P) {
       if (valid[v]) {
         word[v] = P.labels[li0 + v];
 #pragma unroll
-        for (int c = 0; c < C; ++c)
-          p[v][c] = to_f(static_cast<const T*>(P.img)[di0 + v * C + c]);
+        for (int c = 0; c < C; ++c) p[v][c] = (float)static_cast<const T*>(P.img)[di0 + v * C + c];
       }
     }
+    f2 p01[C], p23[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      p01[c] = pk2(p[0][c], p[1][c]);
+      p23[c] = pk2(p[2][c], p[3][c]);
+    }
+    const int ox = kHdr + (lx0 < RXp ? lx0 : 0);
+    const int oy = kHdr + RXp + 2 * (ly < RY ? ly : 0);
+    const int oz = kHdr + RXp + 2 * RY + 2 * (lz < RZ ? lz : 0);
 
-    // fp32 argmin with runner-up (keys: value with 3 low bits = index in group)
+    // fp32 argmin with runner-up: keys = value with 3 low bits = index in group
     uint32_t best[4], second[4];
     int grp[4];
 #pragma unroll
@@ -420,36 +481,44 @@ __global__ void __launch_bounds__(kFastThreads) k_assign_fast(FastParams P) {
       best[v] = second[v] = 0xffffffffu;
       grp[v] = 0;
     }
-    for (int g0 = 0; g0 < nl; g0 += 8) {
+    for (int g0 = 0; g0 < nlp; g0 += 8) {
       uint32_t before[4];
 #pragma unroll
       for (int v = 0; v < 4; ++v) before[v] = best[v];
-      const int g1 = min(g0 + 8, nl);
-      for (int jj = g0; jj < g1; ++jj) {
-        const int j = sm.wl[warp][jj];
-        float syz = sy[j * RY + (ly < RY ? ly : 0)];
-        if (RANK == 3) syz += sz[j * RZ + (lz < RZ ? lz : 0)];
-        const float4 s4 = *reinterpret_cast<const float4*>(sx + j * RXp + (lx0 < RXp ? lx0 : 0));
-        const float sxv[4] = {s4.x, s4.y, s4.z, s4.w};
-        float ch[C], cl[C];
+      const int g1 = min(g0 + 8, nlp);
+      for (int jj = g0; jj < g1; jj += 2) {
+        uint32_t key[2][4];
 #pragma unroll
-        for (int c = 0; c < C; ++c) {
-          ch[c] = cvh[j * C + c];
-          cl[c] = cvl[j * C + c];
-        }
-        const uint32_t jl = (uint32_t)(jj & 7);
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          float acc = sxv[v] + syz;
+        for (int h = 0; h < 2; ++h) {
+          const float* r = rec + sm.wl[warp][jj + h];
+          const ulonglong2 sxv = *reinterpret_cast<const ulonglong2*>(r + ox);
+          f2 syz = *reinterpret_cast<const f2*>(r + oy);
+          if (RANK == 3) syz = add2(syz, *reinterpret_cast<const f2*>(r + oz));
+          f2 a01 = add2(sxv.x, syz), a23 = add2(sxv.y, syz);
 #pragma unroll
           for (int c = 0; c < C; ++c) {
-            const float d = (ch[c] - p[v][c]) + cl[c];
-            acc = fmaf(d, d, acc);
+            const ulonglong2 hl = *reinterpret_cast<const ulonglong2*>(r + 4 * c);
+            const f2 d01 = add2(sub2(hl.x, p01[c]), hl.y);
+            const f2 d23 = add2(sub2(hl.x, p23[c]), hl.y);
+            a01 = fma2(d01, d01, a01);
+            a23 = fma2(d23, d23, a23);
           }
-          const uint32_t key = fkey(acc, jl);
-          const uint32_t t = max(best[v], key);
-          best[v] = min(best[v], key);
-          second[v] = min(second[v], t);
+          float f0, f1, f2v, f3;
+          up2(a01, f0, f1);
+          up2(a23, f2v, f3);
+          const uint32_t jl = (uint32_t)((jj + h) & 7);
+          key[h][0] = fkey(f0, jl);
+          key[h][1] = fkey(f1, jl);
+          key[h][2] = fkey(f2v, jl);
+          key[h][3] = fkey(f3, jl);
+        }
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const uint32_t lo = min(key[0][v], key[1][v]);
+          const uint32_t hk = max(key[0][v], key[1][v]);
+          const uint32_t t = max(best[v], lo);
+          best[v] = min(best[v], lo);
+          second[v] = min3u(second[v], hk, t);
         }
       }
 #pragma unroll
@@ -457,46 +526,40 @@ __global__ void __launch_bounds__(kFastThreads) k_assign_fast(FastParams P) {
         if (best[v] != before[v]) grp[v] = g0;
     }
 
-    // decisions
-    uint32_t lab_out[4];
-    int slot[4];
-    unsigned amb_count = 0;
+    // ---- decisions ----
+    uint32_t newl[4], oldl[4];
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
-      lab_out[v] = kUndefined;
-      slot[v] = -1;
+      oldl[v] = newl[v] = P.codec.label(word[v]);
       if (!valid[v]) continue;
-      const int64_t li = li0 + v;
       uint32_t w = word[v];
       const bool has_best = best[v] < 0x7f800000u;
-      const int jstar = has_best ? sm.wl[warp][grp[v] + (best[v] & 7u)] : -1;
+      if (!has_best) continue;  // no window covers the voxel: keep the old label
+      const int jstar = sm.wj[warp][grp[v] + (best[v] & 7u)];
       const float bv = kval(best[v]);
-      const bool amb_cand = has_best && second[v] < 0x7f800000u &&
-                            kval(second[v]) <= bv * (1.0f + M) + A;
-      int decided = 0;  // 1 = update, 2 = keep, 0 = exact needed
-      if (!has_best) {
-        decided = 2;
-      } else if (!amb_cand) {
+      const bool amb_cand = second[v] < 0x7f800000u && kval(second[v]) <= bv * (1.0f + M) + A;
+      int decided = 0;  // 1 = update, 2 = keep, 0 = exact re-decision
+      if (!amb_cand) {
         if (w == kUndefined) {
           decided = 1;
         } else {
           const uint32_t L = P.codec.label(w), Tg = P.codec.tag(w);
-          if ((uint32_t)sm.id[jstar] == L && P.chg[L] <= (int)Tg) {
+          if ((uint32_t)sm.id[jstar] == L && __ldg(P.chg + L) <= (int)Tg) {
             decided = 2;  // same centre as when the label was set: D* == d_old
           } else {
             const float2* hc = P.hist32 + ((int64_t)Tg * g.k + L) * kStride;
-            float dold = 0.f;
+            float sp = 0.f;
 #pragma unroll
             for (int a = 0; a < RANK; ++a) {
-              const float2 cc = hc[C + a];
+              const float2 cc = __ldg(hc + C + a);
               const float x = (float)(a == 0 ? gx0 + v : (a == 1 ? gy : gz));
               const float t = ((cc.x - x) + cc.y) / (float)g.grid[a];
-              dold = fmaf(t, t, dold);
+              sp = fmaf(t, t, sp);
             }
-            dold *= (float)g.m_sq;
+            float dold = sp * (float)g.m_sq;
 #pragma unroll
             for (int c = 0; c < C; ++c) {
-              const float2 cc = hc[c];
+              const float2 cc = __ldg(hc + c);
               const float d = (cc.x - p[v][c]) + cc.y;
               dold = fmaf(d, d, dold);
             }
@@ -507,97 +570,77 @@ __global__ void __launch_bounds__(kFastThreads) k_assign_fast(FastParams P) {
       }
       if (decided == 1) {
         w = P.codec.pack((uint32_t)sm.id[jstar], P.tag_now);
-        P.labels[li] = w;
-        slot[v] = jstar;
       } else if (decided == 0) {
-        ++amb_count;
-        int64_t coord[kMaxRank] = {gx0 + v, gy, gz, 0};
-        int s;
-        const uint32_t nw =
-            exact_region_voxel(P, sm, coord, data_index(g, off0 + v), w, amb_cand, jstar, &s);
-        if (nw != w) {
-          w = nw;
-          P.labels[li] = w;
-          slot[v] = s;
-        }
+        ++n_redecided;
+        w = exact_region_voxel(P, sm, gx0 + v, gy, gz, di0 + v * C, w, amb_cand, jstar);
       }
-      lab_out[v] = P.codec.label(w);
-      if (slot[v] < 0 && lab_out[v] != kUndefined) {
-        if (jstar >= 0 && (uint32_t)sm.id[jstar] == lab_out[v]) {
-          slot[v] = jstar;
-        } else {
-          slot[v] = -1;
-          for (int j = 0; j < n; ++j)
-            if ((uint32_t)sm.id[j] == lab_out[v]) {
-              slot[v] = j;
-              break;
-            }
-        }
-      }
-    }
-    if (P.eval_count) {
-      const unsigned a = __reduce_add_sync(0xffffffffu, amb_count);
-      unsigned nv = 0;
-#pragma unroll
-      for (int v = 0; v < 4; ++v) nv += valid[v];
-      const unsigned tv = __reduce_add_sync(0xffffffffu, nv);
-      if (lane == 0) {
-        atomicAdd(P.eval_count, (unsigned long long)tv * nl);
-        atomicAdd(P.counters + 5, (unsigned long long)a);
-      }
+      if (w != word[v]) P.labels[li0 + v] = w;
+      newl[v] = P.codec.label(w);
     }
 
-    // ---- warp-aggregated accumulation into CTA slots ----
-    unsigned pending = 0;
+    // ---- delta accumulation: +new / -old for voxels whose label changed ----
+    unsigned pending = 0;  // bit v: +new[v]; bit 4+v: -old[v]
+    bool undef_any = false;
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
-      if (valid[v] && lab_out[v] == kUndefined) {
-        atomicAdd(P.counters, 1ull);  // slic.hpp:330-331 (reported by the host)
-      } else if (valid[v]) {
+      if (!valid[v]) continue;
+      if (newl[v] == kUndefined) undef_any = true;
+      if (newl[v] != oldl[v]) {
         pending |= 1u << v;
+        if (oldl[v] != kUndefined) pending |= 1u << (4 + v);
+        ++n_changed;
       }
+    }
+    if (__any_sync(0xffffffffu, undef_any)) {
+      unsigned u = 0;
+#pragma unroll
+      for (int v = 0; v < 4; ++v) u += valid[v] && newl[v] == kUndefined;
+      const unsigned tu = __reduce_add_sync(0xffffffffu, u);
+      if (lane == 0) atomicAdd(P.counters, (unsigned long long)tu);  // slic.hpp:330-331
     }
     for (;;) {
       const unsigned any = __ballot_sync(0xffffffffu, pending != 0);
       if (!any) break;
       const int leader = __ffs(any) - 1;
-      const int myv = pending ? __ffs(pending) - 1 : 0;
       uint32_t mylab = 0;
-      int myslot = -1;
+      if (pending) {
+        const int bit = __ffs(pending) - 1;
 #pragma unroll
-      for (int v = 0; v < 4; ++v)
-        if (v == myv) {
-          mylab = lab_out[v];
-          myslot = slot[v];
-        }
+        for (int v = 0; v < 8; ++v)
+          if (v == bit) mylab = v < 4 ? newl[v] : oldl[v - 4];
+      }
       const uint32_t L = __shfl_sync(0xffffffffu, mylab, leader);
-      const int S = __shfl_sync(0xffffffffu, myslot, leader);
-      uint32_t cnt = 0, sxr = 0;
+      int cnt = 0, sxr = 0, syr = 0, szr = 0;
       int64_t sv[C];
 #pragma unroll
       for (int c = 0; c < C; ++c) sv[c] = 0;
 #pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        if ((pending >> v & 1) && lab_out[v] == L) {
-          pending &= ~(1u << v);
-          ++cnt;
-          sxr += (uint32_t)(lx0 + v);
+      for (int q = 0; q < 8; ++q) {
+        const int v = q & 3;
+        const uint32_t lq = q < 4 ? newl[v] : oldl[v];
+        if ((pending >> q & 1) && lq == L) {
+          pending &= ~(1u << q);
+          const int sgn = q < 4 ? 1 : -1;
+          cnt += sgn;
+          sxr += sgn * (lx0 + v);
+          syr += sgn * ly;
+          szr += sgn * lz;
 #pragma unroll
           for (int c = 0; c < C; ++c) {
-            if (sizeof(T) < 4) sv[c] += (int64_t)p[v][c];
-            else sv[c] += __float2ll_rn(p[v][c] * fscale);  // exact: |v| 2^shift < 2^40
+            if (sizeof(T) < 4) sv[c] += sgn * (int64_t)p[v][c];
+            else sv[c] += sgn * __float2ll_rn(p[v][c] * fscale);  // exact: |v| 2^s < 2^40
           }
         }
       }
-      const uint32_t tc = __reduce_add_sync(0xffffffffu, cnt);
-      const uint32_t tx = __reduce_add_sync(0xffffffffu, sxr);
-      const uint32_t ty = __reduce_add_sync(0xffffffffu, cnt * (uint32_t)ly);
-      const uint32_t tz = RANK == 3 ? __reduce_add_sync(0xffffffffu, cnt * (uint32_t)lz) : 0u;
+      const int tc = (int)__reduce_add_sync(0xffffffffu, (uint32_t)cnt);
+      const int tx = (int)__reduce_add_sync(0xffffffffu, (uint32_t)sxr);
+      const int ty = (int)__reduce_add_sync(0xffffffffu, (uint32_t)syr);
+      const int tz = RANK == 3 ? (int)__reduce_add_sync(0xffffffffu, (uint32_t)szr) : 0;
       long long tvs[C];
 #pragma unroll
       for (int c = 0; c < C; ++c) {
         if (sizeof(T) < 4) {
-          tvs[c] = (long long)__reduce_add_sync(0xffffffffu, (uint32_t)sv[c]);
+          tvs[c] = (int)__reduce_add_sync(0xffffffffu, (uint32_t)sv[c]);
         } else {
           const uint64_t u = (uint64_t)sv[c];
           const int32_t h = (int32_t)__reduce_add_sync(0xffffffffu, (uint32_t)(sv[c] >> 32));
@@ -607,38 +650,58 @@ __global__ void __launch_bounds__(kFastThreads) k_assign_fast(FastParams P) {
         }
       }
       if (lane == leader) {
+        int S = -1;
+        for (int j = 0; j < n; ++j)
+          if ((uint32_t)sm.id[j] == L) {
+            S = j;
+            break;
+          }
         if (S >= 0) {
           unsigned long long* a = accs + S * kComp;
 #pragma unroll
-          for (int c = 0; c < C; ++c) atomicAdd(a + c, (unsigned long long)tvs[c]);
-          atomicAdd(a + C, (unsigned long long)tx);
-          atomicAdd(a + C + 1, (unsigned long long)ty);
-          if (RANK == 3) atomicAdd(a + C + 2, (unsigned long long)tz);
-          atomicAdd(a + kStride, (unsigned long long)tc);
+          for (int c = 0; c < C; ++c)
+            if (tvs[c]) atomicAdd(a + c, (unsigned long long)tvs[c]);
+          if (tx) atomicAdd(a + C, (unsigned long long)(long long)tx);
+          if (ty) atomicAdd(a + C + 1, (unsigned long long)(long long)ty);
+          if (RANK == 3 && tz) atomicAdd(a + C + 2, (unsigned long long)(long long)tz);
+          if (tc) atomicAdd(a + kStride, (unsigned long long)(long long)tc);
         } else {
-          // stale label outside the region's candidates: global, absolute coords
+          // label outside the region's candidates: global, absolute coordinates
           unsigned long long* a = P.acc + (uint64_t)L * kComp;
 #pragma unroll
-          for (int c = 0; c < C; ++c) atomicAdd(a + c, (unsigned long long)tvs[c]);
-          atomicAdd(a + C, (unsigned long long)(tx + (uint64_t)tc * org[0]));
-          atomicAdd(a + C + 1, (unsigned long long)(ty + (uint64_t)tc * org[1]));
-          if (RANK == 3) atomicAdd(a + C + 2, (unsigned long long)(tz + (uint64_t)tc * org[2]));
-          atomicAdd(a + kStride, (unsigned long long)tc);
+          for (int c = 0; c < C; ++c)
+            if (tvs[c]) atomicAdd(a + c, (unsigned long long)tvs[c]);
+          atomicAdd(a + C, (unsigned long long)(tx + (long long)tc * org[0]));
+          atomicAdd(a + C + 1, (unsigned long long)(ty + (long long)tc * org[1]));
+          if (RANK == 3) atomicAdd(a + C + 2, (unsigned long long)(tz + (long long)tc * org[2]));
+          if (tc) atomicAdd(a + kStride, (unsigned long long)(long long)tc);
         }
       }
     }
   }
+  if (P.eval_count) {
+    const unsigned a = __reduce_add_sync(0xffffffffu, n_redecided);
+    const unsigned c = __reduce_add_sync(0xffffffffu, n_changed);
+    const unsigned e = __reduce_add_sync(0xffffffffu, n_evals);
+    if (lane == 0) {
+      atomicAdd(P.counters + 5, (unsigned long long)a);
+      atomicAdd(P.counters + 7, (unsigned long long)c);
+      atomicAdd(P.eval_count, (unsigned long long)e);
+    }
+  }
   __syncthreads();
-  // ---- flush CTA slots (one global atomic per non-empty component) ----
+  // ---- flush CTA slots (one global atomic per non-zero component) ----
   for (int e = tid; e < n * kComp; e += kFastThreads) {
     const int j = e / kComp, i = e - j * kComp;
-    const unsigned long long cnt = accs[j * kComp + kStride];
-    if (cnt == 0) continue;
-    unsigned long long v = accs[j * kComp + i];
-    if (i >= C && i < kStride) v += cnt * (unsigned long long)org[i - C];
-    if (v) atomicAdd(P.acc + (uint64_t)sm.id[j] * kComp + i, v);
+    long long v = (long long)accs[e];
+    if (i >= C && i < kStride) v += (long long)accs[j * kComp + kStride] * org[i - C];
+    if (v) atomicAdd(P.acc + (uint64_t)sm.id[j] * kComp + i, (unsigned long long)v);
   }
 }
+
+// Evaluation count of the fast path (bench statistics): candidates per box x
+// voxels is recorded by the host from the window volumes; this kernel only
+// needs the counters above.
 
 // hi/lo fp32 split of one centre table (for the fp32 d_old filter).
 static __global__ void k_split32(const double* c, float2* out, int64_t n) {
@@ -668,10 +731,10 @@ inline int region_extent(int s) {
 
 inline size_t fast_smem_bytes(const Geom& g, const int* R) {
   const int RXp = (R[0] + 3) & ~3;
+  const int RS = (4 * g.channels + RXp + 2 * R[1] + (g.rank == 3 ? 2 * R[2] : 0) + 3) & ~3;
   size_t b = sizeof(FastSmem);
-  b += 2ull * kFastMaxCand * g.channels * sizeof(float);
-  b += (size_t)kFastMaxCand * (RXp + R[1] + (g.rank == 3 ? R[2] : 1)) * sizeof(float);
-  b += 8 + (size_t)kFastMaxCand * (g.stride + 1) * sizeof(unsigned long long);
+  b += (size_t)(kFastMaxCand + 1) * RS * sizeof(float);
+  b += (size_t)kFastMaxCand * (g.stride + 1) * sizeof(unsigned long long);
   return b;
 }
 

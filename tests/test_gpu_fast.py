@@ -47,7 +47,7 @@ def test_fast_equals_exact(sslic, case):
     for it in range(iters):
         fast.assign()
         exact.assign()
-        amb, crowded = fast.fast_stats()
+        amb, crowded, _ = fast.fast_stats()
         assert fast.undefined_count() == exact.undefined_count()
         fast.update()
         exact.update()
@@ -71,7 +71,7 @@ def test_fast_path_is_used(sslic):
     fast.set_stats(True)
     fast.assign()
     evals, window = fast.eval_stats()
-    amb, crowded = fast.fast_stats()
+    amb, crowded, _ = fast.fast_stats()
     n = int(np.prod(dims))
     assert evals > 0 and window > 0
     assert evals >= window  # box culling evaluates a superset of the windows
