@@ -1,0 +1,149 @@
+// sslic_b200.hpp — C++ drop-in for users of the reference library.
+//
+// Include it AFTER the reference headers ("sslic/slic.hpp" and
+// "sslic/connectivity.hpp"): it is written against the reference's own types
+// (NDImage, SlicParams, ClusterTable, LabelMap, DistanceMap, SlicResult) and
+// forwards to the C ABI in sslic_b200.h, so switching a caller from the CPU
+// path to the B200 path is a namespace change:
+//
+//   sslic::SlicResult r = sslic::run_slic(img, params, workers);        // CPU
+//   sslic::SlicResult r = sslic::b200::run_slic(img, params);           // B200
+//
+// Errors are rethrown as the reference's exception classes
+// (std::invalid_argument / std::logic_error / std::out_of_range), CUDA
+// failures as std::runtime_error. The fp64 NDImage is narrowed losslessly to
+// uint8 / uint16 / float32 when every value is representable (so the fast
+// fp32-filter kernel applies); otherwise it is passed as fp64.
+#pragma once
+
+#include <cstdint>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "sslic_b200.h"
+
+namespace sslic {
+namespace b200 {
+
+namespace detail {
+
+inline void check(int status) {
+  if (status == SSLIC_OK) return;
+  const std::string msg = sslic_last_error();
+  switch (status) {
+    case SSLIC_EINVAL: throw std::invalid_argument(msg);
+    case SSLIC_ELOGIC: throw std::logic_error(msg);
+    case SSLIC_ERANGE: throw std::out_of_range(msg);
+    default: throw std::runtime_error("sslic_b200: " + msg);
+  }
+}
+
+// Native-dtype copy of an NDImage (image.hpp:236-285), narrowed losslessly.
+struct NativeImage {
+  sslic_image desc{};
+  std::vector<unsigned char> bytes;
+};
+
+inline NativeImage narrow(const NDImage& img) {
+  NativeImage out;
+  const std::vector<double>& d = img.data();
+  bool u8 = true, u16 = true, f32 = true;
+  for (double v : d) {
+    const bool integral = v == static_cast<double>(static_cast<int64_t>(v));
+    u8 = u8 && integral && v >= 0.0 && v <= 255.0;
+    u16 = u16 && integral && v >= 0.0 && v <= 65535.0;
+    f32 = f32 && static_cast<double>(static_cast<float>(v)) == v;
+    if (!u16 && !f32) break;
+  }
+  const int dtype = u8 ? SSLIC_U8 : (u16 ? SSLIC_U16 : (f32 ? SSLIC_F32 : SSLIC_F64));
+  const size_t esz = dtype == SSLIC_U8 ? 1 : dtype == SSLIC_U16 ? 2 : dtype == SSLIC_F32 ? 4 : 8;
+  out.bytes.resize(d.size() * esz);
+  for (size_t i = 0; i < d.size(); ++i) {
+    switch (dtype) {
+      case SSLIC_U8: out.bytes[i] = static_cast<uint8_t>(d[i]); break;
+      case SSLIC_U16: {
+        const uint16_t v = static_cast<uint16_t>(d[i]);
+        std::memcpy(&out.bytes[i * 2], &v, 2);
+        break;
+      }
+      case SSLIC_F32: {
+        const float v = static_cast<float>(d[i]);
+        std::memcpy(&out.bytes[i * 4], &v, 4);
+        break;
+      }
+      default: std::memcpy(&out.bytes[i * 8], &d[i], 8);
+    }
+  }
+  out.desc.rank = img.rank();
+  for (int a = 0; a < 4; ++a) out.desc.dims[a] = a < img.rank() ? img.dims()[a] : 1;
+  out.desc.channels = img.channels();
+  out.desc.dtype = dtype;
+  out.desc.data = out.bytes.data();
+  return out;
+}
+
+inline sslic_params params_of(const SlicParams& p) {
+  sslic_params c{};
+  for (int a = 0; a < 4; ++a) c.grid[a] = a < p.grid.size() ? p.grid[a] : 1;
+  c.weight_m = p.weight_m;
+  c.max_iterations = p.max_iterations;
+  c.enforce_connectivity = p.enforce_connectivity ? 1 : 0;
+  c.has_residual_threshold = p.residual_threshold.has_value() ? 1 : 0;
+  c.residual_threshold = p.residual_threshold.value_or(0.0);
+  return c;
+}
+
+}  // namespace detail
+
+/// run_slic (slic.hpp:384-415) on a B200. `device` replaces `workers`.
+inline SlicResult run_slic(const NDImage& img, const SlicParams& params, int device = 0) {
+  params.validate(img.dims());  // same exceptions as the reference, before any copy
+  detail::NativeImage nimg = detail::narrow(img);
+  const sslic_params p = detail::params_of(params);
+  const int iters = params.iterations_for(img.rank());
+  std::vector<int64_t> dims(img.dims().begin(), img.dims().end());
+  std::vector<int64_t> grid(params.grid.begin(), params.grid.end());
+  ClusterTable table(img.channels(), img.rank(),
+                     sslic_cluster_count(img.rank(), dims.data(), grid.data()));
+  LabelMap labels(img.dims());
+  std::vector<double> residuals(iters > 0 ? iters : 1);
+  int done = 0;
+  detail::check(sslic_run_slic(&nimg.desc, &p, device, labels.data().data(),
+                               table.data().data(), residuals.data(), &done));
+  residuals.resize(done);
+  return SlicResult{std::move(labels), std::move(table), std::move(residuals)};
+}
+
+/// enforce_connectivity (connectivity.hpp:265-273) on a B200.
+inline LabelMap enforce_connectivity(const LabelMap& labels, const ClusterTable& table,
+                                     const SlicParams& params, int device = 0) {
+  std::vector<int64_t> dims(labels.dims().begin(), labels.dims().end());
+  std::vector<int64_t> grid(params.grid.begin(), params.grid.end());
+  LabelMap out(labels.dims());
+  uint32_t next = 0;
+  detail::check(sslic_enforce_connectivity(
+      labels.rank(), dims.data(), labels.data().data(), table.data().data(), table.channels(),
+      table.count(), grid.data(), device, out.data().data(), &next));
+  return out;
+}
+
+/// perturb_centers (slic.hpp:236-267) on a B200.
+inline ClusterTable perturb_centers(const NDImage& img, ClusterTable table, int device = 0) {
+  detail::NativeImage nimg = detail::narrow(img);
+  detail::check(sslic_perturb_centers(&nimg.desc, table.data().data(), table.count(), device));
+  return table;
+}
+
+/// One assign_labels pass over the whole image (slic.hpp:275-310), in place.
+inline void assign_labels(const NDImage& img, const ClusterTable& table, const SlicParams& params,
+                          LabelMap& labels, DistanceMap& dists, int device = 0) {
+  detail::NativeImage nimg = detail::narrow(img);
+  const sslic_params p = detail::params_of(params);
+  detail::check(sslic_assign_pass(&nimg.desc, &p, table.data().data(), table.count(), device,
+                                  labels.data().data(), dists.data().data()));
+}
+
+}  // namespace b200
+}  // namespace sslic

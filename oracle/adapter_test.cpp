@@ -1,0 +1,49 @@
+// TEST INFRASTRUCTURE ONLY — drives include/sslic_b200.hpp (the C++ drop-in
+// over the C ABI) side by side with the UNMODIFIED reference headers and
+// checks that a caller switching sslic::run_slic -> sslic::b200::run_slic and
+// sslic::enforce_connectivity -> sslic::b200::enforce_connectivity gets
+// bit-identical results. Built by oracle/Makefile into oracle/_ref/ (it needs
+// /root/reference at build time); run by tests/test_gpu_adapter.py.
+#include <cstdio>
+#include <random>
+
+#include "sslic/connectivity.hpp"
+#include "sslic/slic.hpp"
+#include "support/oracles.hpp"
+#include "sslic_b200.hpp"
+
+int main() {
+  std::mt19937_64 rng(0x55110C);
+  int failures = 0, cases = 0;
+  for (int i = 0; i < 40; ++i) {
+    const int rank = std::uniform_int_distribution<int>(1, 3)(rng);
+    const int channels = rng() % 2 == 0 ? 1 : 3;
+    sslic::NDImage img = oracle::random_image(rng, rank, 24, channels);
+    if (i % 2 == 1)  // integer-valued images exercise the u8 narrowing / fast path
+      for (double& v : img.data()) v = static_cast<double>(static_cast<int>(v));
+    sslic::SlicParams params;
+    params.grid = oracle::random_grid(rng, img.dims());
+    params.weight_m = oracle::random_weight(rng);
+    const sslic::SlicResult cpu = sslic::run_slic(img, params, 2);
+    const sslic::SlicResult gpu = sslic::b200::run_slic(img, params);
+    const sslic::LabelMap cc_cpu = sslic::enforce_connectivity(cpu.labels, cpu.centers, params, 2);
+    const sslic::LabelMap cc_gpu = sslic::b200::enforce_connectivity(gpu.labels, gpu.centers, params);
+    const bool ok = cpu.labels == gpu.labels && cpu.centers == gpu.centers && cc_cpu == cc_gpu &&
+                    cpu.residuals.size() == gpu.residuals.size();
+    if (!ok) {
+      std::printf("case %d differs (rank %d, channels %d)\n", i, rank, channels);
+      ++failures;
+    }
+    ++cases;
+  }
+  // exceptions keep the reference's classes
+  try {
+    sslic::SlicParams bad;
+    bad.grid = sslic::GridSize{9, 8};
+    sslic::b200::run_slic(sslic::NDImage::zeros(sslic::Shape{8, 8}, 1), bad);
+    ++failures;
+  } catch (const std::invalid_argument&) {
+  }
+  std::printf("adapter: %d cases, %d failures\n", cases, failures);
+  return failures ? 1 : 0;
+}
