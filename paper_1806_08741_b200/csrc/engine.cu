@@ -6,7 +6,7 @@
 #include <cstring>
 
 #include "engine.cuh"
-#include "kernels_fast.cuh"
+#include "kernels_fast_main.cuh"
 
 namespace sslic_b200 {
 

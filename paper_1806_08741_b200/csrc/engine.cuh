@@ -5,7 +5,7 @@
 
 #include "common.cuh"
 #include "kernels_exact.cuh"
-#include "kernels_fast.cuh"
+#include "kernels_fast_main.cuh"
 
 namespace sslic_b200 {
 

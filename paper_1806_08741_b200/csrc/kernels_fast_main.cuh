@@ -1,0 +1,692 @@
+// K2 fast path, main kernel and launchers (helpers, exact re-decision and the
+// crowded-region fallback are in kernels_fast.cuh; design notes there and in
+// DESIGN.md "K2").
+#pragma once
+
+#include "kernels_fast.cuh"
+
+namespace sslic_b200 {
+
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem_dst, const void* gsrc) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
+// sum over the warp of a pair of signed 16-bit quantities packed in 32 bits
+// (|sum| < 2^15 each)
+__device__ __forceinline__ void redux_pair(int lo, int hi, int& slo, int& shi) {
+  const uint32_t t = __reduce_add_sync(0xffffffffu, (uint32_t)(lo + hi * 65536));
+  slo = (int)(int16_t)(t & 0xffffu);
+  shi = ((int)t - slo) >> 16;
+}
+
+// 4 consecutive voxels x C channels of T, vector loads when aligned
+template <int C, typename T>
+__device__ __forceinline__ void load_run(const T* src, bool vec, const bool* valid, float (&p)[4][C]) {
+  constexpr int NW = C * (int)sizeof(T);  // 32-bit words for 4 voxels
+  if (vec) {
+    uint32_t w[NW];
+    if (NW % 4 == 0) {
+#pragma unroll
+      for (int i = 0; i < NW / 4; ++i) {
+        const uint4 q = __ldg(reinterpret_cast<const uint4*>(src) + i);
+        w[4 * i] = q.x;
+        w[4 * i + 1] = q.y;
+        w[4 * i + 2] = q.z;
+        w[4 * i + 3] = q.w;
+      }
+    } else if (NW % 2 == 0) {
+#pragma unroll
+      for (int i = 0; i < NW / 2; ++i) {
+        const uint2 q = __ldg(reinterpret_cast<const uint2*>(src) + i);
+        w[2 * i] = q.x;
+        w[2 * i + 1] = q.y;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < NW; ++i) w[i] = __ldg(reinterpret_cast<const uint32_t*>(src) + i);
+    }
+    T vals[4 * C];
+    memcpy(vals, w, sizeof(vals));
+#pragma unroll
+    for (int v = 0; v < 4; ++v)
+#pragma unroll
+      for (int c = 0; c < C; ++c) p[v][c] = (float)vals[v * C + c];
+  } else {
+#pragma unroll
+    for (int v = 0; v < 4; ++v)
+#pragma unroll
+      for (int c = 0; c < C; ++c) p[v][c] = valid[v] ? (float)__ldg(src + v * C + c) : 0.f;
+  }
+}
+
+template <int RANK, int C, typename T>
+__global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
+  using Box = BoxShape<RANK>;
+  constexpr int kStride = C + RANK;
+  constexpr int kComp = kStride + 1;
+  constexpr int kHdr = 4 * C;  // (hi, hi, lo, lo) per channel
+  constexpr int kWarps = kFastThreads / 32;
+  const Geom& g = P.g;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  FastSmem& sm = *reinterpret_cast<FastSmem*>(smem_raw);
+  const int RX = P.R[0], RY = P.R[1], RZ = RANK == 3 ? P.R[2] : 1;
+  const int RXp = (RX + 3) & ~3;
+  const int RS = (kHdr + RXp + 2 * RY + (RANK == 3 ? 2 * RZ : 0) + 3) & ~3;
+  float* rec = reinterpret_cast<float*>(smem_raw + sizeof(FastSmem));  // [cand+1][RS]
+  unsigned long long* accs =
+      reinterpret_cast<unsigned long long*>(rec + (size_t)(kFastMaxCand + 1) * RS);
+  // per-warp staging of the carried-over centres: [warp][v][i][lane] float2, chg [warp][v][lane]
+  float2* stage = reinterpret_cast<float2*>(accs + kFastMaxCand * kComp);
+  int* stage_chg = reinterpret_cast<int*>(stage + kWarps * 4 * kStride * 32);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // ---- region ----
+  int64_t rb = blockIdx.x;
+  const int rxi = (int)(rb % P.nreg[0]);
+  rb /= P.nreg[0];
+  const int ryi = (int)(rb % P.nreg[1]);
+  rb /= P.nreg[1];
+  const int rzi = (int)rb;
+  const int64_t org[3] = {(int64_t)rxi * RX, (int64_t)ryi * RY,
+                          RANK == 3 ? P.reg_z0 + (int64_t)rzi * RZ : 0};
+  const int64_t hi[3] = {min(org[0] + RX, g.dims[0]) - 1, min(org[1] + RY, g.dims[1]) - 1,
+                         RANK == 3 ? min(org[2] + RZ, g.dims[2]) - 1 : 0};
+  const int64_t zlo = RANK == 3 ? max(org[2], g.slab_begin) : 0;
+  const int64_t zhi = RANK == 3 ? min(hi[2], g.slab_end - 1) : 0;
+  // region-local inclusive bounds (32-bit)
+  const int ex = (int)(hi[0] - org[0]), ey = (int)(hi[1] - org[1]);
+  const int ez_lo = (int)(zlo - org[2]), ez_hi = (int)(zhi - org[2]);
+
+  // ---- gather candidates (warp 0) ----
+  if (warp == 0) {
+    int clo[3], chi[3], nc = 1;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      if (a < RANK) {
+        const int64_t lo_a = a == 2 ? zlo : org[a];
+        const int64_t hi_a = a == 2 ? zhi : hi[a];
+        const int64_t l = lo_a - g.grid[a];
+        clo[a] = l < 0 ? 0 : (int)(l / g.grid[a]);
+        const int64_t h = (hi_a + g.grid[a]) / g.grid[a];
+        chi[a] = h > g.cells[a] - 1 ? g.cells[a] - 1 : (int)h;
+      } else {
+        clo[a] = chi[a] = 0;
+      }
+      nc *= chi[a] - clo[a] + 1;
+    }
+    int total = 0;
+    for (int base = 0; base < nc; base += 32) {
+      const int i = base + lane;
+      int cnt = 0, cstart = 0;
+      if (i < nc) {
+        const int nx = chi[0] - clo[0] + 1, ny = chi[1] - clo[1] + 1;
+        const int cx = clo[0] + i % nx, cy = clo[1] + (i / nx) % ny, cz = clo[2] + i / (nx * ny);
+        const int64_t cell = ((int64_t)cz * g.cells[1] + cy) * g.cells[0] + cx;
+        cstart = P.cell_start[cell];
+        cnt = P.cell_start[cell + 1] - cstart;
+      }
+      int incl = cnt;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      const int excl = total + incl - cnt;
+      for (int q = 0; q < cnt; ++q)
+        if (excl + q < kFastMaxCand) sm.id[excl + q] = P.items[cstart + q];
+      total += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) {
+      sm.n_cand = total < kFastMaxCand ? total : kFastMaxCand;
+      sm.overflow = total > kFastMaxCand;
+    }
+  }
+  __syncthreads();
+  const int n = sm.n_cand;
+  if (sm.overflow) {
+    if (tid == 0) atomicAdd(P.counters + 6, 1ull);
+    crowded_region<RANK, C>(P, org, hi, zlo, zhi);
+    return;
+  }
+
+  // ---- stage candidate records (+ one all-inf padding record at slot n) ----
+  for (int j = tid; j <= n; j += kFastThreads) {
+    float* r = rec + (size_t)j * RS;
+    if (j < n) {
+      const int kid = sm.id[j];
+      const double* ctr = P.centers + (int64_t)kid * g.stride;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const float h = __double2float_rn(ctr[c]);
+        const float l = __double2float_rn(ctr[c] - (double)h);
+        r[4 * c] = h;
+        r[4 * c + 1] = h;
+        r[4 * c + 2] = l;
+        r[4 * c + 3] = l;
+      }
+      // anchors stored region-local (32-bit)
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+        sm.anc[j][a] = a < RANK ? (int)(P.anchors[kid * kMaxRank + a] - org[a]) : 0;
+    } else {
+#pragma unroll
+      for (int c = 0; c < 4 * C; ++c) r[c] = 0.f;
+    }
+  }
+  for (int i = tid; i < n * kComp; i += kFastThreads) accs[i] = 0ull;
+  __syncthreads();
+  {
+    const int per = RX + RY + (RANK == 3 ? RZ : 0);
+    for (int e = tid; e < (n + 1) * per; e += kFastThreads) {
+      const int j = e / per;
+      int r = e - j * per, a = 0;
+      if (r >= RX) {
+        r -= RX;
+        a = 1;
+        if (r >= RY) {
+          r -= RY;
+          a = 2;
+        }
+      }
+      float v = kInf;
+      if (j < n) {
+        const int kid = sm.id[j];
+        const int an = a == 0 ? sm.anc[j][0] : (a == 1 ? sm.anc[j][1] : sm.anc[j][2]);
+        const int s = g.grid[a];
+        const int dx = r - an;
+        if (dx >= -s && dx <= s) {
+          const int64_t x = (a == 0 ? org[0] : (a == 1 ? org[1] : org[2])) + r;
+          const double t = (P.centers[(int64_t)kid * g.stride + C + a] - (double)x) / (double)s;
+          v = __double2float_rn(g.m_sq * (t * t));
+        }
+      }
+      float* rj = rec + (size_t)j * RS + kHdr;
+      if (a == 0) {
+        rj[r] = v;
+      } else if (a == 1) {
+        rj[RXp + 2 * r] = v;
+        rj[RXp + 2 * r + 1] = v;
+      } else {
+        rj[RXp + 2 * RY + 2 * r] = v;
+        rj[RXp + 2 * RY + 2 * r + 1] = v;
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- per-warp sweep over the region's boxes ----
+  const int nbx = (RX + Box::X - 1) / Box::X, nby = (RY + Box::Y - 1) / Box::Y;
+  const int nbz = RANK == 3 ? (RZ + Box::Z - 1) / Box::Z : 1;
+  const int nbox = nbx * nby * nbz;
+  const int xq = lane & 1;
+  const int yq = RANK == 3 ? (lane >> 1) & 3 : lane >> 1;
+  const int zq = RANK == 3 ? lane >> 3 : 0;
+  const float M = P.margin;
+  const float A = P.abs_margin;
+  const float fscale = ldexpf(1.0f, P.shift);
+  const float msq = (float)g.m_sq;
+  const int64_t lab_base = -g.slab_begin * g.plane;
+  const int64_t img_base = -g.data_begin * g.plane;
+  float2* my_stage = stage + (size_t)warp * 4 * kStride * 32 + lane;
+  int* my_chg = stage_chg + warp * 4 * 32 + lane;
+  unsigned n_changed = 0, n_redecided = 0, n_evals = 0;
+
+#pragma unroll 1
+  for (int b = warp; b < nbox; b += kWarps) {
+    const int bx = b % nbx, by = (b / nbx) % nby, bz = b / (nbx * nby);
+    // box bounds in region-local coordinates, clipped
+    const int bx0 = bx * Box::X, by0 = by * Box::Y, bz0 = bz * Box::Z;
+    const int bx1 = min(bx0 + Box::X - 1, ex), by1 = min(by0 + Box::Y - 1, ey);
+    const int bz0c = RANK == 3 ? max(bz0, ez_lo) : 0;
+    const int bz1 = RANK == 3 ? min(bz0 + Box::Z - 1, ez_hi) : 0;
+    if (bx0 > bx1 || by0 > by1 || bz0c > bz1) continue;  // uniform
+    const int lx0 = bx0 + 4 * xq, ly = by0 + yq, lz = bz0 + zq;
+    const bool row_ok = ly <= by1 && (RANK == 2 || (lz >= bz0c && lz <= bz1));
+    bool valid[4];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) valid[v] = row_ok && lx0 + v <= ex && lx0 + v < RX;
+    const bool all4 = valid[0] && valid[1] && valid[2] && valid[3];
+
+    // candidates covering this box -> compact warp list (padded to even)
+    __syncwarp();
+    int nl;
+    {
+      bool cov[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int j = lane + 32 * h;
+        bool c = j < n;
+        if (c) {
+          const int s0 = g.grid[0], s1 = g.grid[1];
+          c = sm.anc[j][0] + s0 >= bx0 && sm.anc[j][0] - s0 <= bx1 && sm.anc[j][1] + s1 >= by0 &&
+              sm.anc[j][1] - s1 <= by1;
+          if (RANK == 3) {
+            const int s2 = g.grid[2];
+            c = c && sm.anc[j][2] + s2 >= bz0c && sm.anc[j][2] - s2 <= bz1;
+          }
+        }
+        cov[h] = c;
+      }
+      const unsigned m0 = __ballot_sync(0xffffffffu, cov[0]);
+      const unsigned m1 = __ballot_sync(0xffffffffu, cov[1]);
+      const unsigned lt = (1u << lane) - 1u;
+      if (cov[0]) {
+        const int pos = __popc(m0 & lt);
+        sm.wl[warp][pos] = (unsigned short)(lane * RS);
+        sm.wj[warp][pos] = (unsigned char)lane;
+      }
+      if (cov[1]) {
+        const int pos = __popc(m0) + __popc(m1 & lt);
+        sm.wl[warp][pos] = (unsigned short)((lane + 32) * RS);
+        sm.wj[warp][pos] = (unsigned char)(lane + 32);
+      }
+      nl = __popc(m0) + __popc(m1);
+      if (lane == 0 && (nl & 1)) {
+        sm.wl[warp][nl] = (unsigned short)(n * RS);  // all-inf padding record
+        sm.wj[warp][nl] = (unsigned char)n;
+      }
+      __syncwarp();
+    }
+    const int nlp = (nl + 1) & ~1;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) n_evals += valid[v] ? nl : 0;
+
+    // label words + pixels (vector loads for aligned full runs)
+    const int64_t gx0 = org[0] + lx0, gy = org[1] + ly, gz = org[2] + lz;
+    const int64_t off0 = gx0 + gy * g.strides[1] + (RANK == 3 ? gz * g.strides[2] : 0);
+    const bool vec = P.aligned4 && all4;
+    uint32_t word[4];
+    if (vec) {
+      const uint4 q = *reinterpret_cast<const uint4*>(P.labels + off0 + lab_base);
+      word[0] = q.x;
+      word[1] = q.y;
+      word[2] = q.z;
+      word[3] = q.w;
+    } else {
+#pragma unroll
+      for (int v = 0; v < 4; ++v) word[v] = valid[v] ? P.labels[off0 + lab_base + v] : kUndefined;
+    }
+    float p[4][C];
+    const T* px = static_cast<const T*>(P.img) + (off0 + img_base) * C;
+    load_run<C, T>(px, vec, valid, p);
+
+    // prefetch the carried-over centres (history tables) into shared memory;
+    // consumed after the candidate loop, so the gather latency is hidden
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      if (valid[v] && word[v] != kUndefined) {
+        const uint32_t L = P.codec.label(word[v]), Tg = P.codec.tag(word[v]);
+        const float2* hc = P.hist32 + ((int64_t)Tg * g.k + L) * kStride;
+#pragma unroll
+        for (int i = 0; i < kStride; ++i) cp_async8(my_stage + (v * kStride + i) * 32, hc + i);
+        cp_async4(my_chg + v * 32, P.chg + L);
+      }
+    }
+    cp_async_commit();
+
+    f2 p01[C], p23[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      p01[c] = pk2(p[0][c], p[1][c]);
+      p23[c] = pk2(p[2][c], p[3][c]);
+    }
+    const int ox = kHdr + (lx0 < RXp ? lx0 : 0);
+    const int oy = kHdr + RXp + 2 * (ly < RY ? ly : 0);
+    const int oz = kHdr + RXp + 2 * RY + 2 * (lz < RZ ? lz : 0);
+
+    // fp32 argmin with runner-up: keys = value with 3 low bits = index in group
+    uint32_t best[4], second[4];
+    int grp[4];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      best[v] = second[v] = 0xffffffffu;
+      grp[v] = 0;
+    }
+#pragma unroll 1
+    for (int g0 = 0; g0 < nlp; g0 += 8) {
+      uint32_t before[4];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) before[v] = best[v];
+      const int g1 = min(g0 + 8, nlp);
+      for (int jj = g0; jj < g1; jj += 2) {
+        uint32_t key[2][4];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const float* r = rec + sm.wl[warp][jj + h];
+          const ulonglong2 sxv = *reinterpret_cast<const ulonglong2*>(r + ox);
+          f2 syz = *reinterpret_cast<const f2*>(r + oy);
+          if (RANK == 3) syz = add2(syz, *reinterpret_cast<const f2*>(r + oz));
+          f2 a01 = add2(sxv.x, syz), a23 = add2(sxv.y, syz);
+#pragma unroll
+          for (int c = 0; c < C; ++c) {
+            const ulonglong2 hl = *reinterpret_cast<const ulonglong2*>(r + 4 * c);
+            const f2 d01 = add2(sub2(hl.x, p01[c]), hl.y);
+            const f2 d23 = add2(sub2(hl.x, p23[c]), hl.y);
+            a01 = fma2(d01, d01, a01);
+            a23 = fma2(d23, d23, a23);
+          }
+          float f0, f1, f2v, f3;
+          up2(a01, f0, f1);
+          up2(a23, f2v, f3);
+          const uint32_t jl = (uint32_t)((jj + h) & 7);
+          key[h][0] = fkey(f0, jl);
+          key[h][1] = fkey(f1, jl);
+          key[h][2] = fkey(f2v, jl);
+          key[h][3] = fkey(f3, jl);
+        }
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const uint32_t lo = min(key[0][v], key[1][v]);
+          const uint32_t hk = max(key[0][v], key[1][v]);
+          const uint32_t t = max(best[v], lo);
+          best[v] = min(best[v], lo);
+          second[v] = min3u(second[v], hk, t);
+        }
+      }
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+        if (best[v] != before[v]) grp[v] = g0;
+    }
+    cp_async_wait_all();
+
+    // ---- decisions ----
+    uint32_t newl[4], oldl[4];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      oldl[v] = newl[v] = P.codec.label(word[v]);
+      if (!valid[v]) continue;
+      uint32_t w = word[v];
+      if (best[v] >= 0x7f800000u) continue;  // no window covers the voxel: keep
+      const int jstar = sm.wj[warp][grp[v] + (best[v] & 7u)];
+      const float bv = kval(best[v]);
+      const bool amb_cand = second[v] < 0x7f800000u && kval(second[v]) <= bv * (1.0f + M) + A;
+      int decided = 0;  // 1 = update, 2 = keep, 0 = exact re-decision
+      if (!amb_cand) {
+        if (w == kUndefined) {
+          decided = 1;
+        } else {
+          const uint32_t L = oldl[v], Tg = P.codec.tag(w);
+          if ((uint32_t)sm.id[jstar] == L && my_chg[v * 32] <= (int)Tg) {
+            decided = 2;  // same centre as when the label was set: D* == d_old
+          } else {
+            const float2* hc = my_stage + v * kStride * 32;
+            float sp = 0.f;
+#pragma unroll
+            for (int a = 0; a < RANK; ++a) {
+              const float2 cc = hc[(C + a) * 32];
+              const float x = (float)(a == 0 ? lx0 + v : (a == 1 ? ly : lz)) + (float)org[a];
+              const float t = ((cc.x - x) + cc.y) * P.inv_grid[a];
+              sp = fmaf(t, t, sp);
+            }
+            float dold = sp * msq;
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+              const float2 cc = hc[c * 32];
+              const float d = (cc.x - p[v][c]) + cc.y;
+              dold = fmaf(d, d, dold);
+            }
+            if (bv * (1.0f + M) + A < dold) decided = 1;
+            else if (bv > dold * (1.0f + M) + A) decided = 2;
+          }
+        }
+      }
+      if (decided == 1) {
+        w = P.codec.pack((uint32_t)sm.id[jstar], P.tag_now);
+      } else if (decided == 0) {
+        ++n_redecided;
+        w = exact_region_voxel(P, sm, gx0 + v, gy, gz, (off0 + img_base + v) * C, w, amb_cand,
+                               jstar, org);
+      }
+      if (w != word[v]) P.labels[off0 + lab_base + v] = w;
+      newl[v] = P.codec.label(w);
+    }
+
+    // ---- delta accumulation: +new / -old for voxels whose label changed ----
+    unsigned pending = 0;  // bit v: +new[v]; bit 4+v: -old[v]
+    unsigned undef = 0;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      if (!valid[v]) continue;
+      undef += newl[v] == kUndefined;
+      if (newl[v] != oldl[v]) {
+        pending |= 1u << v;
+        if (oldl[v] != kUndefined) pending |= 1u << (4 + v);
+        ++n_changed;
+      }
+    }
+    if (__any_sync(0xffffffffu, undef != 0)) {
+      const unsigned tu = __reduce_add_sync(0xffffffffu, undef);
+      if (lane == 0) atomicAdd(P.counters, (unsigned long long)tu);  // slic.hpp:330-331
+    }
+#pragma unroll 1
+    for (;;) {
+      const unsigned any = __ballot_sync(0xffffffffu, pending != 0);
+      if (!any) break;
+      const int leader = __ffs(any) - 1;
+      uint32_t mylab = 0;
+      if (pending) {
+        const int bit = __ffs(pending) - 1;
+        mylab = bit < 4 ? newl[0] : oldl[0];
+#pragma unroll
+        for (int v = 1; v < 4; ++v)
+          if ((bit & 3) == v) mylab = bit < 4 ? newl[v] : oldl[v];
+      }
+      const uint32_t L = __shfl_sync(0xffffffffu, mylab, leader);
+      int cnt = 0, sxr = 0, syr = 0, szr = 0;
+      int sv32[C];
+      int64_t sv64[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        sv32[c] = 0;
+        sv64[c] = 0;
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int v = q & 3;
+        const uint32_t lq = q < 4 ? newl[v] : oldl[v];
+        if ((pending >> q & 1) && lq == L) {
+          pending &= ~(1u << q);
+          const int sgn = q < 4 ? 1 : -1;
+          cnt += sgn;
+          sxr += sgn * (lx0 + v);
+          syr += sgn * ly;
+          szr += sgn * lz;
+#pragma unroll
+          for (int c = 0; c < C; ++c) {
+            if (sizeof(T) < 4) sv32[c] += sgn * (int)p[v][c];
+            else sv64[c] += sgn * __float2ll_rn(p[v][c] * fscale);  // exact: |v| 2^s < 2^40
+          }
+        }
+      }
+      int tx, ty, tz, tc;
+      redux_pair(sxr, syr, tx, ty);
+      redux_pair(szr, cnt, tz, tc);
+      long long tvs[C];
+      if (sizeof(T) == 1) {
+#pragma unroll
+        for (int c = 0; c < C; c += 2) {
+          int a0, a1;
+          redux_pair(sv32[c], c + 1 < C ? sv32[c + 1] : 0, a0, a1);
+          tvs[c] = a0;
+          if (c + 1 < C) tvs[c + 1] = a1;
+        }
+      } else if (sizeof(T) == 2) {
+#pragma unroll
+        for (int c = 0; c < C; ++c) tvs[c] = (int)__reduce_add_sync(0xffffffffu, (uint32_t)sv32[c]);
+      } else {
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          const uint64_t u = (uint64_t)sv64[c];
+          const int32_t h = (int32_t)__reduce_add_sync(0xffffffffu, (uint32_t)(sv64[c] >> 32));
+          const uint32_t l1 = __reduce_add_sync(0xffffffffu, (uint32_t)(u & 0xffffu));
+          const uint32_t l2 = __reduce_add_sync(0xffffffffu, (uint32_t)((u >> 16) & 0xffffu));
+          tvs[c] = (long long)h * 4294967296LL + (long long)l2 * 65536LL + (long long)l1;
+        }
+      }
+      if (lane == leader) {
+        int S = -1;
+        for (int j = 0; j < n; ++j)
+          if ((uint32_t)sm.id[j] == L) {
+            S = j;
+            break;
+          }
+        if (S >= 0) {
+          unsigned long long* a = accs + S * kComp;
+#pragma unroll
+          for (int c = 0; c < C; ++c)
+            if (tvs[c]) atomicAdd(a + c, (unsigned long long)tvs[c]);
+          if (tx) atomicAdd(a + C, (unsigned long long)(long long)tx);
+          if (ty) atomicAdd(a + C + 1, (unsigned long long)(long long)ty);
+          if (RANK == 3 && tz) atomicAdd(a + C + 2, (unsigned long long)(long long)tz);
+          if (tc) atomicAdd(a + kStride, (unsigned long long)(long long)tc);
+        } else {
+          // label outside the region's candidates: global, absolute coordinates
+          unsigned long long* a = P.acc + (uint64_t)L * kComp;
+#pragma unroll
+          for (int c = 0; c < C; ++c)
+            if (tvs[c]) atomicAdd(a + c, (unsigned long long)tvs[c]);
+          atomicAdd(a + C, (unsigned long long)(tx + (long long)tc * org[0]));
+          atomicAdd(a + C + 1, (unsigned long long)(ty + (long long)tc * org[1]));
+          if (RANK == 3) atomicAdd(a + C + 2, (unsigned long long)(tz + (long long)tc * org[2]));
+          if (tc) atomicAdd(a + kStride, (unsigned long long)(long long)tc);
+        }
+      }
+    }
+  }
+  if (P.eval_count) {
+    const unsigned a = __reduce_add_sync(0xffffffffu, n_redecided);
+    const unsigned c = __reduce_add_sync(0xffffffffu, n_changed);
+    const unsigned e = __reduce_add_sync(0xffffffffu, n_evals);
+    if (lane == 0) {
+      atomicAdd(P.counters + 5, (unsigned long long)a);
+      atomicAdd(P.counters + 7, (unsigned long long)c);
+      atomicAdd(P.eval_count, (unsigned long long)e);
+    }
+  }
+  __syncthreads();
+  // ---- flush CTA slots (one global atomic per non-zero component) ----
+  for (int e = tid; e < n * kComp; e += kFastThreads) {
+    const int j = e / kComp, i = e - j * kComp;
+    long long v = (long long)accs[e];
+    if (i >= C && i < kStride) v += (long long)accs[j * kComp + kStride] * org[i - C];
+    if (v) atomicAdd(P.acc + (uint64_t)sm.id[j] * kComp + i, (unsigned long long)v);
+  }
+}
+
+// hi/lo fp32 split of one centre table (for the fp32 d_old filter).
+static __global__ void k_split32(const double* c, float2* out, int64_t n) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float h = __double2float_rn(c[i]);
+  out[i] = make_float2(h, __double2float_rn(c[i] - (double)h));
+}
+
+inline bool fast_path_supported(const Geom& g) {
+  if (g.rank != 2 && g.rank != 3) return false;
+  if (g.channels < 1 || g.channels > 4) return false;
+  if (g.dtype != SSLIC_U8 && g.dtype != SSLIC_U16 && g.dtype != SSLIC_F32) return false;
+  for (int a = 0; a < g.rank; ++a)
+    if (g.grid[a] > kFastMaxR) return false;
+  if (g.k >= (int64_t)1 << 30) return false;
+  for (int a = 0; a < g.rank; ++a)
+    if (g.dims[a] >= ((int64_t)1 << 30)) return false;
+  return true;
+}
+
+// Region extent per axis: a multiple of S, at least 16 voxels (and <= 64).
+inline int region_extent(int s) {
+  int f = (16 + s - 1) / s;
+  int r = f * s;
+  while (r > kFastMaxR && f > 1) r = --f * s;
+  return r;
+}
+
+inline size_t fast_smem_bytes(const Geom& g, const int* R) {
+  const int RXp = (R[0] + 3) & ~3;
+  const int RS = (4 * g.channels + RXp + 2 * R[1] + (g.rank == 3 ? 2 * R[2] : 0) + 3) & ~3;
+  const int warps = kFastThreads / 32;
+  size_t b = sizeof(FastSmem);
+  b += (size_t)(kFastMaxCand + 1) * RS * sizeof(float);
+  b += (size_t)kFastMaxCand * (g.stride + 1) * sizeof(unsigned long long);
+  b += (size_t)warps * 4 * g.stride * 32 * sizeof(float2);
+  b += (size_t)warps * 4 * 32 * sizeof(int);
+  return b;
+}
+
+template <int RANK, int C, typename T>
+void launch_fast_t(const FastParams& P, size_t smem, int64_t nblocks, cudaStream_t s) {
+  auto kern = k_assign_fast<RANK, C, T>;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    configured = true;
+  }
+  kern<<<(unsigned)nblocks, kFastThreads, smem, s>>>(P);
+}
+
+template <int RANK, int C>
+void launch_fast_c(const FastParams& P, size_t smem, int64_t nb, cudaStream_t s) {
+  switch (P.g.dtype) {
+    case SSLIC_U8: launch_fast_t<RANK, C, uint8_t>(P, smem, nb, s); break;
+    case SSLIC_U16: launch_fast_t<RANK, C, uint16_t>(P, smem, nb, s); break;
+    default: launch_fast_t<RANK, C, float>(P, smem, nb, s); break;
+  }
+}
+
+template <int RANK>
+void launch_fast_r(const FastParams& P, size_t smem, int64_t nb, cudaStream_t s) {
+  switch (P.g.channels) {
+    case 1: launch_fast_c<RANK, 1>(P, smem, nb, s); break;
+    case 2: launch_fast_c<RANK, 2>(P, smem, nb, s); break;
+    case 3: launch_fast_c<RANK, 3>(P, smem, nb, s); break;
+    default: launch_fast_c<RANK, 4>(P, smem, nb, s); break;
+  }
+}
+
+// Relative fp32 decision margin: each fp32
+// distance is within (C + 12) u of the fp64 one (u = 2^-24; includes the
+// reciprocal-multiply of the d_old filter) and keys are truncated by < 8 ulp
+// (2^-20 relative); 2x for the two sides, 1.5x slack.
+inline float fast_margin(int channels) {
+  const double u = 1.0 / 16777216.0;
+  return (float)(1.5 * (2.0 * (channels + 12) * u + 1.0 / 1048576.0));
+}
+
+inline void launch_fast_assign(FastParams P, cudaStream_t s) {
+  const Geom& g = P.g;
+  for (int a = 0; a < 3; ++a) {
+    P.R[a] = a < g.rank ? region_extent(g.grid[a]) : 1;
+    P.inv_grid[a] = 1.0f / (float)g.grid[a];
+  }
+  P.nreg[0] = (int)((g.dims[0] + P.R[0] - 1) / P.R[0]);
+  P.nreg[1] = (int)((g.dims[1] + P.R[1] - 1) / P.R[1]);
+  if (g.rank == 3) {
+    const int64_t z0 = g.slab_begin / P.R[2] * P.R[2];
+    P.reg_z0 = z0;
+    P.nreg[2] = (int)((g.slab_end - z0 + P.R[2] - 1) / P.R[2]);
+  } else {
+    P.reg_z0 = 0;
+    P.nreg[2] = 1;
+  }
+  P.margin = fast_margin(g.channels);
+  // vector loads of 4-voxel runs need 4 | dims[0], 4 | RX and 16-byte bases
+  P.aligned4 = (g.dims[0] % 4 == 0 && P.R[0] % 4 == 0 &&
+                reinterpret_cast<uintptr_t>(P.img) % 16 == 0 &&
+                reinterpret_cast<uintptr_t>(P.labels) % 16 == 0)
+                   ? 1
+                   : 0;
+  const int64_t nb = (int64_t)P.nreg[0] * P.nreg[1] * P.nreg[2];
+  const size_t smem = fast_smem_bytes(g, P.R);
+  if (g.rank == 3) launch_fast_r<3>(P, smem, nb, s);
+  else launch_fast_r<2>(P, smem, nb, s);
+}
+
+}  // namespace sslic_b200
