@@ -61,6 +61,7 @@ struct FastParams {
   float margin;       // relative fp32 decision margin
   float abs_margin;   // absolute term (hi/lo split residue)
   float inv_grid[3];  // fl32(1/S_a) (d_old filter; its rounding is in the margin)
+  double inv_grid64[3];
   int aligned4;       // dims[0] % 4 == 0: 4-voxel runs are vector-aligned
 };
 
@@ -78,7 +79,23 @@ struct alignas(16) FastSmem {
   int anc[kFastMaxCand][3];
   unsigned short wl[kFastThreads / 32][kFastMaxCand + 2];   // record offsets (floats)
   unsigned char wj[kFastThreads / 32][kFastMaxCand + 2];    // candidate slots
+  int htab[2 * kFastMaxCand];                               // cluster id -> slot
 };
+
+constexpr int kSlotHash = 2 * kFastMaxCand;
+// up to this many delta contributions per warp box, lanes add their own
+// contributions directly (sparse path); above it, warp-aggregate per label
+constexpr unsigned kSparseDeltas = 24;
+__device__ __forceinline__ int slot_hash(uint32_t id) { return (int)((id * 0x9E3779B1u) >> 25); }
+// Slot of cluster `id` in the region's candidate list, -1 if absent.
+__device__ __forceinline__ int slot_of(const FastSmem& sm, uint32_t id) {
+  int h = slot_hash(id);
+  for (;;) {
+    const int s = sm.htab[h];
+    if (s < 0 || (uint32_t)sm.id[s] == id) return s;
+    h = (h + 1) & (kSlotHash - 1);
+  }
+}
 
 // ---- fp32x2 (sm_100a paired FP32) --------------------------------------------
 typedef unsigned long long f2;

@@ -182,12 +182,18 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
     }
   }
   for (int i = tid; i < n * kComp; i += kFastThreads) accs[i] = 0ull;
+  for (int i = tid; i < kSlotHash; i += kFastThreads) sm.htab[i] = -1;
   __syncthreads();
+  for (int j = tid; j < n; j += kFastThreads) {  // id -> slot hash (linear probing)
+    int h = slot_hash((uint32_t)sm.id[j]);
+    while (atomicCAS(&sm.htab[h], -1, j) != -1) h = (h + 1) & (kSlotHash - 1);
+  }
   {
+    // spatial tables: one warp per candidate, lanes over the table entries
     const int per = RX + RY + (RANK == 3 ? RZ : 0);
-    for (int e = tid; e < (n + 1) * per; e += kFastThreads) {
-      const int j = e / per;
-      int r = e - j * per, a = 0;
+    for (int j = warp; j <= n; j += kWarps)
+    for (int r0 = lane; r0 < per; r0 += 32) {
+      int r = r0, a = 0;
       if (r >= RX) {
         r -= RX;
         a = 1;
@@ -204,7 +210,8 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
         const int dx = r - an;
         if (dx >= -s && dx <= s) {
           const int64_t x = (a == 0 ? org[0] : (a == 1 ? org[1] : org[2])) + r;
-          const double t = (P.centers[(int64_t)kid * g.stride + C + a] - (double)x) / (double)s;
+          // filter table: (c - x) * (1/S) in fp64 (its rounding is far below the margin)
+          const double t = (P.centers[(int64_t)kid * g.stride + C + a] - (double)x) * P.inv_grid64[a];
           v = __double2float_rn(g.m_sq * (t * t));
         }
       }
@@ -239,9 +246,18 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
   int* my_chg = stage_chg + warp * 4 * 32 + lane;
   unsigned n_changed = 0, n_redecided = 0, n_evals = 0;
 
+  int bx = warp % nbx, by = (warp / nbx) % nby, bz = warp / (nbx * nby);
+  bx -= kWarps;  // pre-decrement: the loop head advances by kWarps boxes
 #pragma unroll 1
   for (int b = warp; b < nbox; b += kWarps) {
-    const int bx = b % nbx, by = (b / nbx) % nby, bz = b / (nbx * nby);
+    bx += kWarps;
+    while (bx >= nbx) {
+      bx -= nbx;
+      if (++by >= nby) {
+        by = 0;
+        ++bz;
+      }
+    }
     // box bounds in region-local coordinates, clipped
     const int bx0 = bx * Box::X, by0 = by * Box::Y, bz0 = bz * Box::Z;
     const int bx1 = min(bx0 + Box::X - 1, ex), by1 = min(by0 + Box::Y - 1, ey);
@@ -466,6 +482,42 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
       const unsigned tu = __reduce_add_sync(0xffffffffu, undef);
       if (lane == 0) atomicAdd(P.counters, (unsigned long long)tu);  // slic.hpp:330-331
     }
+    // Sparse deltas (the common case after the first iterations): each lane
+    // adds its own contributions straight into the CTA slots. Dense deltas
+    // (first iterations): warp-aggregate per label first.
+    const unsigned npend = __reduce_add_sync(0xffffffffu, (unsigned)__popc(pending));
+    if (npend <= kSparseDeltas) {
+      while (pending) {
+        const int q = __ffs(pending) - 1;
+        pending &= pending - 1;
+        const int v = q & 3;
+        const long long sgn = q < 4 ? 1 : -1;
+        uint32_t L = q < 4 ? newl[0] : oldl[0];
+        float pv[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) pv[c] = p[0][c];
+#pragma unroll
+        for (int u = 1; u < 4; ++u)
+          if (v == u) {
+            L = q < 4 ? newl[u] : oldl[u];
+#pragma unroll
+            for (int c = 0; c < C; ++c) pv[c] = p[u][c];
+          }
+        const int S = slot_of(sm, L);
+        const long long co[3] = {lx0 + v, ly, lz};
+        unsigned long long* a = S >= 0 ? accs + S * kComp : P.acc + (uint64_t)L * kComp;
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          const long long val =
+              sizeof(T) < 4 ? (long long)pv[c] : (long long)__float2ll_rn(pv[c] * fscale);
+          atomicAdd(a + c, (unsigned long long)(sgn * val));
+        }
+#pragma unroll
+        for (int ax = 0; ax < RANK; ++ax)
+          atomicAdd(a + C + ax, (unsigned long long)(sgn * (co[ax] + (S >= 0 ? 0 : org[ax]))));
+        atomicAdd(a + kStride, (unsigned long long)sgn);
+      }
+    }
 #pragma unroll 1
     for (;;) {
       const unsigned any = __ballot_sync(0xffffffffu, pending != 0);
@@ -532,12 +584,7 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
         }
       }
       if (lane == leader) {
-        int S = -1;
-        for (int j = 0; j < n; ++j)
-          if ((uint32_t)sm.id[j] == L) {
-            S = j;
-            break;
-          }
+        const int S = slot_of(sm, L);
         if (S >= 0) {
           unsigned long long* a = accs + S * kComp;
 #pragma unroll
@@ -573,11 +620,12 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
   }
   __syncthreads();
   // ---- flush CTA slots (one global atomic per non-zero component) ----
-  for (int e = tid; e < n * kComp; e += kFastThreads) {
-    const int j = e / kComp, i = e - j * kComp;
-    long long v = (long long)accs[e];
-    if (i >= C && i < kStride) v += (long long)accs[j * kComp + kStride] * org[i - C];
-    if (v) atomicAdd(P.acc + (uint64_t)sm.id[j] * kComp + i, (unsigned long long)v);
+  for (int j = warp; j < n; j += kWarps) {
+    if (lane < kComp) {
+      long long v = (long long)accs[j * kComp + lane];
+      if (lane >= C && lane < kStride) v += (long long)accs[j * kComp + kStride] * org[lane - C];
+      if (v) atomicAdd(P.acc + (uint64_t)sm.id[j] * kComp + lane, (unsigned long long)v);
+    }
   }
 }
 
@@ -665,6 +713,7 @@ inline void launch_fast_assign(FastParams P, cudaStream_t s) {
   for (int a = 0; a < 3; ++a) {
     P.R[a] = a < g.rank ? region_extent(g.grid[a]) : 1;
     P.inv_grid[a] = 1.0f / (float)g.grid[a];
+    P.inv_grid64[a] = 1.0 / (double)g.grid[a];
   }
   P.nreg[0] = (int)((g.dims[0] + P.R[0] - 1) / P.R[0]);
   P.nreg[1] = (int)((g.dims[1] + P.R[1] - 1) / P.R[1]);

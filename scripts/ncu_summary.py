@@ -1,0 +1,42 @@
+"""Summarise an ncu report: headline metrics + per-source-line instruction and
+stall shares (needs -lineinfo builds and --import-source on)."""
+import csv, io, subprocess, sys
+from collections import defaultdict
+
+rep = sys.argv[1]
+def run(args):
+    return subprocess.run(["ncu", "-i", rep] + args, capture_output=True, text=True).stdout
+
+det = run(["--page", "details", "--csv"])
+keys = ["Duration", "Executed Ipc Active", "Issue Slots Busy", "Warp Cycles Per Issued Instruction",
+        "No Eligible", "Registers Per Thread", "Achieved Occupancy", "DRAM Throughput",
+        "L1/TEX Hit Rate", "L2 Hit Rate", "Dynamic Shared Memory Per Block", "Memory Throughput"]
+for row in csv.reader(io.StringIO(det)):
+    if len(row) > 3 and row[-3] in keys:
+        print(f"{row[-3]:40s} {row[-1]:>14s} {row[-2]}")
+src = run(["--page", "source", "--csv", "--print-source=cuda,sass"])
+rows = list(csv.reader(io.StringIO(src)))
+hdr = next((r for r in rows if "Instructions Executed" in r), None)
+if hdr is None:
+    sys.exit(0)
+ie = hdr.index("Instructions Executed"); ss = hdr.index("Warp Stall Sampling (All Samples)")
+agg = defaultdict(lambda: [0, 0, ""])
+cur_file, cur = "?", "?"
+for r in rows:
+    if not r:
+        continue
+    if r[0] == "File Path":
+        cur_file = r[1].split("/")[-1]
+        continue
+    if r[0] and r[0].isdigit():
+        cur = f"{cur_file}:{r[0]}"
+        agg[cur][2] = r[1].strip()[:80]
+        continue
+    if len(r) > ss and r[2].startswith("0x"):
+        agg[cur][0] += int(r[ie] or 0)
+        agg[cur][1] += int(r[ss] or 0)
+tot = sum(v[0] for v in agg.values()) or 1; st = sum(v[1] for v in agg.values()) or 1
+print("total warp instrs %.4g, stall samples %d" % (tot, st))
+n = int(sys.argv[2]) if len(sys.argv) > 2 else 40
+for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1])[:n]:
+    print(f"{k:>28s} instr {100*v[0]/tot:5.1f}% stall {100*v[1]/st:5.1f}%  {v[2]}")
