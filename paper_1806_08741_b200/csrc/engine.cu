@@ -72,7 +72,7 @@ Engine::Engine(const sslic_image& img, const sslic_params& p, int device, int64_
   if (dist_mode_) {
     dists_ = dalloc<double>(nv, s);  // filled with +inf below (DistanceMap, image.hpp:323)
   } else {
-    hist32_ = dalloc<float2>((size_t)n_tables_ * g_.k * g_.stride, s);
+    hist32_ = dalloc<float2>((size_t)n_tables_ * g_.k * hist32_stride(g_.stride), s);
     chg_ = dalloc<int>(g_.k, s);
     SSLIC_CUDA_CHECK(cudaMemsetAsync(chg_, 0, g_.k * sizeof(int), s));
   }
@@ -179,9 +179,9 @@ void Engine::commit() {
   k_bin_sort<<<blocks_for(g_.ncells, 256), 256, 0, s>>>(g_.ncells, cell_start_, items_);
   launch_check("bin_sort");
   if (!dist_mode_) {
-    const int64_t nc = centers_count();
-    k_split32<<<blocks_for(nc, 256), 256, 0, s>>>(
-        current_centers(), hist32_ + (size_t)iter_ * g_.k * g_.stride, nc);
+    const int s2 = hist32_stride(g_.stride);
+    k_split32<<<blocks_for(g_.k * s2, 256), 256, 0, s>>>(
+        current_centers(), hist32_ + (size_t)iter_ * g_.k * s2, g_.k, g_.stride);
     launch_check("split32");
   }
 }

@@ -83,6 +83,8 @@ struct alignas(16) FastSmem {
 };
 
 constexpr int kSlotHash = 2 * kFastMaxCand;
+// float2 entries per hi/lo history row, padded to a 16-byte multiple
+__host__ __device__ constexpr int hist32_stride(int stride) { return (stride + 1) & ~1; }
 // up to this many delta contributions per warp box, lanes add their own
 // contributions directly (sparse path); above it, warp-aggregate per label
 constexpr unsigned kSparseDeltas = 24;

@@ -11,6 +11,10 @@ __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gsrc) : "memory");
 }
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gsrc) : "memory");
+}
 __device__ __forceinline__ void cp_async4(void* smem_dst, const void* gsrc) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(gsrc) : "memory");
@@ -73,6 +77,7 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
   using Box = BoxShape<RANK>;
   constexpr int kStride = C + RANK;
   constexpr int kComp = kStride + 1;
+  constexpr int kS2 = (kStride + 1) & ~1;  // hi/lo history entry, padded to 16 B
   constexpr int kHdr = 4 * C;  // (hi, hi, lo, lo) per channel
   constexpr int kWarps = kFastThreads / 32;
   const Geom& g = P.g;
@@ -86,7 +91,7 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
       reinterpret_cast<unsigned long long*>(rec + (size_t)(kFastMaxCand + 1) * RS);
   // per-warp staging of the carried-over centres: [warp][v][i][lane] float2, chg [warp][v][lane]
   float2* stage = reinterpret_cast<float2*>(accs + kFastMaxCand * kComp);
-  int* stage_chg = reinterpret_cast<int*>(stage + kWarps * 4 * kStride * 32);
+  int* stage_chg = reinterpret_cast<int*>(stage + kWarps * 4 * kS2 * 32);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // ---- region ----
@@ -242,7 +247,8 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
   const float msq = (float)g.m_sq;
   const int64_t lab_base = -g.slab_begin * g.plane;
   const int64_t img_base = -g.data_begin * g.plane;
-  float2* my_stage = stage + (size_t)warp * 4 * kStride * 32 + lane;
+  // [warp][v][lane][kS2]: each lane's entry is contiguous (16-byte cp.async)
+  float2* my_stage = stage + ((size_t)warp * 4 * 32 + lane) * kS2;
   int* my_chg = stage_chg + warp * 4 * 32 + lane;
   unsigned n_changed = 0, n_redecided = 0, n_evals = 0;
 
@@ -336,13 +342,18 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
 
     // prefetch the carried-over centres (history tables) into shared memory;
     // consumed after the candidate loop, so the gather latency is hidden
+    // (once per distinct label word of the lane's run: rep[v] = first voxel
+    // of the run carrying the same word)
+    int rep[4];
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
-      if (valid[v] && word[v] != kUndefined) {
+      rep[v] = v;
+      if (v > 0 && word[v] == word[v - 1]) rep[v] = rep[v - 1];
+      if (rep[v] == v && valid[v] && word[v] != kUndefined) {
         const uint32_t L = P.codec.label(word[v]), Tg = P.codec.tag(word[v]);
-        const float2* hc = P.hist32 + ((int64_t)Tg * g.k + L) * kStride;
+        const float2* hc = P.hist32 + ((int64_t)Tg * g.k + L) * kS2;
 #pragma unroll
-        for (int i = 0; i < kStride; ++i) cp_async8(my_stage + (v * kStride + i) * 32, hc + i);
+        for (int i = 0; i < kS2; i += 2) cp_async16(my_stage + v * 32 * kS2 + i, hc + i);
         cp_async4(my_chg + v * 32, P.chg + L);
       }
     }
@@ -430,14 +441,14 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
           decided = 1;
         } else {
           const uint32_t L = oldl[v], Tg = P.codec.tag(w);
-          if ((uint32_t)sm.id[jstar] == L && my_chg[v * 32] <= (int)Tg) {
+          if ((uint32_t)sm.id[jstar] == L && my_chg[rep[v] * 32] <= (int)Tg) {
             decided = 2;  // same centre as when the label was set: D* == d_old
           } else {
-            const float2* hc = my_stage + v * kStride * 32;
+            const float2* hc = my_stage + rep[v] * 32 * kS2;
             float sp = 0.f;
 #pragma unroll
             for (int a = 0; a < RANK; ++a) {
-              const float2 cc = hc[(C + a) * 32];
+              const float2 cc = hc[C + a];
               const float x = (float)(a == 0 ? lx0 + v : (a == 1 ? ly : lz)) + (float)org[a];
               const float t = ((cc.x - x) + cc.y) * P.inv_grid[a];
               sp = fmaf(t, t, sp);
@@ -445,7 +456,7 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
             float dold = sp * msq;
 #pragma unroll
             for (int c = 0; c < C; ++c) {
-              const float2 cc = hc[c * 32];
+              const float2 cc = hc[c];
               const float d = (cc.x - p[v][c]) + cc.y;
               dold = fmaf(d, d, dold);
             }
@@ -629,12 +640,21 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
   }
 }
 
-// hi/lo fp32 split of one centre table (for the fp32 d_old filter).
-static __global__ void k_split32(const double* c, float2* out, int64_t n) {
+// hi/lo fp32 split of one centre table (for the fp32 d_old filter); entries
+// padded to hist32_stride(stride) float2 (16-byte multiples, zero padding).
+static __global__ void k_split32(const double* c, float2* out, int64_t k, int stride) {
+  const int s2 = hist32_stride(stride);
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const float h = __double2float_rn(c[i]);
-  out[i] = make_float2(h, __double2float_rn(c[i] - (double)h));
+  if (i >= k * s2) return;
+  const int64_t id = i / s2;
+  const int comp = (int)(i - id * s2);
+  if (comp >= stride) {
+    out[i] = make_float2(0.f, 0.f);
+    return;
+  }
+  const double v = c[id * stride + comp];
+  const float h = __double2float_rn(v);
+  out[i] = make_float2(h, __double2float_rn(v - (double)h));
 }
 
 inline bool fast_path_supported(const Geom& g) {
@@ -664,7 +684,7 @@ inline size_t fast_smem_bytes(const Geom& g, const int* R) {
   size_t b = sizeof(FastSmem);
   b += (size_t)(kFastMaxCand + 1) * RS * sizeof(float);
   b += (size_t)kFastMaxCand * (g.stride + 1) * sizeof(unsigned long long);
-  b += (size_t)warps * 4 * g.stride * 32 * sizeof(float2);
+  b += (size_t)warps * 4 * hist32_stride(g.stride) * 32 * sizeof(float2);
   b += (size_t)warps * 4 * 32 * sizeof(int);
   return b;
 }
