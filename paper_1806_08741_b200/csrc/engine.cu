@@ -104,8 +104,19 @@ Engine::Engine(const sslic_image& img, const sslic_params& p, int device, int64_
     const double e = vmax_ * std::ldexp(1.0, -48);
     const double M = fast_margin(g_.channels);
     abs_margin_ = (float)(8.0 * e * e / M + e * e + 1e-37);
+    // key scale 2^-k: the largest possible fp32 distance of a covered
+    // candidate, C (2 vmax + 1)^2 + m^2 rank 4, must map below 2^-67
+    // (kernels_fast.cuh "Keys"). Exact power-of-two scaling.
+    const double dmax = g_.channels * (2.0 * vmax_ + 1.0) * (2.0 * vmax_ + 1.0) +
+                        g_.m_sq * g_.rank * 4.0 + 1.0;
+    const int k = (int)std::ceil((std::log2(dmax) + 67.0) / 2.0);
+    key_scale_ = (float)std::ldexp(1.0, -k);
+    if (!(k < 120)) fast_ok_scale_ = false;  // absurd ranges: keep the exact path
   }
-  path_ = fast_path_supported(g_) && !dist_mode_ ? AssignPath::kFast : AssignPath::kExact;
+  path_ = fast_path_supported(g_) && !dist_mode_ && fast_ok_scale_ ? AssignPath::kFast
+                                                                    : AssignPath::kExact;
+  if (path_ == AssignPath::kFast)
+    region_cand_ = dalloc<int>((size_t)fast_region_count(g_) * kRegionCandStride, s);
 }
 
 Engine::~Engine() {
@@ -113,7 +124,7 @@ Engine::~Engine() {
   cudaStream_t s = stream_;
   void* ptrs[] = {centers_, labels_, dists_, acc_, anchors_, cell_of_, cell_count_,
                   cell_start_, cursor_, items_, scan_tmp_, block_partials_, residuals_,
-                  counters_, hist32_, chg_, sums_};
+                  counters_, hist32_, chg_, sums_, region_cand_};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, s);
   cudaStreamSynchronize(s);
@@ -237,7 +248,13 @@ void Engine::launch_assign_kernel(bool accumulate) {
     P.counters = counters_;
     P.eval_count = collect_stats_ ? counters_ + 2 : nullptr;
     P.abs_margin = abs_margin_;
+    P.cur32 = hist32_ + (size_t)iter_ * g_.k * hist32_stride(g_.stride);
+    P.key_scale = key_scale_;
+    P.key_scale2 = key_scale_ * key_scale_;
+    P.abs_margin = abs_margin_ * P.key_scale2;
+    P.region_cand = region_cand_;
     launch_fast_assign(P, s);
+    ++launches_;  // k_region_cand + k_assign_fast
     launch_check("assign_fast");
     return;
   }

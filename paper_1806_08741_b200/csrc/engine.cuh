@@ -105,6 +105,9 @@ class Engine {
   int64_t launches_ = 0;
   float2* hist32_ = nullptr;  // hi/lo fp32 split of every history table
   int* chg_ = nullptr;        // per cluster: first table index of its current centre
+  int* region_cand_ = nullptr;  // fast path: per-region candidate lists
+  float key_scale_ = 1.f;       // fast path: 2^-k operand scaling of the fp32 keys
+  bool fast_ok_scale_ = true;
   double vmax_ = 0.0;
   float abs_margin_ = 0.f;
   std::vector<cudaEvent_t> ev_start_, ev_stop_;

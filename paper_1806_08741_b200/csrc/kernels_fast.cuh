@@ -62,6 +62,11 @@ struct FastParams {
   float abs_margin;   // absolute term (hi/lo split residue)
   float inv_grid[3];  // fl32(1/S_a) (d_old filter; its rounding is in the margin)
   double inv_grid64[3];
+  const float2* cur32;      // hi/lo split of the current table (padded rows)
+  float key_scale;          // 2^-k: fp32 distances are computed on scaled operands
+  float key_scale2;         // 2^-2k
+  const int* region_cand;   // per region: [count, ids...] (k_region_cand)
+  int* region_cand_out;     // same buffer, written by k_region_cand
   int aligned4;       // dims[0] % 4 == 0: 4-voxel runs are vector-aligned
 };
 
@@ -83,6 +88,7 @@ struct alignas(16) FastSmem {
 };
 
 constexpr int kSlotHash = 2 * kFastMaxCand;
+constexpr int kRegionCandStride = kFastMaxCand + 1;  // [count, ids...] per region
 // float2 entries per hi/lo history row, padded to a 16-byte multiple
 __host__ __device__ constexpr int hist32_stride(int stride) { return (stride + 1) & ~1; }
 // up to this many delta contributions per warp box, lanes add their own
@@ -125,10 +131,17 @@ __device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
   return r;
 }
 
+// Keys: every fp32 distance is pre-scaled by 2^-2k (exact) so that real
+// distances are < 2^-67 and any sum with uncovered-axis sentinels (2^-66
+// each, at most 3) stays < 2^-63, i.e. below bit pattern 2^29. Then
+// key = bits * 8 + j orders by (D, j) lexicographically with no mantissa
+// lost, and is one IMAD (FMA pipe); keys >= kSentKey mean "not covered".
 __device__ __forceinline__ uint32_t fkey(float d, uint32_t j) {
-  return (__float_as_uint(d) & ~7u) | j;
+  return __float_as_uint(d) * 8u + j;
 }
-__device__ __forceinline__ float kval(uint32_t key) { return __uint_as_float(key & ~7u); }
+__device__ __forceinline__ float kval(uint32_t key) { return __uint_as_float(key >> 3); }
+constexpr uint32_t kSentKey = 0x1E800000u * 8u;        // fkey(2^-66, 0)
+constexpr float kSentinel = 1.3552527156068805e-20f;   // 2^-66
 __device__ __forceinline__ uint32_t min3u(uint32_t a, uint32_t b, uint32_t c) {
   return min(min(a, b), c);
 }

@@ -111,46 +111,14 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
   const int ex = (int)(hi[0] - org[0]), ey = (int)(hi[1] - org[1]);
   const int ez_lo = (int)(zlo - org[2]), ez_hi = (int)(zhi - org[2]);
 
-  // ---- gather candidates (warp 0) ----
-  if (warp == 0) {
-    int clo[3], chi[3], nc = 1;
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      if (a < RANK) {
-        const int64_t lo_a = a == 2 ? zlo : org[a];
-        const int64_t hi_a = a == 2 ? zhi : hi[a];
-        const int64_t l = lo_a - g.grid[a];
-        clo[a] = l < 0 ? 0 : (int)(l / g.grid[a]);
-        const int64_t h = (hi_a + g.grid[a]) / g.grid[a];
-        chi[a] = h > g.cells[a] - 1 ? g.cells[a] - 1 : (int)h;
-      } else {
-        clo[a] = chi[a] = 0;
-      }
-      nc *= chi[a] - clo[a] + 1;
-    }
-    int total = 0;
-    for (int base = 0; base < nc; base += 32) {
-      const int i = base + lane;
-      int cnt = 0, cstart = 0;
-      if (i < nc) {
-        const int nx = chi[0] - clo[0] + 1, ny = chi[1] - clo[1] + 1;
-        const int cx = clo[0] + i % nx, cy = clo[1] + (i / nx) % ny, cz = clo[2] + i / (nx * ny);
-        const int64_t cell = ((int64_t)cz * g.cells[1] + cy) * g.cells[0] + cx;
-        cstart = P.cell_start[cell];
-        cnt = P.cell_start[cell + 1] - cstart;
-      }
-      int incl = cnt;
-      for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
-      }
-      const int excl = total + incl - cnt;
-      for (int q = 0; q < cnt; ++q)
-        if (excl + q < kFastMaxCand) sm.id[excl + q] = P.items[cstart + q];
-      total += __shfl_sync(0xffffffffu, incl, 31);
-    }
-    if (lane == 0) {
-      sm.n_cand = total < kFastMaxCand ? total : kFastMaxCand;
+  // ---- candidates of this region (precomputed by k_region_cand) ----
+  {
+    const int* rc = P.region_cand + (int64_t)blockIdx.x * kRegionCandStride;
+    const int total = __ldg(rc);
+    const int nn = total < kFastMaxCand ? total : kFastMaxCand;
+    for (int j = tid; j < nn; j += kFastThreads) sm.id[j] = __ldg(rc + 1 + j);
+    if (tid == 0) {
+      sm.n_cand = nn;
       sm.overflow = total > kFastMaxCand;
     }
   }
@@ -167,15 +135,14 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
     float* r = rec + (size_t)j * RS;
     if (j < n) {
       const int kid = sm.id[j];
-      const double* ctr = P.centers + (int64_t)kid * g.stride;
+      const float2* c32 = P.cur32 + (int64_t)kid * kS2;  // hi/lo split of the current table
 #pragma unroll
       for (int c = 0; c < C; ++c) {
-        const float h = __double2float_rn(ctr[c]);
-        const float l = __double2float_rn(ctr[c] - (double)h);
-        r[4 * c] = h;
-        r[4 * c + 1] = h;
-        r[4 * c + 2] = l;
-        r[4 * c + 3] = l;
+        const float2 hl = __ldg(c32 + c);
+        r[4 * c] = hl.x * P.key_scale;  // power-of-two scaling: exact
+        r[4 * c + 1] = hl.x * P.key_scale;
+        r[4 * c + 2] = hl.y * P.key_scale;
+        r[4 * c + 3] = hl.y * P.key_scale;
       }
       // anchors stored region-local (32-bit)
 #pragma unroll
@@ -207,17 +174,18 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
           a = 2;
         }
       }
-      float v = kInf;
+      float v = kSentinel;
       if (j < n) {
         const int kid = sm.id[j];
         const int an = a == 0 ? sm.anc[j][0] : (a == 1 ? sm.anc[j][1] : sm.anc[j][2]);
         const int s = g.grid[a];
         const int dx = r - an;
         if (dx >= -s && dx <= s) {
-          const int64_t x = (a == 0 ? org[0] : (a == 1 ? org[1] : org[2])) + r;
-          // filter table: (c - x) * (1/S) in fp64 (its rounding is far below the margin)
-          const double t = (P.centers[(int64_t)kid * g.stride + C + a] - (double)x) * P.inv_grid64[a];
-          v = __double2float_rn(g.m_sq * (t * t));
+          const float x = (float)((a == 0 ? org[0] : (a == 1 ? org[1] : org[2])) + r);
+          // fp32 filter table from the hi/lo centre split (error in the margin)
+          const float2 cc = __ldg(P.cur32 + (int64_t)kid * kS2 + C + a);
+          const float t = ((cc.x - x) + cc.y) * P.inv_grid[a];
+          v = (float)g.m_sq * (t * t) * P.key_scale2;
         }
       }
       float* rj = rec + (size_t)j * RS + kHdr;
@@ -362,8 +330,8 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
     f2 p01[C], p23[C];
 #pragma unroll
     for (int c = 0; c < C; ++c) {
-      p01[c] = pk2(p[0][c], p[1][c]);
-      p23[c] = pk2(p[2][c], p[3][c]);
+      p01[c] = pk2(p[0][c] * P.key_scale, p[1][c] * P.key_scale);
+      p23[c] = pk2(p[2][c] * P.key_scale, p[3][c] * P.key_scale);
     }
     const int ox = kHdr + (lx0 < RXp ? lx0 : 0);
     const int oy = kHdr + RXp + 2 * (ly < RY ? ly : 0);
@@ -431,10 +399,10 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
       oldl[v] = newl[v] = P.codec.label(word[v]);
       if (!valid[v]) continue;
       uint32_t w = word[v];
-      if (best[v] >= 0x7f800000u) continue;  // no window covers the voxel: keep
+      if (best[v] >= kSentKey) continue;  // no window covers the voxel: keep
       const int jstar = sm.wj[warp][grp[v] + (best[v] & 7u)];
       const float bv = kval(best[v]);
-      const bool amb_cand = second[v] < 0x7f800000u && kval(second[v]) <= bv * (1.0f + M) + A;
+      const bool amb_cand = second[v] < kSentKey && kval(second[v]) <= bv * (1.0f + M) + A;
       int decided = 0;  // 1 = update, 2 = keep, 0 = exact re-decision
       if (!amb_cand) {
         if (w == kUndefined) {
@@ -460,6 +428,7 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
               const float d = (cc.x - p[v][c]) + cc.y;
               dold = fmaf(d, d, dold);
             }
+            dold *= P.key_scale2;  // into the keys' (exactly) scaled domain
             if (bv * (1.0f + M) + A < dold) decided = 1;
             else if (bv > dold * (1.0f + M) + A) decided = 2;
           }
@@ -640,6 +609,84 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
   }
 }
 
+inline int region_extent(int s);
+
+// Candidate list of every region (one warp per region): the clusters binned
+// in the anchor cells within one cell of the region box, in
+// cell order. Written as [count, ids...]; count > kFastMaxCand marks a
+// crowded region (the main kernel then takes the exact generic path).
+template <int RANK>
+__global__ void __launch_bounds__(128) k_region_cand(FastParams P, int64_t nregions) {
+  const Geom& g = P.g;
+  const int lane = threadIdx.x & 31;
+  const int64_t region = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (region >= nregions) return;
+  int64_t rb = region;
+  const int rxi = (int)(rb % P.nreg[0]);
+  rb /= P.nreg[0];
+  const int ryi = (int)(rb % P.nreg[1]);
+  rb /= P.nreg[1];
+  const int rzi = (int)rb;
+  const int64_t org[3] = {(int64_t)rxi * P.R[0], (int64_t)ryi * P.R[1],
+                          RANK == 3 ? P.reg_z0 + (int64_t)rzi * P.R[2] : 0};
+  const int64_t hi[3] = {min(org[0] + P.R[0], g.dims[0]) - 1, min(org[1] + P.R[1], g.dims[1]) - 1,
+                         RANK == 3 ? min(org[2] + P.R[2], g.dims[2]) - 1 : 0};
+  const int64_t zlo = RANK == 3 ? max(org[2], g.slab_begin) : 0;
+  const int64_t zhi = RANK == 3 ? min(hi[2], g.slab_end - 1) : 0;
+  int clo[3], chi[3], nc = 1;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    if (a < RANK) {
+      const int64_t lo_a = a == 2 ? zlo : org[a];
+      const int64_t hi_a = a == 2 ? zhi : hi[a];
+      const int64_t l = lo_a - g.grid[a];
+      clo[a] = l < 0 ? 0 : (int)(l / g.grid[a]);
+      const int64_t h = (hi_a + g.grid[a]) / g.grid[a];
+      chi[a] = h > g.cells[a] - 1 ? g.cells[a] - 1 : (int)h;
+    } else {
+      clo[a] = chi[a] = 0;
+    }
+    nc *= chi[a] - clo[a] + 1;
+  }
+  int* out = P.region_cand_out + region * kRegionCandStride;
+  int total = 0;
+  for (int base = 0; base < nc; base += 32) {
+    const int i = base + lane;
+    int cnt = 0, cstart = 0;
+    if (i < nc) {
+      const int nx = chi[0] - clo[0] + 1, ny = chi[1] - clo[1] + 1;
+      const int cx = clo[0] + i % nx, cy = clo[1] + (i / nx) % ny, cz = clo[2] + i / (nx * ny);
+      const int64_t cell = ((int64_t)cz * g.cells[1] + cy) * g.cells[0] + cx;
+      cstart = __ldg(P.cell_start + cell);
+      cnt = __ldg(P.cell_start + cell + 1) - cstart;
+    }
+    int incl = cnt;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int excl = total + incl - cnt;
+    for (int q = 0; q < cnt; ++q)
+      if (excl + q < kFastMaxCand) out[1 + excl + q] = __ldg(P.items + cstart + q);
+    total += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  if (lane == 0) out[0] = total;
+}
+
+inline int64_t fast_region_count(const Geom& g) {
+  int64_t n = 1;
+  for (int a = 0; a < g.rank; ++a) {
+    const int r = region_extent(g.grid[a]);
+    if (a == g.rank - 1 && g.rank == 3) {
+      const int64_t z0 = g.slab_begin / r * r;
+      n *= (g.slab_end - z0 + r - 1) / r;
+    } else {
+      n *= (g.dims[a] + r - 1) / r;
+    }
+  }
+  return n;
+}
+
 // hi/lo fp32 split of one centre table (for the fp32 d_old filter); entries
 // padded to hist32_stride(stride) float2 (16-byte multiples, zero padding).
 static __global__ void k_split32(const double* c, float2* out, int64_t k, int stride) {
@@ -720,12 +767,12 @@ void launch_fast_r(const FastParams& P, size_t smem, int64_t nb, cudaStream_t s)
 }
 
 // Relative fp32 decision margin: each fp32
-// distance is within (C + 12) u of the fp64 one (u = 2^-24; includes the
-// reciprocal-multiply of the d_old filter) and keys are truncated by < 8 ulp
-// (2^-20 relative); 2x for the two sides, 1.5x slack.
+// distance is within (C + 14) u of the fp64 one (u = 2^-24; includes the
+// fp32 spatial tables and reciprocal multiplies; the key scaling is exact and
+// keys keep every mantissa bit); 2x for the two sides, 1.5x slack.
 inline float fast_margin(int channels) {
   const double u = 1.0 / 16777216.0;
-  return (float)(1.5 * (2.0 * (channels + 12) * u + 1.0 / 1048576.0));
+  return (float)(1.5 * 2.0 * (channels + 14) * u);
 }
 
 inline void launch_fast_assign(FastParams P, cudaStream_t s) {
@@ -754,8 +801,15 @@ inline void launch_fast_assign(FastParams P, cudaStream_t s) {
                    : 0;
   const int64_t nb = (int64_t)P.nreg[0] * P.nreg[1] * P.nreg[2];
   const size_t smem = fast_smem_bytes(g, P.R);
-  if (g.rank == 3) launch_fast_r<3>(P, smem, nb, s);
-  else launch_fast_r<2>(P, smem, nb, s);
+  // region candidate lists first (one warp per region), then the sweep
+  P.region_cand_out = const_cast<int*>(P.region_cand);
+  if (g.rank == 3) {
+    k_region_cand<3><<<(unsigned)((nb + 3) / 4), 128, 0, s>>>(P, nb);
+    launch_fast_r<3>(P, smem, nb, s);
+  } else {
+    k_region_cand<2><<<(unsigned)((nb + 3) / 4), 128, 0, s>>>(P, nb);
+    launch_fast_r<2>(P, smem, nb, s);
+  }
 }
 
 }  // namespace sslic_b200
