@@ -82,8 +82,8 @@ struct alignas(16) FastSmem {
   int pad;
   int id[kFastMaxCand];
   int anc[kFastMaxCand][3];
-  unsigned short wl[kFastThreads / 32][kFastMaxCand + 2];   // record offsets (floats)
-  unsigned char wj[kFastThreads / 32][kFastMaxCand + 2];    // candidate slots
+  unsigned short wl[kFastThreads / 32][kFastMaxCand + 8];   // record offsets (floats)
+  unsigned char wj[kFastThreads / 32][kFastMaxCand + 8];    // candidate slots
   int htab[2 * kFastMaxCand];                               // cluster id -> slot
 };
 

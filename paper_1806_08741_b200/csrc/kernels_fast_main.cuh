@@ -279,13 +279,13 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
         sm.wj[warp][pos] = (unsigned char)(lane + 32);
       }
       nl = __popc(m0) + __popc(m1);
-      if (lane == 0 && (nl & 1)) {
-        sm.wl[warp][nl] = (unsigned short)(n * RS);  // all-inf padding record
-        sm.wj[warp][nl] = (unsigned char)n;
+      if (lane < ((8 - (nl & 7)) & 7)) {  // pad to a multiple of 8: sentinel record
+        sm.wl[warp][nl + lane] = (unsigned short)(n * RS);
+        sm.wj[warp][nl + lane] = (unsigned char)n;
       }
       __syncwarp();
     }
-    const int nlp = (nl + 1) & ~1;
+    const int nlp = (nl + 7) & ~7;
 #pragma unroll
     for (int v = 0; v < 4; ++v) n_evals += valid[v] ? nl : 0;
 
@@ -350,12 +350,12 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
       uint32_t before[4];
 #pragma unroll
       for (int v = 0; v < 4; ++v) before[v] = best[v];
-      const int g1 = min(g0 + 8, nlp);
-      for (int jj = g0; jj < g1; jj += 2) {
+#pragma unroll
+      for (int jj = 0; jj < 8; jj += 2) {  // the list is padded to 8 (sentinel records)
         uint32_t key[2][4];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const float* r = rec + sm.wl[warp][jj + h];
+          const float* r = rec + sm.wl[warp][g0 + jj + h];
           const ulonglong2 sxv = *reinterpret_cast<const ulonglong2*>(r + ox);
           f2 syz = *reinterpret_cast<const f2*>(r + oy);
           if (RANK == 3) syz = add2(syz, *reinterpret_cast<const f2*>(r + oz));
@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
           float f0, f1, f2v, f3;
           up2(a01, f0, f1);
           up2(a23, f2v, f3);
-          const uint32_t jl = (uint32_t)((jj + h) & 7);
+          const uint32_t jl = (uint32_t)(jj + h);  // compile-time index in the group
           key[h][0] = fkey(f0, jl);
           key[h][1] = fkey(f1, jl);
           key[h][2] = fkey(f2v, jl);
