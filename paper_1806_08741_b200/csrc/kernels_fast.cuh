@@ -85,6 +85,7 @@ struct alignas(16) FastSmem {
   unsigned short wl[kFastThreads / 32][kFastMaxCand + 8];   // record offsets (floats)
   unsigned char wj[kFastThreads / 32][kFastMaxCand + 8];    // candidate slots
   int htab[2 * kFastMaxCand];                               // cluster id -> slot
+  float2 cpos[kFastMaxCand][3];                             // hi/lo centre coordinates
 };
 
 constexpr int kSlotHash = 2 * kFastMaxCand;

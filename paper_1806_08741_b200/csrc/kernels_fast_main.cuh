@@ -95,12 +95,11 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // ---- region ----
-  int64_t rb = blockIdx.x;
-  const int rxi = (int)(rb % P.nreg[0]);
-  rb /= P.nreg[0];
-  const int ryi = (int)(rb % P.nreg[1]);
-  rb /= P.nreg[1];
-  const int rzi = (int)rb;
+  unsigned rb = blockIdx.x;  // 32-bit region index math
+  const int rxi = (int)(rb % (unsigned)P.nreg[0]);
+  rb /= (unsigned)P.nreg[0];
+  const int ryi = (int)(rb % (unsigned)P.nreg[1]);
+  const int rzi = (int)(rb / (unsigned)P.nreg[1]);
   const int64_t org[3] = {(int64_t)rxi * RX, (int64_t)ryi * RY,
                           RANK == 3 ? P.reg_z0 + (int64_t)rzi * RZ : 0};
   const int64_t hi[3] = {min(org[0] + RX, g.dims[0]) - 1, min(org[1] + RY, g.dims[1]) - 1,
@@ -144,10 +143,12 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
         r[4 * c + 2] = hl.y * P.key_scale;
         r[4 * c + 3] = hl.y * P.key_scale;
       }
-      // anchors stored region-local (32-bit)
+      // anchors stored region-local (32-bit); hi/lo coordinates for the tables
 #pragma unroll
-      for (int a = 0; a < 3; ++a)
+      for (int a = 0; a < 3; ++a) {
         sm.anc[j][a] = a < RANK ? (int)(P.anchors[kid * kMaxRank + a] - org[a]) : 0;
+        if (a < RANK) sm.cpos[j][a] = __ldg(c32 + C + a);
+      }
     } else {
 #pragma unroll
       for (int c = 0; c < 4 * C; ++c) r[c] = 0.f;
@@ -183,7 +184,7 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
         if (dx >= -s && dx <= s) {
           const float x = (float)((a == 0 ? org[0] : (a == 1 ? org[1] : org[2])) + r);
           // fp32 filter table from the hi/lo centre split (error in the margin)
-          const float2 cc = __ldg(P.cur32 + (int64_t)kid * kS2 + C + a);
+          const float2 cc = sm.cpos[j][a];
           const float t = ((cc.x - x) + cc.y) * P.inv_grid[a];
           v = (float)g.m_sq * (t * t) * P.key_scale2;
         }
@@ -212,7 +213,7 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
   const float M = P.margin;
   const float A = P.abs_margin;
   const float fscale = ldexpf(1.0f, P.shift);
-  const float msq = (float)g.m_sq;
+  const float ks = P.key_scale;
   const int64_t lab_base = -g.slab_begin * g.plane;
   const int64_t img_base = -g.data_begin * g.plane;
   // [warp][v][lane][kS2]: each lane's entry is contiguous (16-byte cp.async)
@@ -245,50 +246,6 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
     for (int v = 0; v < 4; ++v) valid[v] = row_ok && lx0 + v <= ex && lx0 + v < RX;
     const bool all4 = valid[0] && valid[1] && valid[2] && valid[3];
 
-    // candidates covering this box -> compact warp list (padded to even)
-    __syncwarp();
-    int nl;
-    {
-      bool cov[2];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int j = lane + 32 * h;
-        bool c = j < n;
-        if (c) {
-          const int s0 = g.grid[0], s1 = g.grid[1];
-          c = sm.anc[j][0] + s0 >= bx0 && sm.anc[j][0] - s0 <= bx1 && sm.anc[j][1] + s1 >= by0 &&
-              sm.anc[j][1] - s1 <= by1;
-          if (RANK == 3) {
-            const int s2 = g.grid[2];
-            c = c && sm.anc[j][2] + s2 >= bz0c && sm.anc[j][2] - s2 <= bz1;
-          }
-        }
-        cov[h] = c;
-      }
-      const unsigned m0 = __ballot_sync(0xffffffffu, cov[0]);
-      const unsigned m1 = __ballot_sync(0xffffffffu, cov[1]);
-      const unsigned lt = (1u << lane) - 1u;
-      if (cov[0]) {
-        const int pos = __popc(m0 & lt);
-        sm.wl[warp][pos] = (unsigned short)(lane * RS);
-        sm.wj[warp][pos] = (unsigned char)lane;
-      }
-      if (cov[1]) {
-        const int pos = __popc(m0) + __popc(m1 & lt);
-        sm.wl[warp][pos] = (unsigned short)((lane + 32) * RS);
-        sm.wj[warp][pos] = (unsigned char)(lane + 32);
-      }
-      nl = __popc(m0) + __popc(m1);
-      if (lane < ((8 - (nl & 7)) & 7)) {  // pad to a multiple of 8: sentinel record
-        sm.wl[warp][nl + lane] = (unsigned short)(n * RS);
-        sm.wj[warp][nl + lane] = (unsigned char)n;
-      }
-      __syncwarp();
-    }
-    const int nlp = (nl + 7) & ~7;
-#pragma unroll
-    for (int v = 0; v < 4; ++v) n_evals += valid[v] ? nl : 0;
-
     // label words + pixels (vector loads for aligned full runs)
     const int64_t gx0 = org[0] + lx0, gy = org[1] + ly, gz = org[2] + lz;
     const int64_t off0 = gx0 + gy * g.strides[1] + (RANK == 3 ? gz * g.strides[2] : 0);
@@ -308,15 +265,14 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
     const T* px = static_cast<const T*>(P.img) + (off0 + img_base) * C;
     load_run<C, T>(px, vec, valid, p);
 
-    // prefetch the carried-over centres (history tables) into shared memory;
-    // consumed after the candidate loop, so the gather latency is hidden
-    // (once per distinct label word of the lane's run: rep[v] = first voxel
-    // of the run carrying the same word)
+    // carried-over centres (history tables), once per distinct label word
     int rep[4];
+    bool any_undef = false;
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
       rep[v] = v;
       if (v > 0 && word[v] == word[v - 1]) rep[v] = rep[v - 1];
+      any_undef |= valid[v] && word[v] == kUndefined;
       if (rep[v] == v && valid[v] && word[v] != kUndefined) {
         const uint32_t L = P.codec.label(word[v]), Tg = P.codec.tag(word[v]);
         const float2* hc = P.hist32 + ((int64_t)Tg * g.k + L) * kS2;
@@ -327,17 +283,136 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
     }
     cp_async_commit();
 
+    // box pixel range per channel (scaled domain) for the candidates' lower bounds
+    float pmin[C], pmax[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      float lo = kInf, hv = -kInf;
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+        if (valid[v]) {
+          lo = fminf(lo, p[v][c]);
+          hv = fmaxf(hv, p[v][c]);
+        }
+      for (int o = 16; o > 0; o >>= 1) {
+        lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hv = fmaxf(hv, __shfl_xor_sync(0xffffffffu, hv, o));
+      }
+      pmin[c] = lo * ks;
+      pmax[c] = hv * ks;
+    }
+
+    // fp32 d_old (scaled), an upper bound of it, and the box maximum
+    cp_async_wait_all();
+    float dold[4];
+    float dmax = 0.f;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      dold[v] = kInf;
+      if (!valid[v] || word[v] == kUndefined) continue;
+      const float2* hc = my_stage + rep[v] * 32 * kS2;
+      float sp = 0.f;
+#pragma unroll
+      for (int a = 0; a < RANK; ++a) {
+        const float2 cc = hc[C + a];
+        const float x = (float)(a == 0 ? gx0 + v : (a == 1 ? gy : gz));
+        const float t = ((cc.x - x) + cc.y) * P.inv_grid[a];
+        sp = fmaf(t, t, sp);
+      }
+      float d = sp * (float)g.m_sq;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const float2 cc = hc[c];
+        const float e = (cc.x - p[v][c]) + cc.y;
+        d = fmaf(e, e, d);
+      }
+      dold[v] = d * P.key_scale2;
+      dmax = fmaxf(dmax, dold[v]);
+    }
+    dmax = any_undef ? kInf : dmax * (1.0f + M) + A;
+    for (int o = 16; o > 0; o >>= 1) dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+
+    // candidates covering this box whose lower bound over the box can beat
+    // some voxel's d_old -> compact warp list (padded to pairs). A candidate
+    // with LB > max d_old is provably never chosen in this box (its distance
+    // exceeds every voxel's carried-over distance), so skipping it is exact.
+    __syncwarp();
+    int nl;
+    {
+      bool keep[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int j = lane + 32 * h;
+        bool c = j < n;
+        if (c) {
+          const int s0 = g.grid[0], s1 = g.grid[1];
+          c = sm.anc[j][0] + s0 >= bx0 && sm.anc[j][0] - s0 <= bx1 && sm.anc[j][1] + s1 >= by0 &&
+              sm.anc[j][1] - s1 <= by1;
+          if (RANK == 3) {
+            const int s2 = g.grid[2];
+            c = c && sm.anc[j][2] + s2 >= bz0c && sm.anc[j][2] - s2 <= bz1;
+          }
+        }
+        if (c && dmax < kInf) {
+          const float* r = rec + j * RS;
+          float lb = 0.f;
+#pragma unroll
+          for (int cc = 0; cc < C; ++cc) {
+            const float ch = r[4 * cc], cl = fabsf(r[4 * cc + 2]);
+            const float t = fmaxf(fmaxf(pmin[cc] - ch, ch - pmax[cc]) - cl, 0.f);
+            lb = fmaf(t, t, lb);
+          }
+          float sl = 0.f;
+          const int b0[3] = {bx0, by0, bz0c}, b1[3] = {bx1, by1, bz1};
+#pragma unroll
+          for (int a = 0; a < RANK; ++a) {
+            const float2 cp = sm.cpos[j][a];
+            const float cpl = (cp.x - (float)org[a]) + cp.y;
+            const float t = fmaxf(fmaxf((float)b0[a] - cpl, cpl - (float)b1[a]) - 1e-3f, 0.f) *
+                            P.inv_grid[a];
+            sl = fmaf(t, t, sl);
+          }
+          lb = fmaf(sl, (float)g.m_sq * P.key_scale2, lb);
+          c = lb * (1.0f - 4.0f * M) <= dmax;
+        }
+        keep[h] = c;
+      }
+      const unsigned m0 = __ballot_sync(0xffffffffu, keep[0]);
+      const unsigned m1 = __ballot_sync(0xffffffffu, keep[1]);
+      const unsigned lt = (1u << lane) - 1u;
+      if (keep[0]) {
+        const int pos = __popc(m0 & lt);
+        sm.wl[warp][pos] = (unsigned short)(lane * RS);
+        sm.wj[warp][pos] = (unsigned char)lane;
+      }
+      if (keep[1]) {
+        const int pos = __popc(m0) + __popc(m1 & lt);
+        sm.wl[warp][pos] = (unsigned short)((lane + 32) * RS);
+        sm.wj[warp][pos] = (unsigned char)(lane + 32);
+      }
+      nl = __popc(m0) + __popc(m1);
+      if (lane == 0 && (nl & 1)) {  // pad to a pair: sentinel record
+        sm.wl[warp][nl] = (unsigned short)(n * RS);
+        sm.wj[warp][nl] = (unsigned char)n;
+      }
+      __syncwarp();
+    }
+    const int nlp = (nl + 1) & ~1;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) n_evals += valid[v] ? nl : 0;
+
     f2 p01[C], p23[C];
 #pragma unroll
     for (int c = 0; c < C; ++c) {
-      p01[c] = pk2(p[0][c] * P.key_scale, p[1][c] * P.key_scale);
-      p23[c] = pk2(p[2][c] * P.key_scale, p[3][c] * P.key_scale);
+      p01[c] = pk2(p[0][c] * ks, p[1][c] * ks);
+      p23[c] = pk2(p[2][c] * ks, p[3][c] * ks);
     }
     const int ox = kHdr + (lx0 < RXp ? lx0 : 0);
     const int oy = kHdr + RXp + 2 * (ly < RY ? ly : 0);
     const int oz = kHdr + RXp + 2 * RY + 2 * (lz < RZ ? lz : 0);
 
-    // fp32 argmin with runner-up: keys = value with 3 low bits = index in group
+    // fp32 argmin with runner-up over the kept candidates: keys carry the
+    // position in the current group of 8 in their 3 low bits
     uint32_t best[4], second[4];
     int grp[4];
 #pragma unroll
@@ -350,12 +425,14 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
       uint32_t before[4];
 #pragma unroll
       for (int v = 0; v < 4; ++v) before[v] = best[v];
-#pragma unroll
-      for (int jj = 0; jj < 8; jj += 2) {  // the list is padded to 8 (sentinel records)
+      const int g1 = min(g0 + 8, nlp);
+#pragma unroll 1
+      for (int jj = g0; jj < g1; jj += 2) {
         uint32_t key[2][4];
+        const uint32_t jl0 = (uint32_t)(jj & 7);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const float* r = rec + sm.wl[warp][g0 + jj + h];
+          const float* r = rec + sm.wl[warp][jj + h];
           const ulonglong2 sxv = *reinterpret_cast<const ulonglong2*>(r + ox);
           f2 syz = *reinterpret_cast<const f2*>(r + oy);
           if (RANK == 3) syz = add2(syz, *reinterpret_cast<const f2*>(r + oz));
@@ -371,7 +448,7 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
           float f0, f1, f2v, f3;
           up2(a01, f0, f1);
           up2(a23, f2v, f3);
-          const uint32_t jl = (uint32_t)(jj + h);  // compile-time index in the group
+          const uint32_t jl = jl0 + h;
           key[h][0] = fkey(f0, jl);
           key[h][1] = fkey(f1, jl);
           key[h][2] = fkey(f2v, jl);
@@ -390,7 +467,6 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
       for (int v = 0; v < 4; ++v)
         if (best[v] != before[v]) grp[v] = g0;
     }
-    cp_async_wait_all();
 
     // ---- decisions ----
     uint32_t newl[4], oldl[4];
@@ -399,7 +475,7 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
       oldl[v] = newl[v] = P.codec.label(word[v]);
       if (!valid[v]) continue;
       uint32_t w = word[v];
-      if (best[v] >= kSentKey) continue;  // no window covers the voxel: keep
+      if (best[v] >= kSentKey) continue;  // nothing kept can beat d_old here: keep
       const int jstar = sm.wj[warp][grp[v] + (best[v] & 7u)];
       const float bv = kval(best[v]);
       const bool amb_cand = second[v] < kSentKey && kval(second[v]) <= bv * (1.0f + M) + A;
@@ -407,31 +483,13 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
       if (!amb_cand) {
         if (w == kUndefined) {
           decided = 1;
-        } else {
-          const uint32_t L = oldl[v], Tg = P.codec.tag(w);
-          if ((uint32_t)sm.id[jstar] == L && my_chg[rep[v] * 32] <= (int)Tg) {
-            decided = 2;  // same centre as when the label was set: D* == d_old
-          } else {
-            const float2* hc = my_stage + rep[v] * 32 * kS2;
-            float sp = 0.f;
-#pragma unroll
-            for (int a = 0; a < RANK; ++a) {
-              const float2 cc = hc[C + a];
-              const float x = (float)(a == 0 ? lx0 + v : (a == 1 ? ly : lz)) + (float)org[a];
-              const float t = ((cc.x - x) + cc.y) * P.inv_grid[a];
-              sp = fmaf(t, t, sp);
-            }
-            float dold = sp * msq;
-#pragma unroll
-            for (int c = 0; c < C; ++c) {
-              const float2 cc = hc[c];
-              const float d = (cc.x - p[v][c]) + cc.y;
-              dold = fmaf(d, d, dold);
-            }
-            dold *= P.key_scale2;  // into the keys' (exactly) scaled domain
-            if (bv * (1.0f + M) + A < dold) decided = 1;
-            else if (bv > dold * (1.0f + M) + A) decided = 2;
-          }
+        } else if ((uint32_t)sm.id[jstar] == oldl[v] &&
+                   my_chg[rep[v] * 32] <= (int)P.codec.tag(w)) {
+          decided = 2;  // same centre as when the label was set: D* == d_old
+        } else if (bv * (1.0f + M) + A < dold[v]) {
+          decided = 1;
+        } else if (bv > dold[v] * (1.0f + M) + A) {
+          decided = 2;
         }
       }
       if (decided == 1) {
@@ -588,6 +646,7 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
       }
     }
   }
+  cp_async_wait_all();
   if (P.eval_count) {
     const unsigned a = __reduce_add_sync(0xffffffffu, n_redecided);
     const unsigned c = __reduce_add_sync(0xffffffffu, n_changed);
@@ -609,7 +668,6 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
   }
 }
 
-inline int region_extent(int s);
 
 // Candidate list of every region (one warp per region): the clusters binned
 // in the anchor cells within one cell of the region box, in
@@ -673,10 +731,37 @@ __global__ void __launch_bounds__(128) k_region_cand(FastParams P, int64_t nregi
   if (lane == 0) out[0] = total;
 }
 
+// Region extents R_a = f_a S_a: grown greedily (smallest extent first) while
+// the region has < 8192 voxels, every extent stays <= 64 and the anchor-cell
+// neighbourhood prod (f_a + 2) stays <= 48 cells (headroom to kFastMaxCand
+// for drifted centres). Larger regions amortize the per-CTA staging.
+inline void region_extents(const Geom& g, int* R) {
+  int f[3] = {1, 1, 1};
+  for (;;) {
+    int best = -1;
+    for (int a = 0; a < g.rank; ++a) {
+      if ((f[a] + 1) * g.grid[a] > kFastMaxR) continue;
+      int cells = 1;
+      for (int b = 0; b < g.rank; ++b) cells *= f[b] + 2 + (b == a ? 1 : 0);
+      if (cells > 48) continue;
+      if (best < 0 || f[a] * g.grid[a] < f[best] * g.grid[best]) best = a;
+    }
+    int64_t vox = 1;
+    for (int a = 0; a < g.rank; ++a) vox *= (int64_t)f[a] * g.grid[a];
+    if (best < 0 || vox >= 8192) break;
+    ++f[best];
+  }
+  for (int a = 0; a < 3; ++a) R[a] = a < g.rank ? f[a] * g.grid[a] : 1;
+  // the x extent must be a multiple of 4 for the vector path; keep >= 8
+  if (R[0] < 8) R[0] = g.grid[0] * ((8 + g.grid[0] - 1) / g.grid[0]);
+}
+
 inline int64_t fast_region_count(const Geom& g) {
+  int R[3];
+  region_extents(g, R);
   int64_t n = 1;
   for (int a = 0; a < g.rank; ++a) {
-    const int r = region_extent(g.grid[a]);
+    const int r = R[a];
     if (a == g.rank - 1 && g.rank == 3) {
       const int64_t z0 = g.slab_begin / r * r;
       n *= (g.slab_end - z0 + r - 1) / r;
@@ -716,13 +801,6 @@ inline bool fast_path_supported(const Geom& g) {
   return true;
 }
 
-// Region extent per axis: a multiple of S, at least 16 voxels (and <= 64).
-inline int region_extent(int s) {
-  int f = (16 + s - 1) / s;
-  int r = f * s;
-  while (r > kFastMaxR && f > 1) r = --f * s;
-  return r;
-}
 
 inline size_t fast_smem_bytes(const Geom& g, const int* R) {
   const int RXp = (R[0] + 3) & ~3;
@@ -777,8 +855,8 @@ inline float fast_margin(int channels) {
 
 inline void launch_fast_assign(FastParams P, cudaStream_t s) {
   const Geom& g = P.g;
+  region_extents(g, P.R);
   for (int a = 0; a < 3; ++a) {
-    P.R[a] = a < g.rank ? region_extent(g.grid[a]) : 1;
     P.inv_grid[a] = 1.0f / (float)g.grid[a];
     P.inv_grid64[a] = 1.0 / (double)g.grid[a];
   }
