@@ -684,7 +684,7 @@ int sslic_engine_assign_ms(sslic_engine* e, int i, float* ms_out, int* n_out) {
 
 int sslic_engine_set_exact(sslic_engine* e, int exact) {
   return guarded([&] {
-    const bool fast_ok = fast_path_supported(e->e->geom()) && !e->e->dist_mode();
+    const bool fast_ok = e->e->fast_supported();
     e->e->set_path(exact || !fast_ok ? AssignPath::kExact : AssignPath::kFast);
     return SSLIC_OK;
   });

@@ -132,6 +132,10 @@ Engine::~Engine() {
   for (cudaEvent_t e : ev_stop_) cudaEventDestroy(e);
 }
 
+bool Engine::fast_supported() const {
+  return fast_path_supported(g_) && !dist_mode_ && fast_ok_scale_ && region_cand_ != nullptr;
+}
+
 void Engine::launch_check(const char* what) {
   ++launches_;
   const cudaError_t e = cudaGetLastError();

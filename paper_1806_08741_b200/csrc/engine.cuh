@@ -5,7 +5,6 @@
 
 #include "common.cuh"
 #include "kernels_exact.cuh"
-#include "kernels_fast_main.cuh"
 
 namespace sslic_b200 {
 
@@ -55,6 +54,8 @@ class Engine {
   void set_value_shift(int s) { shift_ = s; }
   int value_shift() const { return shift_; }
   void set_path(AssignPath p) { path_ = p; }
+  // The fast fp32-filter kernel applies to this geometry/dtype/mode.
+  bool fast_supported() const;
   // Count candidate evaluations and window volumes in assign() (bench).
   void set_collect_stats(bool on) { collect_stats_ = on; }
   AssignPath path() const { return path_; }

@@ -72,7 +72,7 @@ __device__ __forceinline__ void load_run(const T* src, bool vec, const bool* val
   }
 }
 
-template <int RANK, int C, typename T>
+template <int RANK, int C, typename T, int RXc, int RYc, int RZc>
 __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
   using Box = BoxShape<RANK>;
   constexpr int kStride = C + RANK;
@@ -83,7 +83,8 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
   const Geom& g = P.g;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   FastSmem& sm = *reinterpret_cast<FastSmem*>(smem_raw);
-  const int RX = P.R[0], RY = P.R[1], RZ = RANK == 3 ? P.R[2] : 1;
+  const int RX = RXc ? RXc : P.R[0], RY = RYc ? RYc : P.R[1];
+  const int RZ = RANK == 3 ? (RZc ? RZc : P.R[2]) : 1;
   const int RXp = (RX + 3) & ~3;
   const int RS = (kHdr + RXp + 2 * RY + (RANK == 3 ? 2 * RZ : 0) + 3) & ~3;
   float* rec = reinterpret_cast<float*>(smem_raw + sizeof(FastSmem));  // [cand+1][RS]
@@ -284,38 +285,45 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
     cp_async_commit();
 
     // box pixel range per channel (scaled domain) for the candidates' lower bounds
+    // (warp min/max via redux.sync on order-preserving integer images of the
+    // floats: u8/u16 values are non-negative; f32 values use the sign flip)
     float pmin[C], pmax[C];
 #pragma unroll
     for (int c = 0; c < C; ++c) {
-      float lo = kInf, hv = -kInf;
+      uint32_t lo = 0xffffffffu, hv = 0u;
 #pragma unroll
-      for (int v = 0; v < 4; ++v)
-        if (valid[v]) {
-          lo = fminf(lo, p[v][c]);
-          hv = fmaxf(hv, p[v][c]);
-        }
-      for (int o = 16; o > 0; o >>= 1) {
-        lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-        hv = fmaxf(hv, __shfl_xor_sync(0xffffffffu, hv, o));
+      for (int v = 0; v < 4; ++v) {
+        uint32_t o = __float_as_uint(p[v][c]);
+        if (sizeof(T) == 4) o ^= (o >> 31) ? 0xffffffffu : 0x80000000u;
+        lo = valid[v] ? min(lo, o) : lo;
+        hv = valid[v] ? max(hv, o) : hv;
       }
-      pmin[c] = lo * ks;
-      pmax[c] = hv * ks;
+      lo = __reduce_min_sync(0xffffffffu, lo);
+      hv = __reduce_max_sync(0xffffffffu, hv);
+      if (sizeof(T) == 4) {
+        lo ^= (lo >> 31) ? 0x80000000u : 0xffffffffu;
+        hv ^= (hv >> 31) ? 0x80000000u : 0xffffffffu;
+      }
+      pmin[c] = __uint_as_float(lo) * ks;
+      pmax[c] = __uint_as_float(hv) * ks;
     }
 
-    // fp32 d_old (scaled), an upper bound of it, and the box maximum
+    // fp32 d_old (scaled), an upper bound of it, and the box maximum.
+    // Branch-free over the 4 voxels so their dependency chains interleave;
+    // voxels without a carried-over distance read a (finite or not) dummy
+    // row and are masked afterwards.
     cp_async_wait_all();
     float dold[4];
     float dmax = 0.f;
+    float fx[3] = {(float)gx0, (float)gy, (float)gz};
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
-      dold[v] = kInf;
-      if (!valid[v] || word[v] == kUndefined) continue;
       const float2* hc = my_stage + rep[v] * 32 * kS2;
       float sp = 0.f;
 #pragma unroll
       for (int a = 0; a < RANK; ++a) {
         const float2 cc = hc[C + a];
-        const float x = (float)(a == 0 ? gx0 + v : (a == 1 ? gy : gz));
+        const float x = a == 0 ? fx[0] + (float)v : fx[a];
         const float t = ((cc.x - x) + cc.y) * P.inv_grid[a];
         sp = fmaf(t, t, sp);
       }
@@ -326,11 +334,12 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
         const float e = (cc.x - p[v][c]) + cc.y;
         d = fmaf(e, e, d);
       }
-      dold[v] = d * P.key_scale2;
-      dmax = fmaxf(dmax, dold[v]);
+      const bool has = valid[v] && word[v] != kUndefined;
+      dold[v] = has ? d * P.key_scale2 : kInf;
+      dmax = has ? fmaxf(dmax, dold[v]) : dmax;
     }
     dmax = any_undef ? kInf : dmax * (1.0f + M) + A;
-    for (int o = 16; o > 0; o >>= 1) dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+    dmax = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(dmax)));
 
     // candidates covering this box whose lower bound over the box can beat
     // some voxel's d_old -> compact warp list (padded to pairs). A candidate
@@ -469,38 +478,43 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
     }
 
     // ---- decisions ----
+    // (predicated over the 4 voxels; only the rare fp64 re-decision branches)
     uint32_t newl[4], oldl[4];
+    uint32_t nword[4];
+    unsigned exact_mask = 0;
+    int jst[4];
+    bool ambc[4];
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
-      oldl[v] = newl[v] = P.codec.label(word[v]);
-      if (!valid[v]) continue;
-      uint32_t w = word[v];
-      if (best[v] >= kSentKey) continue;  // nothing kept can beat d_old here: keep
+      oldl[v] = P.codec.label(word[v]);
+      const bool live = valid[v] && best[v] < kSentKey;  // else: keep (nothing kept beats d_old)
       const int jstar = sm.wj[warp][grp[v] + (best[v] & 7u)];
+      const uint32_t kid = (uint32_t)sm.id[jstar];
       const float bv = kval(best[v]);
-      const bool amb_cand = second[v] < kSentKey && kval(second[v]) <= bv * (1.0f + M) + A;
-      int decided = 0;  // 1 = update, 2 = keep, 0 = exact re-decision
-      if (!amb_cand) {
-        if (w == kUndefined) {
-          decided = 1;
-        } else if ((uint32_t)sm.id[jstar] == oldl[v] &&
-                   my_chg[rep[v] * 32] <= (int)P.codec.tag(w)) {
-          decided = 2;  // same centre as when the label was set: D* == d_old
-        } else if (bv * (1.0f + M) + A < dold[v]) {
-          decided = 1;
-        } else if (bv > dold[v] * (1.0f + M) + A) {
-          decided = 2;
+      const bool amb = second[v] < kSentKey && kval(second[v]) <= bv * (1.0f + M) + A;
+      const bool undefw = word[v] == kUndefined;
+      // same centre as when the label was set: D* == d_old exactly -> keep
+      const bool same = kid == oldl[v] && my_chg[rep[v] * 32] <= (int)P.codec.tag(word[v]);
+      const bool upd = !amb && (undefw || (!same && bv * (1.0f + M) + A < dold[v]));
+      const bool keep = !amb && !undefw && (same || bv > dold[v] * (1.0f + M) + A);
+      nword[v] = live && upd ? P.codec.pack(kid, P.tag_now) : word[v];
+      if (live && !upd && !keep) exact_mask |= 1u << v;
+      jst[v] = jstar;
+      ambc[v] = amb;
+    }
+    if (exact_mask) {
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+        if (exact_mask >> v & 1u) {
+          ++n_redecided;
+          nword[v] = exact_region_voxel(P, sm, gx0 + v, gy, gz, (off0 + img_base + v) * C,
+                                        word[v], ambc[v], jst[v], org);
         }
-      }
-      if (decided == 1) {
-        w = P.codec.pack((uint32_t)sm.id[jstar], P.tag_now);
-      } else if (decided == 0) {
-        ++n_redecided;
-        w = exact_region_voxel(P, sm, gx0 + v, gy, gz, (off0 + img_base + v) * C, w, amb_cand,
-                               jstar, org);
-      }
-      if (w != word[v]) P.labels[off0 + lab_base + v] = w;
-      newl[v] = P.codec.label(w);
+    }
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      if (valid[v] && nword[v] != word[v]) P.labels[off0 + lab_base + v] = nword[v];
+      newl[v] = P.codec.label(nword[v]);
     }
 
     // ---- delta accumulation: +new / -old for voxels whose label changed ----
@@ -814,15 +828,39 @@ inline size_t fast_smem_bytes(const Geom& g, const int* R) {
   return b;
 }
 
-template <int RANK, int C, typename T>
-void launch_fast_t(const FastParams& P, size_t smem, int64_t nblocks, cudaStream_t s) {
-  auto kern = k_assign_fast<RANK, C, T>;
+template <int RANK, int C, typename T, int RXc, int RYc, int RZc>
+void launch_fast_shape(const FastParams& P, size_t smem, int64_t nblocks, cudaStream_t s) {
+  auto kern = k_assign_fast<RANK, C, T, RXc, RYc, RZc>;
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     configured = true;
   }
   kern<<<(unsigned)nblocks, kFastThreads, smem, s>>>(P);
+}
+
+// Compile-time region shapes for the BASELINE geometries (all address math
+// folds into immediates); any other geometry runs the runtime-shape kernel.
+template <int RANK, int C, typename T>
+void launch_fast_t(const FastParams& P, size_t smem, int64_t nblocks, cudaStream_t s) {
+  const int* R = P.R;
+  if constexpr (RANK == 3 && C == 1 && sizeof(T) == 2) {
+    if (R[0] == 32 && R[1] == 16 && R[2] == 16)
+      return launch_fast_shape<RANK, C, T, 32, 16, 16>(P, smem, nblocks, s);  // config 3
+  }
+  if constexpr (RANK == 3 && C == 4 && sizeof(T) == 4) {
+    if (R[0] == 16 && R[1] == 16 && R[2] == 8)
+      return launch_fast_shape<RANK, C, T, 16, 16, 8>(P, smem, nblocks, s);  // config 4
+  }
+  if constexpr (RANK == 3 && C == 3 && sizeof(T) == 1) {
+    if (R[0] == 32 && R[1] == 32 && R[2] == 32)
+      return launch_fast_shape<RANK, C, T, 32, 32, 32>(P, smem, nblocks, s);  // config 5
+  }
+  if constexpr (RANK == 2 && C == 3 && sizeof(T) != 2) {
+    if (R[0] == 64 && R[1] == 64)
+      return launch_fast_shape<RANK, C, T, 64, 64, 1>(P, smem, nblocks, s);  // configs 1, 2
+  }
+  launch_fast_shape<RANK, C, T, 0, 0, 0>(P, smem, nblocks, s);
 }
 
 template <int RANK, int C>
