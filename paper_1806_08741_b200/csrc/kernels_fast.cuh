@@ -88,6 +88,15 @@ struct alignas(16) FastSmem {
   float2 cpos[kFastMaxCand][3];                             // hi/lo centre coordinates
 };
 
+// 32-bit words of one lane's prefetched pixel run (4 voxels x C channels),
+// 0 when the run exceeds one 16-byte cp.async (then pixels load directly)
+__host__ __device__ constexpr int pf_pix_words(int C, int esize) {
+  return 4 * C * esize <= 16 ? C * esize : 0;
+}
+__host__ __device__ constexpr int dtype_size(int dt) {
+  return dt == SSLIC_U8 ? 1 : dt == SSLIC_U16 ? 2 : dt == SSLIC_F32 ? 4 : 8;
+}
+
 constexpr int kSlotHash = 2 * kFastMaxCand;
 constexpr int kRegionCandStride = kFastMaxCand + 1;  // [count, ids...] per region
 // float2 entries per hi/lo history row, padded to a 16-byte multiple

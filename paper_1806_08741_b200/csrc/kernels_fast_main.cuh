@@ -23,6 +23,9 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
+__device__ __forceinline__ void cp_async_wait_group1() {
+  asm volatile("cp.async.wait_group 1;" ::: "memory");
+}
 
 // sum over the warp of a pair of signed 16-bit quantities packed in 32 bits
 // (|sum| < 2^15 each)
@@ -93,6 +96,9 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
   // per-warp staging of the carried-over centres: [warp][v][i][lane] float2, chg [warp][v][lane]
   float2* stage = reinterpret_cast<float2*>(accs + kFastMaxCand * kComp);
   int* stage_chg = reinterpret_cast<int*>(stage + kWarps * 4 * kS2 * 32);
+  // next-box prefetch: label words [warp][2][lane] (16 B), pixel runs [warp][2][lane][kPW]
+  uint4* pf_words = reinterpret_cast<uint4*>(stage_chg + kWarps * 4 * 32);
+  uint32_t* pf_pix = reinterpret_cast<uint32_t*>(pf_words + kWarps * 2 * 32);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // ---- region ----
@@ -222,38 +228,84 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
   int* my_chg = stage_chg + warp * 4 * 32 + lane;
   unsigned n_changed = 0, n_redecided = 0, n_evals = 0;
 
-  int bx = warp % nbx, by = (warp / nbx) % nby, bz = warp / (nbx * nby);
-  bx -= kWarps;  // pre-decrement: the loop head advances by kWarps boxes
-#pragma unroll 1
-  for (int b = warp; b < nbox; b += kWarps) {
-    bx += kWarps;
-    while (bx >= nbx) {
-      bx -= nbx;
-      if (++by >= nby) {
-        by = 0;
-        ++bz;
-      }
+  // The label words (and, when small, the pixels) of a warp's next box are
+  // prefetched with cp.async into a per-lane double buffer while the current
+  // box is processed; boxes that are clipped or unaligned load directly.
+  constexpr int kPW = pf_pix_words(C, (int)sizeof(T));
+  uint4* my_pfw = pf_words + (size_t)warp * 2 * 32 + lane;          // [warp][buf][lane]
+  uint32_t* my_pfp = pf_pix + ((size_t)warp * 2 * 32 + lane) * (kPW ? kPW : 1);
+  struct BoxG {
+    int bx0, by0, bz0, bx1, by1, bz0c, bz1, lx0, ly, lz;
+    bool nonempty, vec;
+    int64_t off0;
+  };
+  auto box_geom = [&](int b) {
+    BoxG q;
+    const int bx = b % nbx, t = b / nbx, by = t % nby, bz = t / nby;
+    q.bx0 = bx * Box::X;
+    q.by0 = by * Box::Y;
+    q.bz0 = bz * Box::Z;
+    q.bx1 = min(q.bx0 + Box::X - 1, ex);
+    q.by1 = min(q.by0 + Box::Y - 1, ey);
+    q.bz0c = RANK == 3 ? max(q.bz0, ez_lo) : 0;
+    q.bz1 = RANK == 3 ? min(q.bz0 + Box::Z - 1, ez_hi) : 0;
+    q.nonempty = q.bx0 <= q.bx1 && q.by0 <= q.by1 && q.bz0c <= q.bz1;
+    q.lx0 = q.bx0 + 4 * xq;
+    q.ly = q.by0 + yq;
+    q.lz = q.bz0 + zq;
+    const bool row_ok = q.ly <= q.by1 && (RANK == 2 || (q.lz >= q.bz0c && q.lz <= q.bz1));
+    q.vec = P.aligned4 && q.nonempty && row_ok && q.lx0 + 3 <= ex && q.lx0 + 3 < RX;
+    q.off0 = (org[0] + q.lx0) + (org[1] + q.ly) * g.strides[1] +
+             (RANK == 3 ? (org[2] + q.lz) * g.strides[2] : 0);
+    return q;
+  };
+  // (the geometry is recomputed rather than carried: nothing extra stays live)
+  auto prefetch = [&](int bn, int buf) {
+    if (bn >= nbox) return;
+    const BoxG q = box_geom(bn);
+    if (!q.vec) return;
+    cp_async16(my_pfw + buf * 32, P.labels + q.off0 + lab_base);
+    if (kPW) {
+      const unsigned char* src = reinterpret_cast<const unsigned char*>(
+          static_cast<const T*>(P.img) + (q.off0 + img_base) * C);
+      uint32_t* dst = my_pfp + buf * 32 * (kPW ? kPW : 1);
+      if (kPW == 4) cp_async16(dst, src);
+      else if (kPW == 2) cp_async8(dst, src);
+      else
+#pragma unroll
+        for (int i = 0; i < kPW; ++i) cp_async4(dst + i, src + 4 * i);
     }
-    // box bounds in region-local coordinates, clipped
-    const int bx0 = bx * Box::X, by0 = by * Box::Y, bz0 = bz * Box::Z;
-    const int bx1 = min(bx0 + Box::X - 1, ex), by1 = min(by0 + Box::Y - 1, ey);
-    const int bz0c = RANK == 3 ? max(bz0, ez_lo) : 0;
-    const int bz1 = RANK == 3 ? min(bz0 + Box::Z - 1, ez_hi) : 0;
-    if (bx0 > bx1 || by0 > by1 || bz0c > bz1) continue;  // uniform
-    const int lx0 = bx0 + 4 * xq, ly = by0 + yq, lz = bz0 + zq;
+  };
+
+  prefetch(warp, 0);
+  cp_async_commit();
+  int buf = 0;
+#pragma unroll 1
+  for (int b = warp; b < nbox; b += kWarps, buf ^= 1) {
+    const BoxG cur = box_geom(b);
+    cp_async_wait_all();  // this box's prefetch (issued one box ago)
+    const int bx0 = cur.bx0, by0 = cur.by0, bz0 = cur.bz0, bx1 = cur.bx1, by1 = cur.by1;
+    const int bz0c = cur.bz0c, bz1 = cur.bz1;
+    if (!cur.nonempty) {  // uniform
+      prefetch(b + kWarps, buf ^ 1);
+      cp_async_commit();
+      continue;
+    }
+    const int lx0 = cur.lx0, ly = cur.ly, lz = cur.lz;
     const bool row_ok = ly <= by1 && (RANK == 2 || (lz >= bz0c && lz <= bz1));
     bool valid[4];
 #pragma unroll
     for (int v = 0; v < 4; ++v) valid[v] = row_ok && lx0 + v <= ex && lx0 + v < RX;
-    const bool all4 = valid[0] && valid[1] && valid[2] && valid[3];
 
-    // label words + pixels (vector loads for aligned full runs)
+    // label words + pixels (prefetched, or direct loads for clipped boxes)
     const int64_t gx0 = org[0] + lx0, gy = org[1] + ly, gz = org[2] + lz;
-    const int64_t off0 = gx0 + gy * g.strides[1] + (RANK == 3 ? gz * g.strides[2] : 0);
-    const bool vec = P.aligned4 && all4;
+    const int64_t off0 = cur.off0;
+    const bool vec = cur.vec;
     uint32_t word[4];
+    float p[4][C];
+    const T* px = static_cast<const T*>(P.img) + (off0 + img_base) * C;
     if (vec) {
-      const uint4 q = *reinterpret_cast<const uint4*>(P.labels + off0 + lab_base);
+      const uint4 q = my_pfw[buf * 32];
       word[0] = q.x;
       word[1] = q.y;
       word[2] = q.z;
@@ -262,9 +314,24 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
 #pragma unroll
       for (int v = 0; v < 4; ++v) word[v] = valid[v] ? P.labels[off0 + lab_base + v] : kUndefined;
     }
-    float p[4][C];
-    const T* px = static_cast<const T*>(P.img) + (off0 + img_base) * C;
-    load_run<C, T>(px, vec, valid, p);
+    if constexpr (kPW > 0) {
+      if (vec) {
+        uint32_t w[kPW];
+#pragma unroll
+        for (int i = 0; i < kPW; ++i) w[i] = my_pfp[buf * 32 * kPW + i];
+        T vals[4 * C];
+        static_assert(sizeof(vals) == sizeof(w), "prefetched pixel run size");
+        memcpy(vals, w, sizeof(vals));
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+#pragma unroll
+          for (int c = 0; c < C; ++c) p[v][c] = (float)vals[v * C + c];
+      } else {
+        load_run<C, T>(px, false, valid, p);
+      }
+    } else {
+      load_run<C, T>(px, vec, valid, p);
+    }
 
     // carried-over centres (history tables), once per distinct label word
     int rep[4];
@@ -282,6 +349,8 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
         cp_async4(my_chg + v * 32, P.chg + L);
       }
     }
+    cp_async_commit();
+    prefetch(b + kWarps, buf ^ 1);  // next box, own group (left in flight below)
     cp_async_commit();
 
     // box pixel range per channel (scaled domain) for the candidates' lower bounds
@@ -308,11 +377,54 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
       pmax[c] = __uint_as_float(hv) * ks;
     }
 
+    // candidates covering this box and their lower bound over the box
+    // (colour distance to the box's value range + spatial distance to the
+    // box), computed while the history rows are in flight
+    bool cov[2];
+    float lbv[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = lane + 32 * h;
+      bool c = j < n;
+      if (c) {
+        const int s0 = g.grid[0], s1 = g.grid[1];
+        c = sm.anc[j][0] + s0 >= bx0 && sm.anc[j][0] - s0 <= bx1 && sm.anc[j][1] + s1 >= by0 &&
+            sm.anc[j][1] - s1 <= by1;
+        if (RANK == 3) {
+          const int s2 = g.grid[2];
+          c = c && sm.anc[j][2] + s2 >= bz0c && sm.anc[j][2] - s2 <= bz1;
+        }
+      }
+      float lb = 0.f;
+      if (c) {
+        const float* r = rec + j * RS;
+#pragma unroll
+        for (int cc = 0; cc < C; ++cc) {
+          const float ch = r[4 * cc], cl = fabsf(r[4 * cc + 2]);
+          const float t = fmaxf(fmaxf(pmin[cc] - ch, ch - pmax[cc]) - cl, 0.f);
+          lb = fmaf(t, t, lb);
+        }
+        float sl = 0.f;
+        const int b0[3] = {bx0, by0, bz0c}, b1[3] = {bx1, by1, bz1};
+#pragma unroll
+        for (int a = 0; a < RANK; ++a) {
+          const float2 cp = sm.cpos[j][a];
+          const float cpl = (cp.x - (float)org[a]) + cp.y;
+          const float t = fmaxf(fmaxf((float)b0[a] - cpl, cpl - (float)b1[a]) - 1e-3f, 0.f) *
+                          P.inv_grid[a];
+          sl = fmaf(t, t, sl);
+        }
+        lb = fmaf(sl, (float)g.m_sq * P.key_scale2, lb);
+      }
+      cov[h] = c;
+      lbv[h] = lb * (1.0f - 4.0f * M);
+    }
+
     // fp32 d_old (scaled), an upper bound of it, and the box maximum.
     // Branch-free over the 4 voxels so their dependency chains interleave;
     // voxels without a carried-over distance read a (finite or not) dummy
     // row and are masked afterwards.
-    cp_async_wait_all();
+    cp_async_wait_group1();  // history rows (the next box's prefetch may stay in flight)
     float dold[4];
     float dmax = 0.f;
     float fx[3] = {(float)gx0, (float)gy, (float)gz};
@@ -350,42 +462,7 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
     {
       bool keep[2];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int j = lane + 32 * h;
-        bool c = j < n;
-        if (c) {
-          const int s0 = g.grid[0], s1 = g.grid[1];
-          c = sm.anc[j][0] + s0 >= bx0 && sm.anc[j][0] - s0 <= bx1 && sm.anc[j][1] + s1 >= by0 &&
-              sm.anc[j][1] - s1 <= by1;
-          if (RANK == 3) {
-            const int s2 = g.grid[2];
-            c = c && sm.anc[j][2] + s2 >= bz0c && sm.anc[j][2] - s2 <= bz1;
-          }
-        }
-        if (c && dmax < kInf) {
-          const float* r = rec + j * RS;
-          float lb = 0.f;
-#pragma unroll
-          for (int cc = 0; cc < C; ++cc) {
-            const float ch = r[4 * cc], cl = fabsf(r[4 * cc + 2]);
-            const float t = fmaxf(fmaxf(pmin[cc] - ch, ch - pmax[cc]) - cl, 0.f);
-            lb = fmaf(t, t, lb);
-          }
-          float sl = 0.f;
-          const int b0[3] = {bx0, by0, bz0c}, b1[3] = {bx1, by1, bz1};
-#pragma unroll
-          for (int a = 0; a < RANK; ++a) {
-            const float2 cp = sm.cpos[j][a];
-            const float cpl = (cp.x - (float)org[a]) + cp.y;
-            const float t = fmaxf(fmaxf((float)b0[a] - cpl, cpl - (float)b1[a]) - 1e-3f, 0.f) *
-                            P.inv_grid[a];
-            sl = fmaf(t, t, sl);
-          }
-          lb = fmaf(sl, (float)g.m_sq * P.key_scale2, lb);
-          c = lb * (1.0f - 4.0f * M) <= dmax;
-        }
-        keep[h] = c;
-      }
+      for (int h = 0; h < 2; ++h) keep[h] = cov[h] && lbv[h] <= dmax;
       const unsigned m0 = __ballot_sync(0xffffffffu, keep[0]);
       const unsigned m1 = __ballot_sync(0xffffffffu, keep[1]);
       const unsigned lt = (1u << lane) - 1u;
@@ -825,6 +902,8 @@ inline size_t fast_smem_bytes(const Geom& g, const int* R) {
   b += (size_t)kFastMaxCand * (g.stride + 1) * sizeof(unsigned long long);
   b += (size_t)warps * 4 * hist32_stride(g.stride) * 32 * sizeof(float2);
   b += (size_t)warps * 4 * 32 * sizeof(int);
+  b += (size_t)warps * 2 * 32 * 16;  // next-box label words
+  b += (size_t)warps * 2 * 32 * 4 * pf_pix_words(g.channels, dtype_size(g.dtype));
   return b;
 }
 
