@@ -85,7 +85,8 @@ struct alignas(16) FastSmem {
   unsigned short wl[kFastThreads / 32][kFastMaxCand + 8];   // record offsets (floats)
   unsigned char wj[kFastThreads / 32][kFastMaxCand + 8];    // candidate slots
   int htab[2 * kFastMaxCand];                               // cluster id -> slot
-  float2 cpos[kFastMaxCand][3];                             // hi/lo centre coordinates
+  float cpl[kFastMaxCand][3];        // centre coordinates relative to the region origin
+  unsigned long long bmask[3][16];   // per axis and box index: candidates whose window overlaps
 };
 
 // 32-bit words of one lane's prefetched pixel run (4 voxels x C channels),

@@ -76,7 +76,7 @@ __device__ __forceinline__ void load_run(const T* src, bool vec, const bool* val
 }
 
 template <int RANK, int C, typename T, int RXc, int RYc, int RZc>
-__global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
+__global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_constant__ FastParams P) {
   using Box = BoxShape<RANK>;
   constexpr int kStride = C + RANK;
   constexpr int kComp = kStride + 1;
@@ -154,7 +154,10 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
         sm.anc[j][a] = a < RANK ? (int)(P.anchors[kid * kMaxRank + a] - org[a]) : 0;
-        if (a < RANK) sm.cpos[j][a] = __ldg(c32 + C + a);
+        if (a < RANK) {
+          const float2 cp = __ldg(c32 + C + a);
+          sm.cpl[j][a] = (cp.x - (float)org[a]) + cp.y;
+        }
       }
     } else {
 #pragma unroll
@@ -191,7 +194,7 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
         if (dx >= -s && dx <= s) {
           const float x = (float)((a == 0 ? org[0] : (a == 1 ? org[1] : org[2])) + r);
           // fp32 filter table from the hi/lo centre split (error in the margin)
-          const float2 cc = sm.cpos[j][a];
+          const float2 cc = __ldg(P.cur32 + (int64_t)kid * kS2 + C + a);
           const float t = ((cc.x - x) + cc.y) * P.inv_grid[a];
           v = (float)g.m_sq * (t * t) * P.key_scale2;
         }
@@ -208,11 +211,39 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
       }
     }
   }
+  const int nbx = (RX + Box::X - 1) / Box::X, nby = (RY + Box::Y - 1) / Box::Y;
+  const int nbz = RANK == 3 ? (RZ + Box::Z - 1) / Box::Z : 1;
+  // per axis and box index: the candidates whose window overlaps the box's
+  // (clipped) extent on that axis; a box's covering set is the AND of three
+  for (int t = tid; t < nbx + nby + nbz; t += kFastThreads) {
+    const int a = t < nbx ? 0 : (t < nbx + nby ? 1 : 2);
+    const int i = a == 0 ? t : (a == 1 ? t - nbx : t - nbx - nby);
+    int lo, hi;
+    if (a == 0) {
+      lo = i * Box::X;
+      hi = min(lo + Box::X - 1, ex);
+    } else if (a == 1) {
+      lo = i * Box::Y;
+      hi = min(lo + Box::Y - 1, ey);
+    } else {
+      lo = max(i * Box::Z, ez_lo);
+      hi = min(i * Box::Z + Box::Z - 1, ez_hi);
+    }
+    unsigned long long m = 0ull;
+    if (a < RANK) {
+      const int s = g.grid[a];
+      for (int j = 0; j < n; ++j) {
+        const int an = sm.anc[j][a];
+        if (an + s >= lo && an - s <= hi) m |= 1ull << j;
+      }
+    } else {
+      m = ~0ull;
+    }
+    sm.bmask[a][i] = m;
+  }
   __syncthreads();
 
   // ---- per-warp sweep over the region's boxes ----
-  const int nbx = (RX + Box::X - 1) / Box::X, nby = (RY + Box::Y - 1) / Box::Y;
-  const int nbz = RANK == 3 ? (RZ + Box::Z - 1) / Box::Z : 1;
   const int nbox = nbx * nby * nbz;
   const int xq = lane & 1;
   const int yq = RANK == 3 ? (lane >> 1) & 3 : lane >> 1;
@@ -227,6 +258,11 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
   float2* my_stage = stage + ((size_t)warp * 4 * 32 + lane) * kS2;
   int* my_chg = stage_chg + warp * 4 * 32 + lane;
   unsigned n_changed = 0, n_redecided = 0, n_evals = 0;
+  // tag-mode label words (the fast path never runs in dist mode): labels are
+  // < k <= 2^lbits - 2, so the undefined word 0xffffffff maps to label lmask
+  const uint32_t lmask = P.codec.label_mask;
+  const int lbits = P.codec.label_bits;
+  const uint32_t tag_now_bits = P.tag_now << lbits;
 
   // The label words (and, when small, the pixels) of a warp's next box are
   // prefetched with cp.async into a per-lane double buffer while the current
@@ -235,13 +271,16 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
   uint4* my_pfw = pf_words + (size_t)warp * 2 * 32 + lane;          // [warp][buf][lane]
   uint32_t* my_pfp = pf_pix + ((size_t)warp * 2 * 32 + lane) * (kPW ? kPW : 1);
   struct BoxG {
-    int bx0, by0, bz0, bx1, by1, bz0c, bz1, lx0, ly, lz;
+    int bx, by, bz, bx0, by0, bz0, bx1, by1, bz0c, bz1, lx0, ly, lz;
     bool nonempty, vec;
     int64_t off0;
   };
   auto box_geom = [&](int b) {
     BoxG q;
     const int bx = b % nbx, t = b / nbx, by = t % nby, bz = t / nby;
+    q.bx = bx;
+    q.by = by;
+    q.bz = bz;
     q.bx0 = bx * Box::X;
     q.by0 = by * Box::Y;
     q.bz0 = bz * Box::Z;
@@ -286,6 +325,8 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
     cp_async_wait_all();  // this box's prefetch (issued one box ago)
     const int bx0 = cur.bx0, by0 = cur.by0, bz0 = cur.bz0, bx1 = cur.bx1, by1 = cur.by1;
     const int bz0c = cur.bz0c, bz1 = cur.bz1;
+    const unsigned long long bmask =
+        sm.bmask[0][cur.bx] & sm.bmask[1][cur.by] & sm.bmask[2][RANK == 3 ? cur.bz : 0];
     if (!cur.nonempty) {  // uniform
       prefetch(b + kWarps, buf ^ 1);
       cp_async_commit();
@@ -342,7 +383,7 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
       if (v > 0 && word[v] == word[v - 1]) rep[v] = rep[v - 1];
       any_undef |= valid[v] && word[v] == kUndefined;
       if (rep[v] == v && valid[v] && word[v] != kUndefined) {
-        const uint32_t L = P.codec.label(word[v]), Tg = P.codec.tag(word[v]);
+        const uint32_t L = word[v] & lmask, Tg = word[v] >> lbits;
         const float2* hc = P.hist32 + ((int64_t)Tg * g.k + L) * kS2;
 #pragma unroll
         for (int i = 0; i < kS2; i += 2) cp_async16(my_stage + v * 32 * kS2 + i, hc + i);
@@ -385,16 +426,7 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int j = lane + 32 * h;
-      bool c = j < n;
-      if (c) {
-        const int s0 = g.grid[0], s1 = g.grid[1];
-        c = sm.anc[j][0] + s0 >= bx0 && sm.anc[j][0] - s0 <= bx1 && sm.anc[j][1] + s1 >= by0 &&
-            sm.anc[j][1] - s1 <= by1;
-        if (RANK == 3) {
-          const int s2 = g.grid[2];
-          c = c && sm.anc[j][2] + s2 >= bz0c && sm.anc[j][2] - s2 <= bz1;
-        }
-      }
+      const bool c = (uint32_t)(bmask >> (32 * h)) >> lane & 1u;
       float lb = 0.f;
       if (c) {
         const float* r = rec + j * RS;
@@ -408,8 +440,7 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
         const int b0[3] = {bx0, by0, bz0c}, b1[3] = {bx1, by1, bz1};
 #pragma unroll
         for (int a = 0; a < RANK; ++a) {
-          const float2 cp = sm.cpos[j][a];
-          const float cpl = (cp.x - (float)org[a]) + cp.y;
+          const float cpl = sm.cpl[j][a];
           const float t = fmaxf(fmaxf((float)b0[a] - cpl, cpl - (float)b1[a]) - 1e-3f, 0.f) *
                           P.inv_grid[a];
           sl = fmaf(t, t, sl);
@@ -563,7 +594,7 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
     bool ambc[4];
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
-      oldl[v] = P.codec.label(word[v]);
+      oldl[v] = word[v] & lmask;  // undefined -> lmask (never a label)
       const bool live = valid[v] && best[v] < kSentKey;  // else: keep (nothing kept beats d_old)
       const int jstar = sm.wj[warp][grp[v] + (best[v] & 7u)];
       const uint32_t kid = (uint32_t)sm.id[jstar];
@@ -571,10 +602,10 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
       const bool amb = second[v] < kSentKey && kval(second[v]) <= bv * (1.0f + M) + A;
       const bool undefw = word[v] == kUndefined;
       // same centre as when the label was set: D* == d_old exactly -> keep
-      const bool same = kid == oldl[v] && my_chg[rep[v] * 32] <= (int)P.codec.tag(word[v]);
+      const bool same = kid == oldl[v] && my_chg[rep[v] * 32] <= (int)(word[v] >> lbits);
       const bool upd = !amb && (undefw || (!same && bv * (1.0f + M) + A < dold[v]));
       const bool keep = !amb && !undefw && (same || bv > dold[v] * (1.0f + M) + A);
-      nword[v] = live && upd ? P.codec.pack(kid, P.tag_now) : word[v];
+      nword[v] = live && upd ? (tag_now_bits | kid) : word[v];
       if (live && !upd && !keep) exact_mask |= 1u << v;
       jst[v] = jstar;
       ambc[v] = amb;
@@ -591,7 +622,7 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
       if (valid[v] && nword[v] != word[v]) P.labels[off0 + lab_base + v] = nword[v];
-      newl[v] = P.codec.label(nword[v]);
+      newl[v] = nword[v] & lmask;
     }
 
     // ---- delta accumulation: +new / -old for voxels whose label changed ----
@@ -600,10 +631,10 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(FastParams P) {
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
       if (!valid[v]) continue;
-      undef += newl[v] == kUndefined;
+      undef += newl[v] == lmask;
       if (newl[v] != oldl[v]) {
         pending |= 1u << v;
-        if (oldl[v] != kUndefined) pending |= 1u << (4 + v);
+        if (oldl[v] != lmask) pending |= 1u << (4 + v);
         ++n_changed;
       }
     }
