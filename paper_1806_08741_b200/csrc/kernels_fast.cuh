@@ -5,7 +5,7 @@
 // per axis). The region's candidate clusters are exactly those binned in the
 // anchor cells within one cell of the region (any drift). Each
 // candidate is staged once in shared memory as one record
-//   [ (c_hi, c_hi, c_lo, c_lo) per channel | sx[RXp] | (sy,sy)[RY] | (sz,sz)[RZ] ]
+//   [ sx[RXp] | sy[RY] | sz[RZ] | (c_hi, c_lo) per channel ]
 // where s_a[x] = m^2 ((c_a - x)/S_a)^2 or +inf outside the cluster's window,
 // which folds the window test into the arithmetic. Each warp sweeps 8x4x4
 // voxel boxes (8x16 in 2D), each lane 4 consecutive voxels along x, against
@@ -79,7 +79,8 @@ struct alignas(16) FastSmem {
   int n_cand;
   int overflow;
   int rs;  // record stride in floats
-  int pad;
+  int box_next;  // next unclaimed box of the region
+  int wnext[kFastThreads / 32];  // each warp's claimed next box
   int id[kFastMaxCand];
   int anc[kFastMaxCand][3];
   unsigned short wl[kFastThreads / 32][kFastMaxCand + 8];   // record offsets (floats)

@@ -81,7 +81,6 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
   constexpr int kStride = C + RANK;
   constexpr int kComp = kStride + 1;
   constexpr int kS2 = (kStride + 1) & ~1;  // hi/lo history entry, padded to 16 B
-  constexpr int kHdr = 4 * C;  // (hi, hi, lo, lo) per channel
   constexpr int kWarps = kFastThreads / 32;
   const Geom& g = P.g;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -89,7 +88,8 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
   const int RX = RXc ? RXc : P.R[0], RY = RYc ? RYc : P.R[1];
   const int RZ = RANK == 3 ? (RZc ? RZc : P.R[2]) : 1;
   const int RXp = (RX + 3) & ~3;
-  const int RS = (kHdr + RXp + 2 * RY + (RANK == 3 ? 2 * RZ : 0) + 3) & ~3;
+  const int HO = RXp + RY + (RANK == 3 ? RZ : 0);  // (c_hi, c_lo) per channel after the tables
+  const int RS = (HO + 2 * C + 3) & ~3;
   float* rec = reinterpret_cast<float*>(smem_raw + sizeof(FastSmem));  // [cand+1][RS]
   unsigned long long* accs =
       reinterpret_cast<unsigned long long*>(rec + (size_t)(kFastMaxCand + 1) * RS);
@@ -117,6 +117,88 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
   const int ex = (int)(hi[0] - org[0]), ey = (int)(hi[1] - org[1]);
   const int ez_lo = (int)(zlo - org[2]), ez_hi = (int)(zhi - org[2]);
 
+  // ---- box geometry and the next-box prefetch ----
+  const int nbx = (RX + Box::X - 1) / Box::X, nby = (RY + Box::Y - 1) / Box::Y;
+  const int nbz = RANK == 3 ? (RZ + Box::Z - 1) / Box::Z : 1;
+  const int nbox = nbx * nby * nbz;
+  const int xq = lane & 1;
+  const int yq = RANK == 3 ? (lane >> 1) & 3 : lane >> 1;
+  const int zq = RANK == 3 ? lane >> 3 : 0;
+  const float M = P.margin;
+  const float A = P.abs_margin;
+  const float fscale = ldexpf(1.0f, P.shift);
+  const float ks = P.key_scale;
+  // region base pointers; in-region offsets are 32-bit (fast_path_supported
+  // guarantees R_z * plane < 2^31)
+  const int64_t reg_off = org[0] + org[1] * g.strides[1] + (RANK == 3 ? org[2] * g.strides[2] : 0);
+  uint32_t* const lab_r = P.labels + (reg_off - g.slab_begin * g.plane);
+  const T* const img_r = static_cast<const T*>(P.img) + (reg_off - g.data_begin * g.plane) * C;
+  const int s1 = (int)g.strides[1], s2 = RANK == 3 ? (int)g.strides[2] : 0;
+  const int lane_rel = 4 * xq + yq * s1 + zq * s2;
+  // [warp][v][lane][kS2]: each lane's entry is contiguous (16-byte cp.async)
+  float2* my_stage = stage + ((size_t)warp * 4 * 32 + lane) * kS2;
+  int* my_chg = stage_chg + warp * 4 * 32 + lane;
+  unsigned n_changed = 0, n_redecided = 0, n_evals = 0;
+  // tag-mode label words (the fast path never runs in dist mode): labels are
+  // < k <= 2^lbits - 2, so the undefined word 0xffffffff maps to label lmask
+  const uint32_t lmask = P.codec.label_mask;
+  const int lbits = P.codec.label_bits;
+  const uint32_t tag_now_bits = P.tag_now << lbits;
+
+  // The label words (and, when small, the pixels) of a warp's next box are
+  // prefetched with cp.async into a per-lane double buffer while the current
+  // box is processed; boxes that are clipped or unaligned load directly.
+  constexpr int kPW = pf_pix_words(C, (int)sizeof(T));
+  uint4* my_pfw = pf_words + (size_t)warp * 2 * 32 + lane;          // [warp][buf][lane]
+  uint32_t* my_pfp = pf_pix + ((size_t)warp * 2 * 32 + lane) * (kPW ? kPW : 1);
+  struct BoxG {
+    int bx, by, bz, bx0, by0, bz0, bx1, by1, bz0c, bz1, lx0, ly, lz;
+    bool nonempty, vec;
+    int rel;  // offset of the lane's first voxel from the region origin
+  };
+  auto box_geom = [&](int b) {
+    BoxG q;
+    const int bx = b % nbx, t = b / nbx, by = t % nby, bz = t / nby;
+    q.bx = bx;
+    q.by = by;
+    q.bz = bz;
+    q.bx0 = bx * Box::X;
+    q.by0 = by * Box::Y;
+    q.bz0 = bz * Box::Z;
+    q.bx1 = min(q.bx0 + Box::X - 1, ex);
+    q.by1 = min(q.by0 + Box::Y - 1, ey);
+    q.bz0c = RANK == 3 ? max(q.bz0, ez_lo) : 0;
+    q.bz1 = RANK == 3 ? min(q.bz0 + Box::Z - 1, ez_hi) : 0;
+    q.nonempty = q.bx0 <= q.bx1 && q.by0 <= q.by1 && q.bz0c <= q.bz1;
+    q.lx0 = q.bx0 + 4 * xq;
+    q.ly = q.by0 + yq;
+    q.lz = q.bz0 + zq;
+    const bool row_ok = q.ly <= q.by1 && (RANK == 2 || (q.lz >= q.bz0c && q.lz <= q.bz1));
+    q.vec = P.aligned4 && q.nonempty && row_ok && q.lx0 + 3 <= ex && q.lx0 + 3 < RX;
+    q.rel = q.bx0 + q.by0 * s1 + q.bz0 * s2 + lane_rel;
+    return q;
+  };
+  // (the geometry is recomputed rather than carried: nothing extra stays live)
+  auto prefetch = [&](int bn, int buf) {
+    if (bn >= nbox) return;
+    const BoxG q = box_geom(bn);
+    if (!q.vec) return;
+    cp_async16(my_pfw + buf * 32, lab_r + q.rel);
+    if (kPW) {
+      const unsigned char* src = reinterpret_cast<const unsigned char*>(img_r + q.rel * C);
+      uint32_t* dst = my_pfp + buf * 32 * (kPW ? kPW : 1);
+      if (kPW == 4) cp_async16(dst, src);
+      else if (kPW == 2) cp_async8(dst, src);
+      else
+#pragma unroll
+        for (int i = 0; i < kPW; ++i) cp_async4(dst + i, src + 4 * i);
+    }
+  };
+
+  // the warp's first box (its words/pixels load behind the candidate staging)
+  prefetch(warp, 0);
+  cp_async_commit();
+
   // ---- candidates of this region (precomputed by k_region_cand) ----
   {
     const int* rc = P.region_cand + (int64_t)blockIdx.x * kRegionCandStride;
@@ -126,11 +208,13 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
     if (tid == 0) {
       sm.n_cand = nn;
       sm.overflow = total > kFastMaxCand;
+      sm.box_next = kWarps;
     }
   }
   __syncthreads();
   const int n = sm.n_cand;
   if (sm.overflow) {
+    cp_async_wait_all();
     if (tid == 0) atomicAdd(P.counters + 6, 1ull);
     crowded_region<RANK, C>(P, org, hi, zlo, zhi);
     return;
@@ -145,10 +229,8 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
 #pragma unroll
       for (int c = 0; c < C; ++c) {
         const float2 hl = __ldg(c32 + c);
-        r[4 * c] = hl.x * P.key_scale;  // power-of-two scaling: exact
-        r[4 * c + 1] = hl.x * P.key_scale;
-        r[4 * c + 2] = hl.y * P.key_scale;
-        r[4 * c + 3] = hl.y * P.key_scale;
+        r[HO + 2 * c] = hl.x * P.key_scale;  // power-of-two scaling: exact
+        r[HO + 2 * c + 1] = hl.y * P.key_scale;
       }
       // anchors stored region-local (32-bit); hi/lo coordinates for the tables
 #pragma unroll
@@ -161,7 +243,7 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
       }
     } else {
 #pragma unroll
-      for (int c = 0; c < 4 * C; ++c) r[c] = 0.f;
+      for (int c = 0; c < 2 * C; ++c) r[HO + c] = 0.f;
     }
   }
   for (int i = tid; i < n * kComp; i += kFastThreads) accs[i] = 0ull;
@@ -199,20 +281,16 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
           v = (float)g.m_sq * (t * t) * P.key_scale2;
         }
       }
-      float* rj = rec + (size_t)j * RS + kHdr;
+      float* rj = rec + (size_t)j * RS;
       if (a == 0) {
         rj[r] = v;
       } else if (a == 1) {
-        rj[RXp + 2 * r] = v;
-        rj[RXp + 2 * r + 1] = v;
+        rj[RXp + r] = v;
       } else {
-        rj[RXp + 2 * RY + 2 * r] = v;
-        rj[RXp + 2 * RY + 2 * r + 1] = v;
+        rj[RXp + RY + r] = v;
       }
     }
   }
-  const int nbx = (RX + Box::X - 1) / Box::X, nby = (RY + Box::Y - 1) / Box::Y;
-  const int nbz = RANK == 3 ? (RZ + Box::Z - 1) / Box::Z : 1;
   // per axis and box index: the candidates whose window overlaps the box's
   // (clipped) extent on that axis; a box's covering set is the AND of three
   for (int t = tid; t < nbx + nby + nbz; t += kFastThreads) {
@@ -243,81 +321,7 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
   }
   __syncthreads();
 
-  // ---- per-warp sweep over the region's boxes ----
-  const int nbox = nbx * nby * nbz;
-  const int xq = lane & 1;
-  const int yq = RANK == 3 ? (lane >> 1) & 3 : lane >> 1;
-  const int zq = RANK == 3 ? lane >> 3 : 0;
-  const float M = P.margin;
-  const float A = P.abs_margin;
-  const float fscale = ldexpf(1.0f, P.shift);
-  const float ks = P.key_scale;
-  const int64_t lab_base = -g.slab_begin * g.plane;
-  const int64_t img_base = -g.data_begin * g.plane;
-  // [warp][v][lane][kS2]: each lane's entry is contiguous (16-byte cp.async)
-  float2* my_stage = stage + ((size_t)warp * 4 * 32 + lane) * kS2;
-  int* my_chg = stage_chg + warp * 4 * 32 + lane;
-  unsigned n_changed = 0, n_redecided = 0, n_evals = 0;
-  // tag-mode label words (the fast path never runs in dist mode): labels are
-  // < k <= 2^lbits - 2, so the undefined word 0xffffffff maps to label lmask
-  const uint32_t lmask = P.codec.label_mask;
-  const int lbits = P.codec.label_bits;
-  const uint32_t tag_now_bits = P.tag_now << lbits;
-
-  // The label words (and, when small, the pixels) of a warp's next box are
-  // prefetched with cp.async into a per-lane double buffer while the current
-  // box is processed; boxes that are clipped or unaligned load directly.
-  constexpr int kPW = pf_pix_words(C, (int)sizeof(T));
-  uint4* my_pfw = pf_words + (size_t)warp * 2 * 32 + lane;          // [warp][buf][lane]
-  uint32_t* my_pfp = pf_pix + ((size_t)warp * 2 * 32 + lane) * (kPW ? kPW : 1);
-  struct BoxG {
-    int bx, by, bz, bx0, by0, bz0, bx1, by1, bz0c, bz1, lx0, ly, lz;
-    bool nonempty, vec;
-    int64_t off0;
-  };
-  auto box_geom = [&](int b) {
-    BoxG q;
-    const int bx = b % nbx, t = b / nbx, by = t % nby, bz = t / nby;
-    q.bx = bx;
-    q.by = by;
-    q.bz = bz;
-    q.bx0 = bx * Box::X;
-    q.by0 = by * Box::Y;
-    q.bz0 = bz * Box::Z;
-    q.bx1 = min(q.bx0 + Box::X - 1, ex);
-    q.by1 = min(q.by0 + Box::Y - 1, ey);
-    q.bz0c = RANK == 3 ? max(q.bz0, ez_lo) : 0;
-    q.bz1 = RANK == 3 ? min(q.bz0 + Box::Z - 1, ez_hi) : 0;
-    q.nonempty = q.bx0 <= q.bx1 && q.by0 <= q.by1 && q.bz0c <= q.bz1;
-    q.lx0 = q.bx0 + 4 * xq;
-    q.ly = q.by0 + yq;
-    q.lz = q.bz0 + zq;
-    const bool row_ok = q.ly <= q.by1 && (RANK == 2 || (q.lz >= q.bz0c && q.lz <= q.bz1));
-    q.vec = P.aligned4 && q.nonempty && row_ok && q.lx0 + 3 <= ex && q.lx0 + 3 < RX;
-    q.off0 = (org[0] + q.lx0) + (org[1] + q.ly) * g.strides[1] +
-             (RANK == 3 ? (org[2] + q.lz) * g.strides[2] : 0);
-    return q;
-  };
-  // (the geometry is recomputed rather than carried: nothing extra stays live)
-  auto prefetch = [&](int bn, int buf) {
-    if (bn >= nbox) return;
-    const BoxG q = box_geom(bn);
-    if (!q.vec) return;
-    cp_async16(my_pfw + buf * 32, P.labels + q.off0 + lab_base);
-    if (kPW) {
-      const unsigned char* src = reinterpret_cast<const unsigned char*>(
-          static_cast<const T*>(P.img) + (q.off0 + img_base) * C);
-      uint32_t* dst = my_pfp + buf * 32 * (kPW ? kPW : 1);
-      if (kPW == 4) cp_async16(dst, src);
-      else if (kPW == 2) cp_async8(dst, src);
-      else
-#pragma unroll
-        for (int i = 0; i < kPW; ++i) cp_async4(dst + i, src + 4 * i);
-    }
-  };
-
-  prefetch(warp, 0);
-  cp_async_commit();
+  // ---- per-warp sweep over the region's boxes (dynamically claimed) ----
   int buf = 0;
 #pragma unroll 1
   for (int b = warp; b < nbox; b += kWarps, buf ^= 1) {
@@ -340,11 +344,11 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
 
     // label words + pixels (prefetched, or direct loads for clipped boxes)
     const int64_t gx0 = org[0] + lx0, gy = org[1] + ly, gz = org[2] + lz;
-    const int64_t off0 = cur.off0;
+    const int rel = cur.rel;
     const bool vec = cur.vec;
     uint32_t word[4];
     float p[4][C];
-    const T* px = static_cast<const T*>(P.img) + (off0 + img_base) * C;
+    const T* px = img_r + rel * C;
     if (vec) {
       const uint4 q = my_pfw[buf * 32];
       word[0] = q.x;
@@ -353,7 +357,7 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
       word[3] = q.w;
     } else {
 #pragma unroll
-      for (int v = 0; v < 4; ++v) word[v] = valid[v] ? P.labels[off0 + lab_base + v] : kUndefined;
+      for (int v = 0; v < 4; ++v) word[v] = valid[v] ? lab_r[rel + v] : kUndefined;
     }
     if constexpr (kPW > 0) {
       if (vec) {
@@ -384,7 +388,8 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
       any_undef |= valid[v] && word[v] == kUndefined;
       if (rep[v] == v && valid[v] && word[v] != kUndefined) {
         const uint32_t L = word[v] & lmask, Tg = word[v] >> lbits;
-        const float2* hc = P.hist32 + ((int64_t)Tg * g.k + L) * kS2;
+        // (history rows < 2^32: tag mode caps the tables at 8 GB)
+        const float2* hc = P.hist32 + (size_t)(Tg * (uint32_t)g.k + L) * kS2;
 #pragma unroll
         for (int i = 0; i < kS2; i += 2) cp_async16(my_stage + v * 32 * kS2 + i, hc + i);
         cp_async4(my_chg + v * 32, P.chg + L);
@@ -432,7 +437,7 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
         const float* r = rec + j * RS;
 #pragma unroll
         for (int cc = 0; cc < C; ++cc) {
-          const float ch = r[4 * cc], cl = fabsf(r[4 * cc + 2]);
+          const float ch = r[HO + 2 * cc], cl = fabsf(r[HO + 2 * cc + 1]);
           const float t = fmaxf(fmaxf(pmin[cc] - ch, ch - pmax[cc]) - cl, 0.f);
           lb = fmaf(t, t, lb);
         }
@@ -524,9 +529,9 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
       p01[c] = pk2(p[0][c] * ks, p[1][c] * ks);
       p23[c] = pk2(p[2][c] * ks, p[3][c] * ks);
     }
-    const int ox = kHdr + (lx0 < RXp ? lx0 : 0);
-    const int oy = kHdr + RXp + 2 * (ly < RY ? ly : 0);
-    const int oz = kHdr + RXp + 2 * RY + 2 * (lz < RZ ? lz : 0);
+    const int ox = lx0 < RXp ? lx0 : 0;
+    const int oy = RXp + (ly < RY ? ly : 0);
+    const int oz = RXp + RY + (lz < RZ ? lz : 0);
 
     // fp32 argmin with runner-up over the kept candidates: keys carry the
     // position in the current group of 8 in their 3 low bits
@@ -551,14 +556,16 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
         for (int h = 0; h < 2; ++h) {
           const float* r = rec + sm.wl[warp][jj + h];
           const ulonglong2 sxv = *reinterpret_cast<const ulonglong2*>(r + ox);
-          f2 syz = *reinterpret_cast<const f2*>(r + oy);
-          if (RANK == 3) syz = add2(syz, *reinterpret_cast<const f2*>(r + oz));
-          f2 a01 = add2(sxv.x, syz), a23 = add2(sxv.y, syz);
+          float syz = r[oy];
+          if (RANK == 3) syz += r[oz];
+          // (a pair built from one scalar is a free broadcast operand of FADD2)
+          f2 a01 = add2(sxv.x, pk2(syz, syz)), a23 = add2(sxv.y, pk2(syz, syz));
 #pragma unroll
           for (int c = 0; c < C; ++c) {
-            const ulonglong2 hl = *reinterpret_cast<const ulonglong2*>(r + 4 * c);
-            const f2 d01 = add2(sub2(hl.x, p01[c]), hl.y);
-            const f2 d23 = add2(sub2(hl.x, p23[c]), hl.y);
+            const float2 hl = *reinterpret_cast<const float2*>(r + HO + 2 * c);
+            const f2 ch = pk2(hl.x, hl.x), cl = pk2(hl.y, hl.y);
+            const f2 d01 = add2(sub2(ch, p01[c]), cl);
+            const f2 d23 = add2(sub2(ch, p23[c]), cl);
             a01 = fma2(d01, d01, a01);
             a23 = fma2(d23, d23, a23);
           }
@@ -615,13 +622,13 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
       for (int v = 0; v < 4; ++v)
         if (exact_mask >> v & 1u) {
           ++n_redecided;
-          nword[v] = exact_region_voxel(P, sm, gx0 + v, gy, gz, (off0 + img_base + v) * C,
+          nword[v] = exact_region_voxel(P, sm, gx0 + v, gy, gz, (px - static_cast<const T*>(P.img)) + v * C,
                                         word[v], ambc[v], jst[v], org);
         }
     }
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
-      if (valid[v] && nword[v] != word[v]) P.labels[off0 + lab_base + v] = nword[v];
+      if (valid[v] && nword[v] != word[v]) lab_r[rel + v] = nword[v];
       newl[v] = nword[v] & lmask;
     }
 
@@ -918,6 +925,11 @@ inline bool fast_path_supported(const Geom& g) {
   for (int a = 0; a < g.rank; ++a)
     if (g.grid[a] > kFastMaxR) return false;
   if (g.k >= (int64_t)1 << 30) return false;
+  {
+    int R[3];
+    region_extents(g, R);  // 32-bit in-region voxel offsets
+    if ((int64_t)R[g.rank - 1] * g.strides[g.rank - 1] >= ((int64_t)1 << 31)) return false;
+  }
   for (int a = 0; a < g.rank; ++a)
     if (g.dims[a] >= ((int64_t)1 << 30)) return false;
   return true;
@@ -926,7 +938,7 @@ inline bool fast_path_supported(const Geom& g) {
 
 inline size_t fast_smem_bytes(const Geom& g, const int* R) {
   const int RXp = (R[0] + 3) & ~3;
-  const int RS = (4 * g.channels + RXp + 2 * R[1] + (g.rank == 3 ? 2 * R[2] : 0) + 3) & ~3;
+  const int RS = (RXp + R[1] + (g.rank == 3 ? R[2] : 0) + 2 * g.channels + 3) & ~3;
   const int warps = kFastThreads / 32;
   size_t b = sizeof(FastSmem);
   b += (size_t)(kFastMaxCand + 1) * RS * sizeof(float);
