@@ -82,6 +82,7 @@ struct alignas(16) FastSmem {
   int box_next;  // next unclaimed box of the region
   int wnext[kFastThreads / 32];  // each warp's claimed next box
   int id[kFastMaxCand];
+  int cchg[kFastMaxCand];  // chg[] of each candidate (first table of its current centre)
   int anc[kFastMaxCand][3];
   unsigned short wl[kFastThreads / 32][kFastMaxCand + 8];   // record offsets (floats)
   unsigned char wj[kFastThreads / 32][kFastMaxCand + 8];    // candidate slots

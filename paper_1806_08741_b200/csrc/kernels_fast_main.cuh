@@ -93,11 +93,10 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
   float* rec = reinterpret_cast<float*>(smem_raw + sizeof(FastSmem));  // [cand+1][RS]
   unsigned long long* accs =
       reinterpret_cast<unsigned long long*>(rec + (size_t)(kFastMaxCand + 1) * RS);
-  // per-warp staging of the carried-over centres: [warp][v][i][lane] float2, chg [warp][v][lane]
+  // per-warp staging of the carried-over centres: [warp][v][lane][kS2] float2
   float2* stage = reinterpret_cast<float2*>(accs + kFastMaxCand * kComp);
-  int* stage_chg = reinterpret_cast<int*>(stage + kWarps * 4 * kS2 * 32);
   // next-box prefetch: label words [warp][2][lane] (16 B), pixel runs [warp][2][lane][kPW]
-  uint4* pf_words = reinterpret_cast<uint4*>(stage_chg + kWarps * 4 * 32);
+  uint4* pf_words = reinterpret_cast<uint4*>(stage + kWarps * 4 * kS2 * 32);
   uint32_t* pf_pix = reinterpret_cast<uint32_t*>(pf_words + kWarps * 2 * 32);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -137,7 +136,6 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
   const int lane_rel = 4 * xq + yq * s1 + zq * s2;
   // [warp][v][lane][kS2]: each lane's entry is contiguous (16-byte cp.async)
   float2* my_stage = stage + ((size_t)warp * 4 * 32 + lane) * kS2;
-  int* my_chg = stage_chg + warp * 4 * 32 + lane;
   unsigned n_changed = 0, n_redecided = 0, n_evals = 0;
   // tag-mode label words (the fast path never runs in dist mode): labels are
   // < k <= 2^lbits - 2, so the undefined word 0xffffffff maps to label lmask
@@ -225,6 +223,7 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
     float* r = rec + (size_t)j * RS;
     if (j < n) {
       const int kid = sm.id[j];
+      sm.cchg[j] = __ldg(P.chg + kid);
       const float2* c32 = P.cur32 + (int64_t)kid * kS2;  // hi/lo split of the current table
 #pragma unroll
       for (int c = 0; c < C; ++c) {
@@ -392,7 +391,6 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
         const float2* hc = P.hist32 + (size_t)(Tg * (uint32_t)g.k + L) * kS2;
 #pragma unroll
         for (int i = 0; i < kS2; i += 2) cp_async16(my_stage + v * 32 * kS2 + i, hc + i);
-        cp_async4(my_chg + v * 32, P.chg + L);
       }
     }
     cp_async_commit();
@@ -609,7 +607,7 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
       const bool amb = second[v] < kSentKey && kval(second[v]) <= bv * (1.0f + M) + A;
       const bool undefw = word[v] == kUndefined;
       // same centre as when the label was set: D* == d_old exactly -> keep
-      const bool same = kid == oldl[v] && my_chg[rep[v] * 32] <= (int)(word[v] >> lbits);
+      const bool same = kid == oldl[v] && sm.cchg[jstar] <= (int)(word[v] >> lbits);
       const bool upd = !amb && (undefw || (!same && bv * (1.0f + M) + A < dold[v]));
       const bool keep = !amb && !undefw && (same || bv > dold[v] * (1.0f + M) + A);
       nword[v] = live && upd ? (tag_now_bits | kid) : word[v];
@@ -944,7 +942,6 @@ inline size_t fast_smem_bytes(const Geom& g, const int* R) {
   b += (size_t)(kFastMaxCand + 1) * RS * sizeof(float);
   b += (size_t)kFastMaxCand * (g.stride + 1) * sizeof(unsigned long long);
   b += (size_t)warps * 4 * hist32_stride(g.stride) * 32 * sizeof(float2);
-  b += (size_t)warps * 4 * 32 * sizeof(int);
   b += (size_t)warps * 2 * 32 * 16;  // next-box label words
   b += (size_t)warps * 2 * 32 * 4 * pf_pix_words(g.channels, dtype_size(g.dtype));
   return b;

@@ -1,4 +1,4 @@
 cd $GRAFT_REPO_ROOT
-python bench.py --steps 7 --warmup 3 --no-e2e --no-cpu > gpurun_out/p12_plain.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:k_assign_fast -s 9 -c 1 -o gpurun_out/p12_assign python bench.py --steps 7 --warmup 3 --no-e2e --no-cpu > gpurun_out/p12_ncu.log 2>&1
-echo "rc $?" >> gpurun_out/p12_ncu.log
+python bench.py --steps 7 --warmup 3 --no-e2e --no-cpu > gpurun_out/p13_plain.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:k_assign_fast -s 9 -c 1 -o gpurun_out/p13_assign python bench.py --steps 7 --warmup 3 --no-e2e --no-cpu > gpurun_out/p13_ncu.log 2>&1
+echo "rc $?" >> gpurun_out/p13_ncu.log
