@@ -80,7 +80,7 @@ struct alignas(16) FastSmem {
   int overflow;
   int rs;  // record stride in floats
   int box_next;  // next unclaimed box of the region
-  int wnext[kFastThreads / 32];  // each warp's claimed next box
+  int xqn[kFastThreads / 32];    // each warp's queued fp64 re-decisions (this box)
   int id[kFastMaxCand];
   int cchg[kFastMaxCand];  // chg[] of each candidate (first table of its current centre)
   int anc[kFastMaxCand][3];

@@ -88,7 +88,8 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
   const int RX = RXc ? RXc : P.R[0], RY = RYc ? RYc : P.R[1];
   const int RZ = RANK == 3 ? (RZc ? RZc : P.R[2]) : 1;
   const int RXp = (RX + 3) & ~3;
-  const int HO = RXp + RY + (RANK == 3 ? RZ : 0);  // (c_hi, c_lo) per channel after the tables
+  // (c_hi, c_lo) per channel after the tables, 8-byte aligned
+  const int HO = (RXp + RY + (RANK == 3 ? RZ : 0) + 1) & ~1;
   const int RS = (HO + 2 * C + 3) & ~3;
   float* rec = reinterpret_cast<float*>(smem_raw + sizeof(FastSmem));  // [cand+1][RS]
   unsigned long long* accs =
@@ -207,6 +208,7 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
       sm.n_cand = nn;
       sm.overflow = total > kFastMaxCand;
       sm.box_next = kWarps;
+      for (int w = 0; w < kWarps; ++w) sm.xqn[w] = 0;
     }
   }
   __syncthreads();
@@ -595,8 +597,7 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
     uint32_t newl[4], oldl[4];
     uint32_t nword[4];
     unsigned exact_mask = 0;
-    int jst[4];
-    bool ambc[4];
+    uint32_t xinfo[4];
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
       oldl[v] = word[v] & lmask;  // undefined -> lmask (never a label)
@@ -612,17 +613,17 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
       const bool keep = !amb && !undefw && (same || bv > dold[v] * (1.0f + M) + A);
       nword[v] = live && upd ? (tag_now_bits | kid) : word[v];
       if (live && !upd && !keep) exact_mask |= 1u << v;
-      jst[v] = jstar;
-      ambc[v] = amb;
+      // deferred fp64 re-decision: region-local voxel coordinates, amb, slot
+      xinfo[v] = (uint32_t)(lx0 + v) | (uint32_t)ly << 6 | (uint32_t)lz << 12 | (uint32_t)amb << 18 |
+                 (uint32_t)jstar << 19;
     }
-    if (exact_mask) {
+    // undecided voxels are queued in the warp's (now free) history staging
+    // area and re-decided in fp64 after the box, one voxel per lane
+    uint2* xq = reinterpret_cast<uint2*>(stage + (size_t)warp * 4 * 32 * kS2);
+    if (__any_sync(0xffffffffu, exact_mask != 0)) {
 #pragma unroll
       for (int v = 0; v < 4; ++v)
-        if (exact_mask >> v & 1u) {
-          ++n_redecided;
-          nword[v] = exact_region_voxel(P, sm, gx0 + v, gy, gz, (px - static_cast<const T*>(P.img)) + v * C,
-                                        word[v], ambc[v], jst[v], org);
-        }
+        if (exact_mask >> v & 1u) xq[atomicAdd(&sm.xqn[warp], 1)] = make_uint2(word[v], xinfo[v]);
     }
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
@@ -636,7 +637,7 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
       if (!valid[v]) continue;
-      undef += newl[v] == lmask;
+      undef += newl[v] == lmask && !(exact_mask >> v & 1u);
       if (newl[v] != oldl[v]) {
         pending |= 1u << v;
         if (oldl[v] != lmask) pending |= 1u << (4 + v);
@@ -771,6 +772,56 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
           if (tc) atomicAdd(a + kStride, (unsigned long long)(long long)tc);
         }
       }
+    }
+
+    // ---- deferred fp64 re-decisions of this box (one queued voxel per lane) ----
+    __syncwarp();
+    const int nq = sm.xqn[warp];
+    if (nq > 0) {  // uniform
+      for (int i0 = 0; i0 < nq; i0 += 32) {
+        const int i = i0 + lane;
+        if (i < nq) {
+          const uint2 e = xq[i];
+          const int qx = (int)(e.y & 63u), qy = (int)(e.y >> 6 & 63u), qz = (int)(e.y >> 12 & 63u);
+          const bool qamb = e.y >> 18 & 1u;
+          const int qj = (int)(e.y >> 19 & 63u);
+          const int qrel = qx + qy * s1 + qz * s2;
+          const T* qpx = img_r + (size_t)qrel * C;
+          const uint32_t nw = exact_region_voxel(P, sm, org[0] + qx, org[1] + qy, org[2] + qz,
+                                                 qpx - static_cast<const T*>(P.img), e.x, qamb, qj,
+                                                 org);
+          ++n_redecided;
+          const uint32_t ol = e.x & lmask, nl2 = nw & lmask;
+          if (nw != e.x) lab_r[qrel] = nw;
+          if (nl2 == lmask) atomicAdd(P.counters, 1ull);  // slic.hpp:330-331
+          if (nl2 != ol) {
+            ++n_changed;
+            const long long co[3] = {qx, qy, qz};
+#pragma unroll 1
+            for (int sg = 0; sg < 2; ++sg) {
+              const uint32_t L = sg == 0 ? nl2 : ol;
+              if (L == lmask) continue;
+              const long long sgn = sg == 0 ? 1 : -1;
+              const int S = slot_of(sm, L);
+              unsigned long long* a = S >= 0 ? accs + S * kComp : P.acc + (uint64_t)L * kComp;
+#pragma unroll
+              for (int c = 0; c < C; ++c) {
+                const T raw = qpx[c];
+                const long long val = sizeof(T) < 4 ? (long long)raw
+                                                    : (long long)__float2ll_rn((float)raw * fscale);
+                atomicAdd(a + c, (unsigned long long)(sgn * val));
+              }
+#pragma unroll
+              for (int ax = 0; ax < RANK; ++ax)
+                atomicAdd(a + C + ax,
+                          (unsigned long long)(sgn * (co[ax] + (S >= 0 ? 0 : org[ax]))));
+              atomicAdd(a + kStride, (unsigned long long)sgn);
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) sm.xqn[warp] = 0;
     }
   }
   cp_async_wait_all();
@@ -936,7 +987,8 @@ inline bool fast_path_supported(const Geom& g) {
 
 inline size_t fast_smem_bytes(const Geom& g, const int* R) {
   const int RXp = (R[0] + 3) & ~3;
-  const int RS = (RXp + R[1] + (g.rank == 3 ? R[2] : 0) + 2 * g.channels + 3) & ~3;
+  const int HO = (RXp + R[1] + (g.rank == 3 ? R[2] : 0) + 1) & ~1;
+  const int RS = (HO + 2 * g.channels + 3) & ~3;
   const int warps = kFastThreads / 32;
   size_t b = sizeof(FastSmem);
   b += (size_t)(kFastMaxCand + 1) * RS * sizeof(float);
