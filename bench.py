@@ -118,7 +118,7 @@ def cpu_sample(cfg_id, dims, ch, dtype):
     synthetic volume, treated as their own image."""
     if len(dims) == 2:
         return dims, 2
-    planes = {3: 32, 4: 32, 5: 16}[cfg_id]
+    planes = {3: 32, 4: 32, 5: 32}[cfg_id]  # >= S (the reference rejects S > dims)
     return (dims[0], dims[1], planes), 1
 
 

@@ -594,10 +594,14 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
 
     // ---- decisions ----
     // (predicated over the 4 voxels; only the rare fp64 re-decision branches)
+    // Undefined words have dold = +inf and oldl = lmask (never a winner), so
+    // they need no special case: upd <=> !amb. A runner-up key >= kSentKey
+    // decodes to >= 2^-66 > thr, so amb needs no coverage test either.
     uint32_t newl[4], oldl[4];
     uint32_t nword[4];
-    unsigned exact_mask = 0;
-    uint32_t xinfo[4];
+    unsigned exact_mask = 0, amb_mask = 0;
+    int jst[4];
+    const float M1 = 1.0f + M;
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
       oldl[v] = word[v] & lmask;  // undefined -> lmask (never a label)
@@ -605,17 +609,16 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
       const int jstar = sm.wj[warp][grp[v] + (best[v] & 7u)];
       const uint32_t kid = (uint32_t)sm.id[jstar];
       const float bv = kval(best[v]);
-      const bool amb = second[v] < kSentKey && kval(second[v]) <= bv * (1.0f + M) + A;
-      const bool undefw = word[v] == kUndefined;
+      const float thr = fmaf(bv, M1, A);
+      const bool amb = kval(second[v]) <= thr;
       // same centre as when the label was set: D* == d_old exactly -> keep
       const bool same = kid == oldl[v] && sm.cchg[jstar] <= (int)(word[v] >> lbits);
-      const bool upd = !amb && (undefw || (!same && bv * (1.0f + M) + A < dold[v]));
-      const bool keep = !amb && !undefw && (same || bv > dold[v] * (1.0f + M) + A);
+      const bool upd = !amb && !same && thr < dold[v];
+      const bool keep = !amb && (same || bv > fmaf(dold[v], M1, A));
       nword[v] = live && upd ? (tag_now_bits | kid) : word[v];
       if (live && !upd && !keep) exact_mask |= 1u << v;
-      // deferred fp64 re-decision: region-local voxel coordinates, amb, slot
-      xinfo[v] = (uint32_t)(lx0 + v) | (uint32_t)ly << 6 | (uint32_t)lz << 12 | (uint32_t)amb << 18 |
-                 (uint32_t)jstar << 19;
+      if (amb) amb_mask |= 1u << v;
+      jst[v] = jstar;
     }
     // undecided voxels are queued in the warp's (now free) history staging
     // area and re-decided in fp64 after the box, one voxel per lane
@@ -623,7 +626,12 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
     if (__any_sync(0xffffffffu, exact_mask != 0)) {
 #pragma unroll
       for (int v = 0; v < 4; ++v)
-        if (exact_mask >> v & 1u) xq[atomicAdd(&sm.xqn[warp], 1)] = make_uint2(word[v], xinfo[v]);
+        if (exact_mask >> v & 1u) {
+          // deferred fp64 re-decision: region-local voxel coordinates, amb, slot
+          const uint32_t info = (uint32_t)(lx0 + v) | (uint32_t)ly << 6 | (uint32_t)lz << 12 |
+                                (amb_mask >> v & 1u) << 18 | (uint32_t)jst[v] << 19;
+          xq[atomicAdd(&sm.xqn[warp], 1)] = make_uint2(word[v], info);
+        }
     }
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
