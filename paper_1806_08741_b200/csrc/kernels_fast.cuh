@@ -77,16 +77,11 @@ struct BoxShape {
 
 struct alignas(16) FastSmem {
   int n_cand;
-  int overflow;
-  int rs;  // record stride in floats
-  int box_next;  // next unclaimed box of the region
-  int xqn[kFastThreads / 32];    // each warp's queued fp64 re-decisions (this box)
   int id[kFastMaxCand];
   int cchg[kFastMaxCand];  // chg[] of each candidate (first table of its current centre)
-  int anc[kFastMaxCand][3];
+  short anc[kFastMaxCand][3];  // region-local anchors
   unsigned short wl[kFastThreads / 32][kFastMaxCand + 8];   // record offsets (floats)
-  unsigned char wj[kFastThreads / 32][kFastMaxCand + 8];    // candidate slots
-  int htab[2 * kFastMaxCand];                               // cluster id -> slot
+  unsigned short htab[2 * kFastMaxCand];                               // cluster id -> slot
   float cpl[kFastMaxCand][3];        // centre coordinates relative to the region origin
   unsigned long long bmask[3][16];   // per axis and box index: candidates whose window overlaps
 };
@@ -113,7 +108,8 @@ __device__ __forceinline__ int slot_of(const FastSmem& sm, uint32_t id) {
   int h = slot_hash(id);
   for (;;) {
     const int s = sm.htab[h];
-    if (s < 0 || (uint32_t)sm.id[s] == id) return s;
+    if (s == 0xffff) return -1;
+    if ((uint32_t)sm.id[s] == id) return s;
     h = (h + 1) & (kSlotHash - 1);
   }
 }

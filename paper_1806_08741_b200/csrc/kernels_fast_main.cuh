@@ -199,21 +199,13 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
   cp_async_commit();
 
   // ---- candidates of this region (precomputed by k_region_cand) ----
-  {
-    const int* rc = P.region_cand + (int64_t)blockIdx.x * kRegionCandStride;
-    const int total = __ldg(rc);
-    const int nn = total < kFastMaxCand ? total : kFastMaxCand;
-    for (int j = tid; j < nn; j += kFastThreads) sm.id[j] = __ldg(rc + 1 + j);
-    if (tid == 0) {
-      sm.n_cand = nn;
-      sm.overflow = total > kFastMaxCand;
-      sm.box_next = kWarps;
-      for (int w = 0; w < kWarps; ++w) sm.xqn[w] = 0;
-    }
-  }
+  const int* rc = P.region_cand + (int64_t)blockIdx.x * kRegionCandStride;
+  const int total = __ldg(rc);
+  const int n = total < kFastMaxCand ? total : kFastMaxCand;
+  for (int j = tid; j < n; j += kFastThreads) sm.id[j] = __ldg(rc + 1 + j);
+  if (tid == 0) sm.n_cand = n;
   __syncthreads();
-  const int n = sm.n_cand;
-  if (sm.overflow) {
+  if (total > kFastMaxCand) {
     cp_async_wait_all();
     if (tid == 0) atomicAdd(P.counters + 6, 1ull);
     crowded_region<RANK, C>(P, org, hi, zlo, zhi);
@@ -236,7 +228,7 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
       // anchors stored region-local (32-bit); hi/lo coordinates for the tables
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
-        sm.anc[j][a] = a < RANK ? (int)(P.anchors[kid * kMaxRank + a] - org[a]) : 0;
+        sm.anc[j][a] = (short)(a < RANK ? (int)(P.anchors[kid * kMaxRank + a] - org[a]) : 0);
         if (a < RANK) {
           const float2 cp = __ldg(c32 + C + a);
           sm.cpl[j][a] = (cp.x - (float)org[a]) + cp.y;
@@ -248,11 +240,12 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
     }
   }
   for (int i = tid; i < n * kComp; i += kFastThreads) accs[i] = 0ull;
-  for (int i = tid; i < kSlotHash; i += kFastThreads) sm.htab[i] = -1;
+  for (int i = tid; i < kSlotHash; i += kFastThreads) sm.htab[i] = 0xffff;
   __syncthreads();
   for (int j = tid; j < n; j += kFastThreads) {  // id -> slot hash (linear probing)
     int h = slot_hash((uint32_t)sm.id[j]);
-    while (atomicCAS(&sm.htab[h], -1, j) != -1) h = (h + 1) & (kSlotHash - 1);
+    while (atomicCAS(&sm.htab[h], (unsigned short)0xffff, (unsigned short)j) != 0xffff)
+      h = (h + 1) & (kSlotHash - 1);
   }
   {
     // spatial tables: one warp per candidate, lanes over the table entries
@@ -505,17 +498,14 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
       if (keep[0]) {
         const int pos = __popc(m0 & lt);
         sm.wl[warp][pos] = (unsigned short)(lane * RS);
-        sm.wj[warp][pos] = (unsigned char)lane;
       }
       if (keep[1]) {
         const int pos = __popc(m0) + __popc(m1 & lt);
         sm.wl[warp][pos] = (unsigned short)((lane + 32) * RS);
-        sm.wj[warp][pos] = (unsigned char)(lane + 32);
       }
       nl = __popc(m0) + __popc(m1);
       if (lane == 0 && (nl & 1)) {  // pad to a pair: sentinel record
         sm.wl[warp][nl] = (unsigned short)(n * RS);
-        sm.wj[warp][nl] = (unsigned char)n;
       }
       __syncwarp();
     }
@@ -593,6 +583,13 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
     }
 
     // ---- decisions ----
+    // re-decision queue [count | entries...] at the start of the warp's
+    // history staging area (its rows were consumed by d_old above)
+    int* xcnt = reinterpret_cast<int*>(stage + (size_t)warp * 4 * 32 * kS2);
+    uint2* xqueue = reinterpret_cast<uint2*>(xcnt) + 1;
+    __syncwarp();
+    if (lane == 0) *xcnt = 0;
+    __syncwarp();
     // (predicated over the 4 voxels; only the rare fp64 re-decision branches)
     // Undefined words have dold = +inf and oldl = lmask (never a winner), so
     // they need no special case: upd <=> !amb. A runner-up key >= kSentKey
@@ -606,7 +603,7 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
     for (int v = 0; v < 4; ++v) {
       oldl[v] = word[v] & lmask;  // undefined -> lmask (never a label)
       const bool live = valid[v] && best[v] < kSentKey;  // else: keep (nothing kept beats d_old)
-      const int jstar = sm.wj[warp][grp[v] + (best[v] & 7u)];
+      const int jstar = (int)sm.wl[warp][grp[v] + (best[v] & 7u)] / RS;  // record -> slot
       const uint32_t kid = (uint32_t)sm.id[jstar];
       const float bv = kval(best[v]);
       const float thr = fmaf(bv, M1, A);
@@ -622,7 +619,6 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
     }
     // undecided voxels are queued in the warp's (now free) history staging
     // area and re-decided in fp64 after the box, one voxel per lane
-    uint2* xq = reinterpret_cast<uint2*>(stage + (size_t)warp * 4 * 32 * kS2);
     if (__any_sync(0xffffffffu, exact_mask != 0)) {
 #pragma unroll
       for (int v = 0; v < 4; ++v)
@@ -630,7 +626,7 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
           // deferred fp64 re-decision: region-local voxel coordinates, amb, slot
           const uint32_t info = (uint32_t)(lx0 + v) | (uint32_t)ly << 6 | (uint32_t)lz << 12 |
                                 (amb_mask >> v & 1u) << 18 | (uint32_t)jst[v] << 19;
-          xq[atomicAdd(&sm.xqn[warp], 1)] = make_uint2(word[v], info);
+          xqueue[atomicAdd(xcnt, 1)] = make_uint2(word[v], info);
         }
     }
 #pragma unroll
@@ -784,12 +780,12 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
 
     // ---- deferred fp64 re-decisions of this box (one queued voxel per lane) ----
     __syncwarp();
-    const int nq = sm.xqn[warp];
+    const int nq = *xcnt;
     if (nq > 0) {  // uniform
       for (int i0 = 0; i0 < nq; i0 += 32) {
         const int i = i0 + lane;
         if (i < nq) {
-          const uint2 e = xq[i];
+          const uint2 e = xqueue[i];
           const int qx = (int)(e.y & 63u), qy = (int)(e.y >> 6 & 63u), qz = (int)(e.y >> 12 & 63u);
           const bool qamb = e.y >> 18 & 1u;
           const int qj = (int)(e.y >> 19 & 63u);
@@ -828,8 +824,6 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
           }
         }
       }
-      __syncwarp();
-      if (lane == 0) sm.xqn[warp] = 0;
     }
   }
   cp_async_wait_all();
@@ -1013,6 +1007,9 @@ void launch_fast_shape(const FastParams& P, size_t smem, int64_t nblocks, cudaSt
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    // all of the unified L1 as shared memory: occupancy is smem/register bound
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
     configured = true;
   }
   kern<<<(unsigned)nblocks, kFastThreads, smem, s>>>(P);
