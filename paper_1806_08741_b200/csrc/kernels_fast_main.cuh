@@ -532,6 +532,10 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
       best[v] = second[v] = 0xffffffffu;
       grp[v] = 0;
     }
+    // the next pair of record offsets is loaded one step ahead (the list is
+    // padded, so reading one pair past the end stays inside wl)
+    const uint32_t* wl2 = reinterpret_cast<const uint32_t*>(sm.wl[warp]);
+    uint32_t pr = wl2[0];
 #pragma unroll 1
     for (int g0 = 0; g0 < nlp; g0 += 8) {
       uint32_t before[4];
@@ -542,9 +546,11 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
       for (int jj = g0; jj < g1; jj += 2) {
         uint32_t key[2][4];
         const uint32_t jl0 = (uint32_t)(jj & 7);
+        const uint32_t cur = pr;
+        pr = wl2[(jj >> 1) + 1];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const float* r = rec + sm.wl[warp][jj + h];
+          const float* r = rec + (h ? cur >> 16 : cur & 0xffffu);
           const ulonglong2 sxv = *reinterpret_cast<const ulonglong2*>(r + ox);
           float syz = r[oy];
           if (RANK == 3) syz += r[oz];
