@@ -10,7 +10,11 @@
 // raster recurrence whose fills see the labels written by earlier steps; it
 // runs on the host over the device-computed marker map, exactly as the
 // reference orders it (see DESIGN.md "Connectivity" for the status).
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <sys/mman.h>
 #include <vector>
 
 #include "connectivity.cuh"
@@ -129,100 +133,116 @@ __global__ void k_markers(const uint32_t* root, const uint8_t* final_root, uint8
 inline unsigned nblk(int64_t n) { return (unsigned)((n + 255) / 256); }
 
 // sweep_relabel (connectivity.hpp:182-261): raster order over non-final
-// pixels; fills see earlier relabels.
-uint32_t sweep_host(const Geom& g, std::vector<uint32_t>& labels, std::vector<uint8_t>& markers,
+// pixels; fills see earlier relabels. Host, single-threaded by definition of
+// the recurrence; fills carry coordinates (no div/mod per voxel). Any fill order gives the same component set,
+// and the merge-target search is a max/min over it, so the visiting order
+// does not affect the result.
+struct Vox {
+  int64_t off;
+  int32_t c[3];
+};
+
+uint32_t sweep_host(const Geom& g, uint32_t* labels, uint8_t* markers, int64_t n,
                     int64_t min_size, uint32_t k_start) {
-  const int64_t n = (int64_t)labels.size();
-  std::vector<uint8_t> visited(n, 0);
-  std::vector<int64_t> comp, stack;
+  const int rank = g.rank;
+  int64_t dim[3] = {1, 1, 1}, str[3] = {0, 0, 0};
+  for (int a = 0; a < rank; ++a) {
+    dim[a] = g.dims[a];
+    str[a] = g.strides[a];
+  }
+  // markers: bit 0 = final (the reference's MarkerMap), bit 1 = visited by
+  // the current fill (one array: one page walk per neighbour instead of two)
+  uint8_t* const mk = markers;
+  std::vector<Vox> comp;
+  comp.reserve(1 << 16);
   uint32_t next_label = k_start;
-  int64_t coord[kMaxRank];
-  auto decode = [&](int64_t off) {
-    for (int a = 0; a < g.rank; ++a) {
-      coord[a] = off % g.dims[a];
-      off /= g.dims[a];
+  int64_t off = 0;
+  // raster coordinates of `off`, advanced incrementally (no 64-bit div/mod
+  // per event unless the scan jumps more than a row)
+  int64_t cx = 0, cy = 0, cz = 0, prev = 0;
+  while (off < n) {
+    // next unmarked voxel (short runs: a byte loop beats memchr's call cost)
+    while (off < n && markers[off]) ++off;
+    if (off >= n) break;
+    {
+      const int64_t d = off - prev;
+      if (d < dim[0] - cx) {
+        cx += d;
+      } else {
+        int64_t r = off;
+        cx = r % dim[0];
+        r /= dim[0];
+        cy = r % dim[1];
+        cz = r / dim[1];
+      }
+      prev = off;
     }
-  };
-  for (int64_t off = 0; off < n; ++off) {
-    if (markers[off]) continue;
     const uint32_t label = labels[off];
-    comp.clear();
-    stack.clear();
-    stack.push_back(off);
-    visited[off] = 1;
-    while (!stack.empty()) {
-      const int64_t o = stack.back();
-      stack.pop_back();
-      comp.push_back(o);
-      decode(o);
-      for (int a = 0; a < g.rank; ++a) {
-        if (coord[a] > 0) {
-          const int64_t nb = o - g.strides[a];
-          if (!visited[nb] && labels[nb] == label) {
-            visited[nb] = 1;
-            stack.push_back(nb);
-          }
-        }
-        if (coord[a] + 1 < g.dims[a]) {
-          const int64_t nb = o + g.strides[a];
-          if (!visited[nb] && labels[nb] == label) {
-            visited[nb] = 1;
-            stack.push_back(nb);
-          }
-        }
-      }
-    }
-    for (int64_t o : comp) visited[o] = 0;
-    if ((int64_t)comp.size() > min_size) {
-      for (int64_t o : comp) {
-        labels[o] = next_label;
-        markers[o] = 1;
-      }
-      ++next_label;
-      continue;
-    }
+    // one pass: the fill (same label, face-connected, marks ignored as in
+    // scanline_fill) and, from its boundary, the merge candidates
     int64_t best_before = -1, best_after = -1, best_pending = -1;
     uint32_t label_before = 0, label_after = 0, label_pending = 0;
-    for (int64_t o : comp) {
-      decode(o);
-      for (int a = 0; a < g.rank; ++a) {
+    comp.clear();
+    {
+      Vox v;
+      v.off = off;
+      v.c[0] = (int32_t)cx;
+      v.c[1] = (int32_t)cy;
+      v.c[2] = (int32_t)cz;
+      comp.push_back(v);
+      mk[off] |= 2;
+    }
+    for (size_t head = 0; head < comp.size(); ++head) {
+      const Vox v = comp[head];
+      for (int a = 0; a < rank; ++a) {
         for (int dir = -1; dir <= 1; dir += 2) {
-          const int64_t c = coord[a] + dir;
-          if (c < 0 || c >= g.dims[a]) continue;
-          const int64_t adj = o + dir * g.strides[a];
-          if (labels[adj] == label) continue;
-          if (markers[adj]) {
+          const int64_t c = v.c[a] + dir;
+          if (c < 0 || c >= dim[a]) continue;
+          const int64_t adj = v.off + dir * str[a];
+          const uint32_t la = labels[adj];
+          const uint8_t m = mk[adj];
+          if (la == label) {
+            if (!(m & 2)) {
+              mk[adj] = m | 2;
+              Vox w = v;
+              w.off = adj;
+              w.c[a] = (int32_t)c;
+              comp.push_back(w);
+            }
+          } else if (m & 1) {
             if (adj < off) {
               if (adj > best_before) {
                 best_before = adj;
-                label_before = labels[adj];
+                label_before = la;
               }
             } else if (best_after < 0 || adj < best_after) {
               best_after = adj;
-              label_after = labels[adj];
+              label_after = la;
             }
           } else if (best_pending < 0 || adj < best_pending) {
             best_pending = adj;
-            label_pending = labels[adj];
+            label_pending = la;
           }
         }
       }
     }
-    if (best_before >= 0 || best_after >= 0) {
-      const uint32_t target = best_before >= 0 ? label_before : label_after;
-      for (int64_t o : comp) {
-        labels[o] = target;
-        markers[o] = 1;
-      }
+    uint32_t target;
+    uint8_t mark = 1;
+    if ((int64_t)comp.size() > min_size) {
+      target = next_label++;
+    } else if (best_before >= 0 || best_after >= 0) {
+      target = best_before >= 0 ? label_before : label_after;
     } else if (best_pending >= 0) {
-      for (int64_t o : comp) labels[o] = label_pending;
+      target = label_pending;  // adopt the pending label, stay unmarked
+      mark = 0;
     } else {
-      for (int64_t o : comp) {
-        labels[o] = next_label;
-        markers[o] = 1;
-      }
-      ++next_label;
+      target = next_label++;
     }
+    for (const Vox& v : comp) {
+      labels[v.off] = target;
+      mk[v.off] = (uint8_t)((mk[v.off] & 1) | mark);
+    }
+    ++off;
   }
   return next_label;
 }
@@ -258,16 +278,44 @@ uint32_t enforce_connectivity_device(const Geom& g, const uint32_t* labels_in,
   k_markers<<<nblk(n), 256, 0, s>>>(parent, final_root, markers, n);
   SSLIC_CUDA_CHECK(cudaGetLastError());
 
-  std::vector<uint32_t> h_labels(n);
-  std::vector<uint8_t> h_markers(n);
-  SSLIC_CUDA_CHECK(cudaMemcpyAsync(h_labels.data(), labels_in, n * sizeof(uint32_t),
+  const auto tc0 = std::chrono::steady_clock::now();
+  // host staging (labels + markers) for the sweep: 2 MB transparent huge
+  // pages (the fills touch neighbouring planes megabytes apart; 4 KB pages
+  // would make nearly every z-neighbour a TLB miss), then pinned for the copies
+  const size_t host_bytes = ((size_t)n * (sizeof(uint32_t) + 1) + (2u << 20) - 1) & ~(size_t)((2u << 20) - 1);
+  uint8_t* host = nullptr;
+  if (posix_memalign(reinterpret_cast<void**>(&host), 2u << 20, host_bytes) != 0)
+    throw Error(SSLIC_ENOMEM, "enforce_connectivity: host staging");
+  madvise(host, host_bytes, MADV_HUGEPAGE);
+  const bool pinned = cudaHostRegister(host, host_bytes, cudaHostRegisterDefault) == cudaSuccess;
+  if (!pinned) cudaGetLastError();
+  uint32_t* h_labels = reinterpret_cast<uint32_t*>(host);
+  uint8_t* h_markers = host + (size_t)n * sizeof(uint32_t);
+  SSLIC_CUDA_CHECK(cudaMemcpyAsync(h_labels, labels_in, n * sizeof(uint32_t),
                                    cudaMemcpyDeviceToHost, s));
-  SSLIC_CUDA_CHECK(cudaMemcpyAsync(h_markers.data(), markers, n, cudaMemcpyDeviceToHost, s));
+  SSLIC_CUDA_CHECK(cudaMemcpyAsync(h_markers, markers, n, cudaMemcpyDeviceToHost, s));
   SSLIC_CUDA_CHECK(cudaStreamSynchronize(s));
-  const uint32_t next = sweep_host(g, h_labels, h_markers, min_size, (uint32_t)g.k);
-  SSLIC_CUDA_CHECK(cudaMemcpyAsync(labels_out, h_labels.data(), n * sizeof(uint32_t),
+  const auto tc1 = std::chrono::steady_clock::now();
+  uint32_t next = 0;
+  try {
+    next = sweep_host(g, h_labels, h_markers, n, min_size, (uint32_t)g.k);
+  } catch (...) {
+    if (pinned) cudaHostUnregister(host);
+    std::free(host);
+    throw;
+  }
+  const auto tc2 = std::chrono::steady_clock::now();
+  SSLIC_CUDA_CHECK(cudaMemcpyAsync(labels_out, h_labels, n * sizeof(uint32_t),
                                    cudaMemcpyHostToDevice, s));
   SSLIC_CUDA_CHECK(cudaStreamSynchronize(s));
+  if (pinned) cudaHostUnregister(host);
+  std::free(host);
+  if (std::getenv("SSLIC_TIMING")) {
+    const auto tc3 = std::chrono::steady_clock::now();
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    std::fprintf(stderr, "[sslic] connectivity: device CCL+finalize+D2H %.1f ms, host sweep %.1f ms, H2D %.1f ms\n",
+                 ms(tc0, tc1), ms(tc1, tc2), ms(tc2, tc3));
+  }
   cudaFreeAsync(parent, s);
   cudaFreeAsync(sizes, s);
   cudaFreeAsync(final_root, s);
