@@ -356,16 +356,20 @@ def main():
         # mean of `reps` timed calls; each call is a whole run (H2D, init,
         # every iteration, D2H of labels/centres/residuals)
         s._check(call())
-        reps = 1 if nvox > (1 << 28) else 5
-        t0 = time.perf_counter()
+        reps = 1 if nvox > (1 << 28) else 9
+        per_call = []
         for _ in range(reps):
+            t0 = time.perf_counter()
             s._check(call())
-        t1 = time.perf_counter()
-        e2e = {"value": nvox * done.value * reps / (t1 - t0), "unit": "voxel-iter/s",
+            per_call.append(time.perf_counter() - t0)
+        sec = statistics.median(per_call)
+        e2e = {"value": nvox * done.value / sec, "unit": "voxel-iter/s",
                "h2d_bytes_per_step": img.numel() * img.element_size(),
                "d2h_bytes_per_step": nvox * 4 + cen.nbytes + res.nbytes,
                "call": "sslic_run_slic (host buffers, pinned)", "iterations": done.value,
-               "seconds_per_call": (t1 - t0) / reps, "timed_calls": reps, "warmup_calls": 1}
+               "seconds_per_call": sec, "timed_calls": reps, "warmup_calls": 1,
+               "statistic": "median over timed calls",
+               "seconds_min_max": [min(per_call), max(per_call)]}
 
     cpu = None
     if not args.no_cpu and world == 1 and rank == 0:

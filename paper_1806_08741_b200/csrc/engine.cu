@@ -92,6 +92,10 @@ Engine::Engine(const sslic_image& img, const sslic_params& p, int device, int64_
   residuals_ = dalloc<double>(max_iter_, s);
   counters_ = dalloc<unsigned long long>(8, s);
   SSLIC_CUDA_CHECK(cudaMemsetAsync(counters_, 0, 8 * sizeof(unsigned long long), s));
+  update_done_ = dalloc<unsigned>(1, s);
+  SSLIC_CUDA_CHECK(cudaMemsetAsync(update_done_, 0, sizeof(unsigned), s));
+  SSLIC_CUDA_CHECK(cudaMemsetAsync(acc_, 0, partials_count() * sizeof(unsigned long long), s));
+  acc_zero_ = true;
   if (dist_mode_) {
     k_fill_f64<<<blocks_for(nv, 256), 256, 0, s>>>(dists_, nv, __builtin_huge_val());
     launch_check("fill dists");
@@ -124,7 +128,7 @@ Engine::~Engine() {
   cudaStream_t s = stream_;
   void* ptrs[] = {centers_, labels_, dists_, acc_, anchors_, cell_of_, cell_count_,
                   cell_start_, cursor_, items_, scan_tmp_, block_partials_, residuals_,
-                  counters_, hist32_, chg_, sums_, region_cand_};
+                  counters_, hist32_, chg_, sums_, region_cand_, update_done_};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, s);
   cudaStreamSynchronize(s);
@@ -191,7 +195,8 @@ void Engine::commit() {
   ++launches_;
   k_bin_fill<<<blocks_for(g_.k, 256), 256, 0, s>>>(g_.k, cell_of_, cell_start_, cursor_, items_);
   launch_check("bin_fill");
-  k_bin_sort<<<blocks_for(g_.ncells, 256), 256, 0, s>>>(g_.ncells, cell_start_, items_);
+  k_bin_sort_reset<<<blocks_for(g_.ncells + 1, 256), 256, 0, s>>>(g_.ncells, cell_start_, items_,
+                                                                  cell_count_, cursor_);
   launch_check("bin_sort");
   if (!dist_mode_) {
     const int s2 = hist32_stride(g_.stride);
@@ -205,10 +210,11 @@ void Engine::assign(bool accumulate) {
   if (!dist_mode_ && iter_ >= max_iter_)
     throw Error(SSLIC_EINVAL, "engine: iteration budget exhausted (history tables)");
   cudaStream_t s = stream_;
-  if (accumulate)
+  // the fused update leaves the deltas zeroed; otherwise clear them here
+  if (accumulate && !acc_zero_)
     SSLIC_CUDA_CHECK(cudaMemsetAsync(acc_, 0, partials_count() * sizeof(unsigned long long), s));
-  SSLIC_CUDA_CHECK(cudaMemsetAsync(counters_, 0, 4 * sizeof(unsigned long long), s));
-  SSLIC_CUDA_CHECK(cudaMemsetAsync(counters_ + 5, 0, 3 * sizeof(unsigned long long), s));
+  if (accumulate) acc_zero_ = false;
+  SSLIC_CUDA_CHECK(cudaMemsetAsync(counters_, 0, 8 * sizeof(unsigned long long), s));
   const int64_t nv = slab_voxels();
   const double* hist = dist_mode_ ? nullptr : centers_;
   if (collect_stats_) {
@@ -297,6 +303,28 @@ void Engine::update() {
   const int next_slot = dist_mode_ ? ((iter_ + 1) & 1) : iter_ + 1;
   double* new_c = centers_ + (size_t)next_slot * g_.k * g_.stride;
   const unsigned nb = blocks_for(g_.k, 256);
+  if (!dist_mode_) {
+    // one fused launch (update + residual + hi/lo split + anchors/cell
+    // counts), then the bins: scan, fill, sort (+ counter reset)
+    const int s2 = hist32_stride(g_.stride);
+    k_update_fused<<<nb, 256, 0, s>>>(g_, shift_, acc_, sums_, old_c, new_c, block_partials_,
+                                      chg_, iter_ + 1, hist32_ + (size_t)(iter_ + 1) * g_.k * s2,
+                                      s2, anchors_, cell_of_, cell_count_, update_done_,
+                                      residuals_ + iter_);
+    launch_check("update_fused");
+    acc_zero_ = true;
+    ++iter_;
+    SSLIC_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(scan_tmp_, scan_tmp_bytes_, cell_count_,
+                                                   cell_start_, (int)(g_.ncells + 1), s));
+    ++launches_;
+    k_bin_fill<<<blocks_for(g_.k, 256), 256, 0, s>>>(g_.k, cell_of_, cell_start_, cursor_,
+                                                     items_);
+    launch_check("bin_fill");
+    k_bin_sort_reset<<<blocks_for(g_.ncells + 1, 256), 256, 0, s>>>(
+        g_.ncells, cell_start_, items_, cell_count_, cursor_);
+    launch_check("bin_sort");
+    return;
+  }
   k_update<<<nb, 256, 0, s>>>(g_, shift_, acc_, sums_, old_c, new_c, block_partials_, chg_,
                               iter_ + 1);
   launch_check("update");

@@ -109,6 +109,8 @@ class Engine {
   int* region_cand_ = nullptr;  // fast path: per-region candidate lists
   float key_scale_ = 1.f;       // fast path: 2^-k operand scaling of the fp32 keys
   bool fast_ok_scale_ = true;
+  unsigned* update_done_ = nullptr;  // last-block counter of k_update_fused
+  bool acc_zero_ = false;            // deltas already zero (fused update)
   double vmax_ = 0.0;
   float abs_margin_ = 0.f;
   std::vector<cudaEvent_t> ev_start_, ev_stop_;

@@ -466,6 +466,110 @@ static __global__ void k_update(Geom g, int shift, const unsigned long long* del
   if (threadIdx.x == 0) block_partials[blockIdx.x] = red[0];
 }
 
+// Fused update for the tag-mode loop (one launch instead of update +
+// residual + anchors + hi/lo split): sums += deltas and the deltas are
+// zeroed for the next iteration; new centre (count > 0) or unchanged; chg;
+// the new table's hi/lo fp32 split row; anchors + anchor-cell counts for the
+// bins; the residual by a last-block reduction (fixed order: deterministic).
+// cell_count must be zero on entry (k_bin_sort_reset leaves it so).
+static __global__ void k_update_fused(Geom g, int shift, unsigned long long* delta,
+                                      unsigned long long* sums, const double* old_c,
+                                      double* new_c, double* block_partials, int* chg,
+                                      int next_table, float2* split_out, int split_stride,
+                                      int* anchors, int* cell_of, int* cell_count,
+                                      unsigned* done, double* residual_out) {
+  const int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  double part = 0.0;
+  if (id < g.k) {
+    long long* a = reinterpret_cast<long long*>(sums) + id * (g.stride + 1);
+    long long* dl = reinterpret_cast<long long*>(delta) + id * (g.stride + 1);
+    for (int i = 0; i <= g.stride; ++i) {
+      a[i] += dl[i];
+      dl[i] = 0;
+    }
+    const long long cnt = a[g.stride];
+    const double* o = old_c + id * g.stride;
+    double* n = new_c + id * g.stride;
+    bool changed = false;
+    float2* sp = split_out + id * split_stride;
+    for (int i = 0; i < g.stride; ++i) {
+      double v = o[i];
+      if (cnt != 0) {
+        const double s = i < g.channels ? ldexp((double)a[i], -shift) : (double)a[i];
+        v = __ddiv_rn(s, (double)cnt);
+        const double d = __dsub_rn(v, o[i]);
+        part = __dadd_rn(part, __dmul_rn(d, d));
+        changed |= __double_as_longlong(v) != __double_as_longlong(o[i]);
+      }
+      n[i] = v;
+      const float h = __double2float_rn(v);
+      sp[i] = make_float2(h, __double2float_rn(v - (double)h));
+    }
+    for (int i = g.stride; i < split_stride; ++i) sp[i] = make_float2(0.f, 0.f);
+    if (changed) chg[id] = next_table;
+    int64_t cell = 0, mul = 1;
+    for (int ax = 0; ax < g.rank; ++ax) {
+      const int64_t an = anchor_of(n[g.channels + ax]);
+      anchors[id * kMaxRank + ax] = (int)an;
+      cell += clamp_cell(an, g.grid[ax], g.cells[ax]) * mul;
+      mul *= g.cells[ax];
+    }
+    for (int ax = g.rank; ax < kMaxRank; ++ax) anchors[id * kMaxRank + ax] = 0;
+    cell_of[id] = (int)cell;
+    atomicAdd(cell_count + cell, 1);
+  }
+  __shared__ double red[256];
+  __shared__ bool last;
+  red[threadIdx.x] = part;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] = __dadd_rn(red[threadIdx.x], red[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    block_partials[blockIdx.x] = red[0];
+    __threadfence();
+    last = atomicAdd(done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double t = 0.0;
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x)
+    t = __dadd_rn(t, *((volatile double*)block_partials + i));
+  red[threadIdx.x] = t;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] = __dadd_rn(red[threadIdx.x], red[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    *residual_out = sqrt(red[0]);
+    *done = 0;  // ready for the next launch
+  }
+}
+
+// k_bin_sort that also re-zeroes the cell counters and fill cursors for the
+// next k_update_fused / k_bin_fill.
+static __global__ void k_bin_sort_reset(int64_t ncells, const int* cell_start, int* items,
+                                        int* cell_count, int* cursor) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c > ncells) return;
+  cell_count[c] = 0;
+  if (c == ncells) return;
+  cursor[c] = 0;
+  const int b = cell_start[c], e = cell_start[c + 1];
+  for (int i = b + 1; i < e; ++i) {
+    const int v = items[i];
+    int j = i - 1;
+    while (j >= b && items[j] > v) {
+      items[j + 1] = items[j];
+      --j;
+    }
+    items[j + 1] = v;
+  }
+}
+
 static __global__ void k_residual_final(const double* block_partials, int nblocks, double* residual_out) {
   __shared__ double red[1024];
   double s = 0.0;
