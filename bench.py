@@ -145,6 +145,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--path", default="auto", choices=["auto", "exact"])
+    ap.add_argument("--no-graph", action="store_true", help="launch steps directly (N=1)")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
@@ -206,7 +207,9 @@ def main():
     # uint16 volumes live in int16 storage (same bytes; the engine reads uint16)
     tdt = {np.uint8: torch.uint8, np.uint16: torch.int16, np.float32: torch.float32}[dtype]
     img = torch.empty((drange[1] - drange[0]) * plane * ch, dtype=tdt, device="cuda")
-    stream = torch.cuda.current_stream()
+    # a dedicated (non-legacy) stream: CUDA graph capture needs one
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     if len(dims) == 3:
         s.synth_generate(args.config, dims, dtype, ch, SEED, drange[0], drange[1],
                          img.data_ptr(), stream.cuda_stream)
@@ -239,26 +242,39 @@ def main():
     # Inputs larger than L2 (configs 3-5): one event pair around the K steps.
     # Inputs that fit in L2 (configs 1-2): each step timed by its own events
     # with a 512 MB L2-flushing write between steps, outside the timed spans.
+    # On one GPU the steps run as CUDA graphs (capture outside the timed
+    # span, one launch inside it), which removes the per-kernel launch gaps
+    # that dominate the small configs; with NCCL between steps (N > 1) they
+    # are launched directly.
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda") if fits_l2 else None
+    graphs = world == 1 and not args.no_graph
+    config["launch"] = "CUDA graph per timed span" if graphs else "direct launches"
     if flush is None:
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ev0.record(stream)
-        for _ in range(args.steps):
-            loop.iterate()
-        ev1.record(stream)
-        torch.cuda.synchronize()
-        ms = ev0.elapsed_time(ev1)
+        if graphs:
+            ms = eng.iterate_graph(args.steps)
+        else:
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record(stream)
+            for _ in range(args.steps):
+                loop.iterate()
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            ms = ev0.elapsed_time(ev1)
     else:
+        ms = 0.0
         evs = []
         for _ in range(args.steps):
             flush.fill_(1)
+            if graphs:
+                ms += eng.iterate_graph(1)
+                continue
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             loop.iterate()
             e1.record(stream)
             evs.append((e0, e1))
         torch.cuda.synchronize()
-        ms = sum(e0.elapsed_time(e1) for e0, e1 in evs)
+        ms += sum(e0.elapsed_time(e1) for e0, e1 in evs)
         del flush
     if world > 1:
         tdist.barrier()
@@ -356,7 +372,7 @@ def main():
         # mean of `reps` timed calls; each call is a whole run (H2D, init,
         # every iteration, D2H of labels/centres/residuals)
         s._check(call())
-        reps = 1 if nvox > (1 << 28) else 9
+        reps = 3 if nvox > (1 << 28) else 9
         per_call = []
         for _ in range(reps):
             t0 = time.perf_counter()

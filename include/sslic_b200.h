@@ -155,6 +155,9 @@ int sslic_engine_partials(sslic_engine* e, int64_t** dev_ptr, int64_t* count);
 int sslic_engine_update(sslic_engine* e);
 /* assign + update (single slab covering the whole image). */
 int sslic_engine_iterate(sslic_engine* e, int iterations);
+/* Same, captured as one CUDA graph and launched once (single-GPU loops);
+ * ms_out (nullable) receives the device time of the launch. */
+int sslic_engine_iterate_graph(sslic_engine* e, int iterations, float* ms_out);
 
 int sslic_engine_iterations_done(sslic_engine* e);
 /* Copies residuals of the iterations done so far (host). Synchronizes. */

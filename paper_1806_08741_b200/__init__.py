@@ -113,6 +113,7 @@ def lib():
         "sslic_engine_partials": (C.c_int, [vp, C.POINTER(vp), i64p]),
         "sslic_engine_update": (C.c_int, [vp]),
         "sslic_engine_iterate": (C.c_int, [vp, C.c_int]),
+        "sslic_engine_iterate_graph": (C.c_int, [vp, C.c_int, C.POINTER(C.c_float)]),
         "sslic_engine_iterations_done": (C.c_int, [vp]),
         "sslic_engine_residuals": (C.c_int, [vp, f64p]),
         "sslic_engine_labels": (C.c_int, [vp, vp]),
@@ -541,6 +542,13 @@ class Engine:
 
     def iterate(self, n: int = 1):
         _check(lib().sslic_engine_iterate(self.h, n))
+
+    def iterate_graph(self, n: int) -> float:
+        """n iterations captured in one CUDA graph and launched once; returns
+        the launch's device time in ms."""
+        ms = C.c_float(0)
+        _check(lib().sslic_engine_iterate_graph(self.h, int(n), C.byref(ms)))
+        return float(ms.value)
 
     def iterations_done(self):
         return lib().sslic_engine_iterations_done(self.h)

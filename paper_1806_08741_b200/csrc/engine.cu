@@ -229,9 +229,13 @@ void Engine::assign(bool accumulate) {
     ev_start_.push_back(a);
     ev_stop_.push_back(b);
   }
-  SSLIC_CUDA_CHECK(cudaEventRecord(ev_start_[n_assign_], s));
+  // inside a graph capture the timing events must be external record nodes
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  SSLIC_CUDA_CHECK(cudaStreamIsCapturing(s, &cap));
+  const unsigned rf = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0u;
+  SSLIC_CUDA_CHECK(cudaEventRecordWithFlags(ev_start_[n_assign_], s, rf));
   launch_assign_kernel(accumulate);
-  SSLIC_CUDA_CHECK(cudaEventRecord(ev_stop_[n_assign_], s));
+  SSLIC_CUDA_CHECK(cudaEventRecordWithFlags(ev_stop_[n_assign_], s, rf));
   ++n_assign_;
 }
 

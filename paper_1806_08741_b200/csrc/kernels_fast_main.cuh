@@ -922,6 +922,14 @@ __global__ void __launch_bounds__(128) k_region_cand(FastParams P, int64_t nregi
 // neighbourhood prod (f_a + 2) stays <= 48 cells (headroom to kFastMaxCand
 // for drifted centres). Larger regions amortize the per-CTA staging.
 inline void region_extents(const Geom& g, int* R) {
+  // Grow cell-aligned regions (fewer CTAs, more voxels per candidate
+  // staging) up to 8192 voxels, <= 48 cells of candidates, <= 64 per axis,
+  // but keep at least ~8 CTAs per SM on small images (a 512^2 image would
+  // otherwise be 64 CTAs on 148 SMs).
+  int64_t nvox = 1;
+  for (int a = 0; a < g.rank; ++a)
+    nvox *= (a == g.rank - 1 && g.rank == 3) ? (g.slab_end - g.slab_begin) : g.dims[a];
+  const int64_t vox_cap = nvox / (8 * 148);
   int f[3] = {1, 1, 1};
   for (;;) {
     int best = -1;
@@ -935,6 +943,7 @@ inline void region_extents(const Geom& g, int* R) {
     int64_t vox = 1;
     for (int a = 0; a < g.rank; ++a) vox *= (int64_t)f[a] * g.grid[a];
     if (best < 0 || vox >= 8192) break;
+    if (vox / f[best] * (f[best] + 1) > vox_cap) break;
     ++f[best];
   }
   for (int a = 0; a < 3; ++a) R[a] = a < g.rank ? f[a] * g.grid[a] : 1;
@@ -1038,9 +1047,13 @@ void launch_fast_t(const FastParams& P, size_t smem, int64_t nblocks, cudaStream
     if (R[0] == 32 && R[1] == 32 && R[2] == 32)
       return launch_fast_shape<RANK, C, T, 32, 32, 32>(P, smem, nblocks, s);  // config 5
   }
-  if constexpr (RANK == 2 && C == 3 && sizeof(T) != 2) {
-    if (R[0] == 64 && R[1] == 64)
-      return launch_fast_shape<RANK, C, T, 64, 64, 1>(P, smem, nblocks, s);  // configs 1, 2
+  if constexpr (RANK == 2 && C == 3 && sizeof(T) == 4) {
+    if (R[0] == 64 && R[1] == 32)
+      return launch_fast_shape<RANK, C, T, 64, 32, 1>(P, smem, nblocks, s);  // config 2
+  }
+  if constexpr (RANK == 2 && C == 3 && sizeof(T) == 1) {
+    if (R[0] == 16 && R[1] == 16)
+      return launch_fast_shape<RANK, C, T, 16, 16, 1>(P, smem, nblocks, s);  // config 1
   }
   launch_fast_shape<RANK, C, T, 0, 0, 0>(P, smem, nblocks, s);
 }
