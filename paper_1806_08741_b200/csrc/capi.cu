@@ -3,6 +3,9 @@
 // failure is reported as a status code mirroring the reference's exception
 // classes, with the message in sslic_last_error().
 #include <cmath>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -94,6 +97,21 @@ struct DeviceBuf {
   T* as() const { return static_cast<T*>(p); }
 };
 
+// Keep freed device memory in the stream-ordered pool across calls (the
+// default release threshold returns it to the driver at every sync, so each
+// whole-run call would re-map gigabytes).
+void keep_pool_memory(int device) {
+  static bool done[64] = {};
+  if (device < 0 || device >= 64 || done[device]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  cudaGetLastError();
+  done[device] = true;
+}
+
 struct Stream {
   cudaStream_t s = nullptr;
   explicit Stream(int device) {
@@ -102,6 +120,7 @@ struct Stream {
       throw Error(SSLIC_ECUDA, "no CUDA device available (the B200 path has no CPU fallback)");
     if (device < 0 || device >= n) throw Error(SSLIC_EINVAL, "device index out of range");
     SSLIC_CUDA_CHECK(cudaSetDevice(device));
+    keep_pool_memory(device);
     SSLIC_CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
   }
   ~Stream() {
@@ -123,6 +142,30 @@ __global__ void k_count_nonfinite(const void* data, int dtype, int64_t n, unsign
 }
 
 // Uploads a host image; checks finiteness like the NDImage constructor.
+// SSLIC_TIMING=1: per-phase wall times of the whole-run entry points (stderr).
+struct PhaseTimer {
+  const char* what;
+  bool on;
+  std::chrono::steady_clock::time_point t0;
+  std::string line;
+  explicit PhaseTimer(const char* w) : what(w), on(std::getenv("SSLIC_TIMING") != nullptr) {
+    t0 = std::chrono::steady_clock::now();
+  }
+  void mark(Stream& st, const char* phase) {
+    if (!on) return;
+    st.sync();
+    const auto t = std::chrono::steady_clock::now();
+    char buf[96];
+    std::snprintf(buf, sizeof buf, " %s %.1f ms", phase,
+                  std::chrono::duration<double, std::milli>(t - t0).count());
+    line += buf;
+    t0 = t;
+  }
+  ~PhaseTimer() {
+    if (on) std::fprintf(stderr, "[sslic] %s:%s\n", what, line.c_str());
+  }
+};
+
 std::unique_ptr<DeviceBuf> upload_image(const sslic_image* img, Stream& st) {
   const int64_t nvals = pixel_count(*img) * img->channels;
   const size_t bytes = (size_t)nvals * dtype_size(img->dtype);
@@ -161,9 +204,13 @@ int run_loop(Engine& e, const sslic_params* p, Stream& st) {
   e.init(true);
   e.commit();
   const int iters = e.max_iterations();
+  // Tag mode: the fused update latches "an assignment left a voxel
+  // undefined" on the device, so the loop needs no host sync per iteration;
+  // the reference's logic_error (slic.hpp:330-331) is raised after it.
+  const bool latched = !e.dist_mode();
   for (int it = 0; it < iters; ++it) {
     e.assign(true);
-    if (e.undefined_count() > 0)  // slic.hpp:330-331
+    if (!latched && e.undefined_count() > 0)  // slic.hpp:330-331
       throw Error(SSLIC_ELOGIC, "accumulate_region: pixel with undefined label");
     e.update();
     if (p->has_residual_threshold) {
@@ -175,6 +222,8 @@ int run_loop(Engine& e, const sslic_params* p, Stream& st) {
     }
   }
   st.sync();
+  if (latched && e.undefined_seen())
+    throw Error(SSLIC_ELOGIC, "accumulate_region: pixel with undefined label");
   return e.iterations_done();
 }
 
@@ -232,12 +281,16 @@ int sslic_run_slic(const sslic_image* img, const sslic_params* params, int devic
   return guarded([&] {
     validate_image(img);
     validate_params(params, img);
+    PhaseTimer pt("run_slic");
     Stream st(device);
     auto dimg = upload_image(img, st);
+    pt.mark(st, "upload");
     const sslic_image v = device_view(img, dimg->p);
     const int64_t last = img->dims[img->rank - 1];
     Engine e(v, *params, device, 0, last, 0, last, st.s);
+    pt.mark(st, "engine");
     const int done = run_loop(e, params, st);
+    pt.mark(st, "iterations");
     const int64_t n = pixel_count(*img);
     {
       DeviceBuf lab(n * sizeof(uint32_t), st.s);
@@ -246,6 +299,7 @@ int sslic_run_slic(const sslic_image* img, const sslic_params* params, int devic
                                        cudaMemcpyDeviceToHost, st.s));
       st.sync();
     }
+    pt.mark(st, "labels D2H");
     e.copy_centers_to_host(centers_out);
     if (residuals_out) e.residuals_to_host(residuals_out, done);
     if (iterations_done) *iterations_done = done;

@@ -92,8 +92,8 @@ Engine::Engine(const sslic_image& img, const sslic_params& p, int device, int64_
   residuals_ = dalloc<double>(max_iter_, s);
   counters_ = dalloc<unsigned long long>(8, s);
   SSLIC_CUDA_CHECK(cudaMemsetAsync(counters_, 0, 8 * sizeof(unsigned long long), s));
-  update_done_ = dalloc<unsigned>(1, s);
-  SSLIC_CUDA_CHECK(cudaMemsetAsync(update_done_, 0, sizeof(unsigned), s));
+  update_done_ = dalloc<unsigned>(2, s);  // [0] last-block counter, [1] undefined latch
+  SSLIC_CUDA_CHECK(cudaMemsetAsync(update_done_, 0, 2 * sizeof(unsigned), s));
   SSLIC_CUDA_CHECK(cudaMemsetAsync(acc_, 0, partials_count() * sizeof(unsigned long long), s));
   acc_zero_ = true;
   if (dist_mode_) {
@@ -314,7 +314,7 @@ void Engine::update() {
     k_update_fused<<<nb, 256, 0, s>>>(g_, shift_, acc_, sums_, old_c, new_c, block_partials_,
                                       chg_, iter_ + 1, hist32_ + (size_t)(iter_ + 1) * g_.k * s2,
                                       s2, anchors_, cell_of_, cell_count_, update_done_,
-                                      residuals_ + iter_);
+                                      residuals_ + iter_, counters_, update_done_ + 1);
     launch_check("update_fused");
     acc_zero_ = true;
     ++iter_;
@@ -355,6 +355,14 @@ void Engine::residuals_to_host(double* h, int n) {
   SSLIC_CUDA_CHECK(cudaMemcpyAsync(h, residuals_, n * sizeof(double), cudaMemcpyDeviceToHost,
                                    stream_));
   SSLIC_CUDA_CHECK(cudaStreamSynchronize(stream_));
+}
+
+bool Engine::undefined_seen() {
+  unsigned v = 0;
+  SSLIC_CUDA_CHECK(cudaMemcpyAsync(&v, update_done_ + 1, sizeof(v), cudaMemcpyDeviceToHost,
+                                   stream_));
+  SSLIC_CUDA_CHECK(cudaStreamSynchronize(stream_));
+  return v != 0;
 }
 
 int64_t Engine::undefined_count() {

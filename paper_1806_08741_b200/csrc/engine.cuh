@@ -44,6 +44,9 @@ class Engine {
   void copy_centers_to_host(double* h);
   void residuals_to_host(double* h, int n);
   int64_t undefined_count();
+  // Tag mode: some assign since construction left a voxel undefined (latched
+  // by the fused update; reading it synchronizes).
+  bool undefined_seen();
   int64_t out_of_range_count();
   void eval_stats(double* evals, double* window_evals);
   // Fast path: voxels re-decided in fp64, crowded CTAs (last assign).

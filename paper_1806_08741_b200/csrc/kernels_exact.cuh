@@ -477,8 +477,11 @@ static __global__ void k_update_fused(Geom g, int shift, unsigned long long* del
                                       double* new_c, double* block_partials, int* chg,
                                       int next_table, float2* split_out, int split_stride,
                                       int* anchors, int* cell_of, int* cell_count,
-                                      unsigned* done, double* residual_out) {
+                                      unsigned* done, double* residual_out,
+                                      const unsigned long long* undefined_count,
+                                      unsigned* undefined_seen) {
   const int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (id == 0 && *undefined_count) *undefined_seen = 1u;  // latched for run_slic
   double part = 0.0;
   if (id < g.k) {
     long long* a = reinterpret_cast<long long*>(sums) + id * (g.stride + 1);
