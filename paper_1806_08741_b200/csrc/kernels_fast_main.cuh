@@ -662,7 +662,22 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
     // adds its own contributions straight into the CTA slots. Dense deltas
     // (first iterations): warp-aggregate per label first.
     const unsigned npend = __reduce_add_sync(0xffffffffu, (unsigned)__popc(pending));
-    if (npend <= kSparseDeltas) {
+    bool sparse = npend <= kSparseDeltas;
+    if (!sparse) {
+      // Many contributions: aggregate per label when the box is dominated by
+      // few labels (uniform regions), else per-lane atomics (noisy label
+      // maps: aggregation would take one warp round per distinct label).
+      const int fb = pending ? __ffs(pending) - 1 : 0;
+      uint32_t first = fb < 4 ? newl[0] : oldl[0];
+#pragma unroll
+      for (int u = 1; u < 4; ++u)
+        if ((fb & 3) == u) first = fb < 4 ? newl[u] : oldl[u];
+      const unsigned anyp = __ballot_sync(0xffffffffu, pending != 0);
+      const uint32_t l0 = __shfl_sync(0xffffffffu, first, __ffs(anyp) - 1);
+      const unsigned same = __ballot_sync(0xffffffffu, pending != 0 && first == l0);
+      sparse = 4 * __popc(same) < 3 * __popc(anyp);
+    }
+    if (sparse) {
       while (pending) {
         const int q = __ffs(pending) - 1;
         pending &= pending - 1;
