@@ -102,6 +102,10 @@ def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # functional check of the N>1 code path on a one-GPU box (gloo, every
+    # rank on device 0); never used for reported numbers
+    if os.environ.get("SSLIC_BENCH_FUNCTIONAL_CHECK") == "1":
+        local = 0
     return world, rank, local
 
 
@@ -196,7 +200,10 @@ def main():
 
     if world > 1:
         import torch.distributed as tdist
-        tdist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if os.environ.get("SSLIC_BENCH_FUNCTIONAL_CHECK") == "1":
+            tdist.init_process_group("gloo")
+        else:
+            tdist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     import paper_1806_08741_b200 as s
     from paper_1806_08741_b200.sharded import ShardedLoop, data_bounds, slab_bounds
 
@@ -342,6 +349,43 @@ def main():
 
     # end-to-end through the reference-facing C ABI with HOST buffers
     e2e = None
+    if not args.no_e2e and world > 1:
+        # N GPUs: the public multi-GPU API end to end on every rank — H2D of
+        # the rank's slab (+ halo) from pinned host memory, engine setup,
+        # init + all iterations with the NCCL allreduce, D2H of the slab's
+        # labels; wall time between barriers, max over ranks.
+        import torch.distributed as tdist
+        host = torch.empty(img.numel(), dtype=tdt, pin_memory=True)
+        host.copy_(img)
+        slab_vox_e = (slab[1] - slab[0]) * plane
+        labels_h = torch.empty(slab_vox_e, dtype=torch.int32, pin_memory=True)
+        del eng
+        torch.cuda.synchronize()
+        tdist.barrier()
+        t0 = time.perf_counter()
+        img2 = torch.empty_like(img)
+        img2.copy_(host, non_blocking=True)
+        p2 = s.SlicParams(grid=list(grid), weight_m=m, max_iterations=cfg_iters)
+        eng2 = s.Engine(dims, ch, dtype, img2.data_ptr(), p2, slab=slab, data_range=drange,
+                        device=local, stream=stream.cuda_stream)
+        loop2 = ShardedLoop(eng2, allreduce, world)
+        loop2.init()
+        for _ in range(cfg_iters):
+            loop2.iterate()
+        lab_d = torch.empty(slab_vox_e, dtype=torch.int32, device="cuda")
+        eng2.labels_to(lab_d.data_ptr())
+        labels_h.copy_(lab_d)
+        torch.cuda.synchronize()
+        dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+        tdist.all_reduce(dt, op=tdist.ReduceOp.MAX)
+        sec = float(dt.item())
+        e2e = {"value": nvox * cfg_iters / sec, "unit": "voxel-iter/s",
+               "h2d_bytes_per_step": img.numel() * img.element_size(),
+               "d2h_bytes_per_step": slab_vox_e * 4,
+               "call": "Engine + ShardedLoop per rank (host buffers, pinned), NCCL allreduce",
+               "iterations": cfg_iters, "seconds_per_call": sec, "timed_calls": 1,
+               "note": "bytes are per rank"}
+        eng2.close()
     if not args.no_e2e and world == 1:
         host = torch.empty(img.numel(), dtype=tdt, pin_memory=True)
         host.copy_(img)
