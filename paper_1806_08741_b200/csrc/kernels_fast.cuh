@@ -78,7 +78,6 @@ struct BoxShape {
 struct alignas(16) FastSmem {
   int n_cand;
   int id[kFastMaxCand];
-  int cchg[kFastMaxCand];  // chg[] of each candidate (first table of its current centre)
   short anc[kFastMaxCand][3];  // region-local anchors
   unsigned short wl[kFastThreads / 32][kFastMaxCand + 8];   // record offsets (floats)
   unsigned short htab[2 * kFastMaxCand];                               // cluster id -> slot

@@ -90,7 +90,8 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
   const int RXp = (RX + 3) & ~3;
   // (c_hi, c_lo) per channel after the tables, 8-byte aligned
   const int HO = (RXp + RY + (RANK == 3 ? RZ : 0) + 1) & ~1;
-  const int RS = (HO + 2 * C + 3) & ~3;
+  // record: [sx | sy | sz | (c_hi, c_lo) x C | cluster id, chg], 16-byte rows
+  const int RS = (HO + 2 * C + 2 + 3) & ~3;
   float* rec = reinterpret_cast<float*>(smem_raw + sizeof(FastSmem));  // [cand+1][RS]
   unsigned long long* accs =
       reinterpret_cast<unsigned long long*>(rec + (size_t)(kFastMaxCand + 1) * RS);
@@ -217,7 +218,9 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
     float* r = rec + (size_t)j * RS;
     if (j < n) {
       const int kid = sm.id[j];
-      sm.cchg[j] = __ldg(P.chg + kid);
+      // the winner's id and chg sit in its record: one load in the decisions
+      r[HO + 2 * C] = __int_as_float(kid);
+      r[HO + 2 * C + 1] = __int_as_float(__ldg(P.chg + kid));
       const float2* c32 = P.cur32 + (int64_t)kid * kS2;  // hi/lo split of the current table
 #pragma unroll
       for (int c = 0; c < C; ++c) {
@@ -236,11 +239,14 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
       }
     } else {
 #pragma unroll
-      for (int c = 0; c < 2 * C; ++c) r[HO + c] = 0.f;
+      for (int c = 0; c < 2 * C + 2; ++c) r[HO + c] = 0.f;
     }
   }
   for (int i = tid; i < n * kComp; i += kFastThreads) accs[i] = 0ull;
   for (int i = tid; i < kSlotHash; i += kFastThreads) sm.htab[i] = 0xffff;
+  // compaction lists start as valid record offsets: a voxel without any kept
+  // candidate still reads a (never used) winner record
+  for (int i = tid; i < kWarps * (kFastMaxCand + 8); i += kFastThreads) (&sm.wl[0][0])[i] = 0;
   __syncthreads();
   for (int j = tid; j < n; j += kFastThreads) {  // id -> slot hash (linear probing)
     int h = slot_hash((uint32_t)sm.id[j]);
@@ -315,7 +321,7 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
   }
   __syncthreads();
 
-  // ---- per-warp sweep over the region's boxes (dynamically claimed) ----
+  // ---- per-warp sweep over the region's boxes ----
   int buf = 0;
 #pragma unroll 1
   for (int b = warp; b < nbox; b += kWarps, buf ^= 1) {
@@ -609,19 +615,20 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
     for (int v = 0; v < 4; ++v) {
       oldl[v] = word[v] & lmask;  // undefined -> lmask (never a label)
       const bool live = valid[v] && best[v] < kSentKey;  // else: keep (nothing kept beats d_old)
-      const int jstar = (int)sm.wl[warp][grp[v] + (best[v] & 7u)] / RS;  // record -> slot
-      const uint32_t kid = (uint32_t)sm.id[jstar];
+      const int roff = sm.wl[warp][grp[v] + (best[v] & 7u)];  // winner's record
+      const int2 ic = *reinterpret_cast<const int2*>(rec + roff + HO + 2 * C);
+      const uint32_t kid = (uint32_t)ic.x;
       const float bv = kval(best[v]);
       const float thr = fmaf(bv, M1, A);
       const bool amb = kval(second[v]) <= thr;
       // same centre as when the label was set: D* == d_old exactly -> keep
-      const bool same = kid == oldl[v] && sm.cchg[jstar] <= (int)(word[v] >> lbits);
+      const bool same = kid == oldl[v] && ic.y <= (int)(word[v] >> lbits);
       const bool upd = !amb && !same && thr < dold[v];
       const bool keep = !amb && (same || bv > fmaf(dold[v], M1, A));
       nword[v] = live && upd ? (tag_now_bits | kid) : word[v];
       if (live && !upd && !keep) exact_mask |= 1u << v;
       if (amb) amb_mask |= 1u << v;
-      jst[v] = jstar;
+      jst[v] = roff;
     }
     // undecided voxels are queued in the warp's (now free) history staging
     // area and re-decided in fp64 after the box, one voxel per lane
@@ -631,7 +638,7 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
         if (exact_mask >> v & 1u) {
           // deferred fp64 re-decision: region-local voxel coordinates, amb, slot
           const uint32_t info = (uint32_t)(lx0 + v) | (uint32_t)ly << 6 | (uint32_t)lz << 12 |
-                                (amb_mask >> v & 1u) << 18 | (uint32_t)jst[v] << 19;
+                                (amb_mask >> v & 1u) << 18 | (uint32_t)(jst[v] / RS) << 19;
           xqueue[atomicAdd(xcnt, 1)] = make_uint2(word[v], info);
         }
     }
@@ -1020,7 +1027,7 @@ inline bool fast_path_supported(const Geom& g) {
 inline size_t fast_smem_bytes(const Geom& g, const int* R) {
   const int RXp = (R[0] + 3) & ~3;
   const int HO = (RXp + R[1] + (g.rank == 3 ? R[2] : 0) + 1) & ~1;
-  const int RS = (HO + 2 * g.channels + 3) & ~3;
+  const int RS = (HO + 2 * g.channels + 2 + 3) & ~3;
   const int warps = kFastThreads / 32;
   size_t b = sizeof(FastSmem);
   b += (size_t)(kFastMaxCand + 1) * RS * sizeof(float);
