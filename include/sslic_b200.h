@@ -92,6 +92,12 @@ int sslic_init_centers(const sslic_image* img, const sslic_params* params, int p
 /* perturb_centers (slic.hpp:236-267) of a caller-given table (host, in-out). */
 int sslic_perturb_centers(const sslic_image* img, double* centers, int64_t k, int device);
 
+/* convert_image_to_lab (color.hpp:54-66): 3-channel sRGB in [0, 255] to
+ * CIE-Lab, npix*3 doubles into lab_out (host). SSLIC_EINVAL unless 3 channels.
+ * Integral inputs reproduce the reference's transfer values bitwise; the cube
+ * root is the device's (Lab within ~1e-13 of the reference). */
+int sslic_convert_image_to_lab(const sslic_image* img, int device, double* lab_out);
+
 /* gradient_magnitude_sq (color.hpp:71-102) at n coordinates (host, n*rank). */
 int sslic_gradient_sq(const sslic_image* img, const int64_t* coords, int64_t n, int device,
                       double* out);

@@ -145,5 +145,14 @@ inline void assign_labels(const NDImage& img, const ClusterTable& table, const S
                                   labels.data().data(), dists.data().data()));
 }
 
+/// convert_image_to_lab (color.hpp:54-66) on a B200: fp64 Lab image, same
+/// shape; std::invalid_argument unless 3 channels (the C ABI's SSLIC_EINVAL).
+inline NDImage convert_image_to_lab(const NDImage& img, int device = 0) {
+  detail::NativeImage nimg = detail::narrow(img);
+  NDImage out = img;
+  detail::check(sslic_convert_image_to_lab(&nimg.desc, device, out.data().data()));
+  return out;
+}
+
 }  // namespace b200
 }  // namespace sslic

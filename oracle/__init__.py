@@ -73,6 +73,7 @@ class Oracle:
         lib.orc_run_slic.argtypes = [C.c_int, _i64p, C.c_int, _f64p, _i64p, C.c_double, C.c_int,
                                      C.c_int, C.c_double, _u32p, _f64p, _f64p,
                                      C.POINTER(C.c_int)]
+        lib.orc_srgb_to_lab.argtypes = [C.c_int64, _f64p, _f64p]
         lib.orc_size_threshold.restype = C.c_int64
         lib.orc_size_threshold.argtypes = [C.c_int, _i64p]
         lib.orc_finalize.argtypes = [C.c_int, _i64p, _u32p, _f64p, C.c_int, C.c_int64, _i64p,
@@ -188,6 +189,13 @@ class Oracle:
             raise RuntimeError("pixel with undefined label")
         return lab, cen.reshape(k, -1), res[: done.value]
 
+    def srgb_to_lab(self, rgb):
+        """orc_srgb_to_lab: interleaved RGB (n*3) -> Lab (n*3)."""
+        d = np.ascontiguousarray(rgb, dtype=np.float64).reshape(-1)
+        out = np.empty_like(d)
+        self.lib.orc_srgb_to_lab(d.size // 3, _p(d, _f64p), _p(out, _f64p))
+        return out
+
     def size_threshold(self, grid):
         grid = _dims(grid)
         return int(self.lib.orc_size_threshold(len(grid), _p(grid, _i64p)))
@@ -255,6 +263,8 @@ class Reference:
         lib.ref_random_grid.argtypes = [C.c_void_p, C.c_int, _i64p, _i64p]
         lib.ref_random_weight.restype = C.c_double
         lib.ref_random_weight.argtypes = [C.c_void_p]
+        lib.ref_convert_to_lab.restype = C.c_int
+        lib.ref_convert_to_lab.argtypes = [C.c_int, _i64p, _f64p, _f64p]
         lib.ref_time_iterations.restype = C.c_int
         lib.ref_time_iterations.argtypes = [C.c_int, _i64p, C.c_int, _f64p, _i64p, C.c_double,
                                             C.c_int, C.c_int, _f64p, _f64p, _u32p, _f64p]
@@ -319,6 +329,16 @@ class Reference:
                                                _p(grid, _i64p), int(workers), _p(out, _u32p))
         if st != 0:
             raise RuntimeError(f"reference connectivity failed with status {st}")
+        return out
+
+    def convert_to_lab(self, dims, rgb):
+        """convert_image_to_lab (color.hpp:54-66) of the unmodified reference."""
+        dims = _dims(dims)
+        d = np.ascontiguousarray(rgb, dtype=np.float64).reshape(-1)
+        out = np.empty_like(d)
+        st = self.lib.ref_convert_to_lab(len(dims), _p(dims, _i64p), _p(d, _f64p), _p(out, _f64p))
+        if st != 0:
+            raise ValueError(f"reference convert_image_to_lab failed with status {st}")
         return out
 
     def time_iterations(self, data, dims, channels, grid, weight_m, iterations, workers):

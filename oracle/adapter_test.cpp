@@ -7,6 +7,10 @@
 #include <cstdio>
 #include <random>
 
+#include <algorithm>
+#include <cmath>
+
+#include "sslic/color.hpp"
 #include "sslic/connectivity.hpp"
 #include "sslic/slic.hpp"
 #include "support/oracles.hpp"
@@ -35,6 +39,27 @@ int main() {
       ++failures;
     }
     ++cases;
+  }
+  // convert_image_to_lab: same shape, Lab within 1e-12 (the two cube roots
+  // are each within 1 ulp), invalid_argument for a non-RGB image
+  {
+    sslic::NDImage rgb = oracle::random_image(rng, 2, 24, 3);
+    for (double& v : rgb.data()) v = static_cast<double>(static_cast<int>(v * 255.0 / 256.0));
+    const sslic::NDImage a = sslic::convert_image_to_lab(rgb);
+    const sslic::NDImage b = sslic::b200::convert_image_to_lab(rgb);
+    double worst = 0.0;
+    for (std::size_t j = 0; j < a.data().size(); ++j)
+      worst = std::max(worst, std::abs(a.data()[j] - b.data()[j]));
+    if (!(a.dims() == b.dims()) || !(worst < 1e-12)) {
+      std::printf("convert_image_to_lab differs (max %.3g)\n", worst);
+      ++failures;
+    }
+    ++cases;
+    try {
+      sslic::b200::convert_image_to_lab(sslic::NDImage::zeros(sslic::Shape{2, 2}, 1));
+      ++failures;
+    } catch (const std::invalid_argument&) {
+    }
   }
   // exceptions keep the reference's classes
   try {

@@ -137,6 +137,19 @@ int ref_enforce_connectivity(int rank, const int64_t* dims, const uint32_t* labe
   }
 }
 
+// convert_image_to_lab (color.hpp:54-66) on an interleaved 3-channel image.
+int ref_convert_to_lab(int rank, const int64_t* dims, const double* rgb, double* lab_out) {
+  try {
+    const Shape shape = make_shape(rank, dims);
+    NDImage img(shape, 3, std::vector<double>(rgb, rgb + pixel_count(shape) * 3));
+    const NDImage out = convert_image_to_lab(img);
+    std::memcpy(lab_out, out.data().data(), sizeof(double) * out.data().size());
+    return 0;
+  } catch (...) {
+    return status_of(std::current_exception());
+  }
+}
+
 // The test-suite randomized image generator (oracles.hpp:302-311) driven by
 // mt19937_64, exactly as the reference's corpora draw it. State is kept in an
 // opaque handle so a Python script can replay a corpus sequence.

@@ -297,6 +297,31 @@ int orc_run_slic(int rank, const int64_t* dims, int channels, const double* data
 /* Connectivity                                                            */
 /* ---------------------------------------------------------------------- */
 
+/* color.hpp:21-24: IEC 61966-2-1 transfer function on [0, 1]. */
+static double orc_linearize(double u) {
+  return u <= 0.04045 ? u / 12.92 : pow((u + 0.055) / 1.055, 2.4);
+}
+/* color.hpp:27-31: CIE 1976 pivot, eps = 216/24389, kappa = 24389/27. */
+static double orc_pivot(double t) {
+  const double eps = 216.0 / 24389.0, kappa = 24389.0 / 27.0;
+  return t > eps ? cbrt(t) : (kappa * t + 16.0) / 116.0;
+}
+/* color.hpp:36-52: sRGB (D65) -> linear -> XYZ (2 degree) -> Lab. */
+void orc_srgb_to_lab(int64_t n, const double* rgb, double* lab) {
+  for (int64_t i = 0; i < n; ++i) {
+    const double r = orc_linearize(rgb[3 * i] / 255.0);
+    const double g = orc_linearize(rgb[3 * i + 1] / 255.0);
+    const double b = orc_linearize(rgb[3 * i + 2] / 255.0);
+    const double x = 0.4124564 * r + 0.3575761 * g + 0.1804375 * b;
+    const double y = 0.2126729 * r + 0.7151522 * g + 0.0721750 * b;
+    const double z = 0.0193339 * r + 0.1191920 * g + 0.9503041 * b;
+    const double fx = orc_pivot(x / 0.95047), fy = orc_pivot(y / 1.0), fz = orc_pivot(z / 1.08883);
+    lab[3 * i] = 116.0 * fy - 16.0;
+    lab[3 * i + 1] = 500.0 * (fx - fy);
+    lab[3 * i + 2] = 200.0 * (fy - fz);
+  }
+}
+
 int64_t orc_size_threshold(int rank, const int64_t* grid) {
   /* connectivity.hpp:34-38 */
   int64_t p = 1;

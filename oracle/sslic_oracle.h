@@ -78,6 +78,9 @@ int orc_run_slic(int rank, const int64_t* dims, int channels, const double* data
 /* size_threshold (connectivity.hpp:34-38) */
 int64_t orc_size_threshold(int rank, const int64_t* grid);
 
+/* srgb_to_cielab (color.hpp:21-52) for n interleaved RGB pixels in [0, 255]. */
+void orc_srgb_to_lab(int64_t n, const double* rgb, double* lab);
+
 /* finalize_cluster_components (connectivity.hpp:125-173): markers (N bytes) in-out. */
 void orc_finalize(int rank, const int64_t* dims, const uint32_t* labels, const double* centers,
                   int channels, int64_t k, const int64_t* grid, uint8_t* markers);

@@ -95,6 +95,7 @@ def lib():
         "sslic_init_centers": (C.c_int, [ip, pp, C.c_int, C.c_int, f64p]),
         "sslic_perturb_centers": (C.c_int, [ip, f64p, C.c_int64, C.c_int]),
         "sslic_gradient_sq": (C.c_int, [ip, i64p, C.c_int64, C.c_int, f64p]),
+        "sslic_convert_image_to_lab": (C.c_int, [ip, C.c_int, f64p]),
         "sslic_squared_distance": (C.c_int, [C.c_int, C.c_int, i64p, C.c_double, C.c_int64,
                                              f64p, f64p, i64p, C.c_int, f64p]),
         "sslic_assign_pass": (C.c_int, [ip, pp, f64p, C.c_int64, C.c_int, u32p, f64p]),
@@ -351,6 +352,17 @@ def perturb_centers(img: NDImage, table: ClusterTable, workers: int = 1,
     d = img._desc()
     _check(lib().sslic_perturb_centers(C.byref(d), _p(out, C.c_double), out.shape[0], device))
     return ClusterTable(table.channels, table.rank, out)
+
+
+def convert_image_to_lab(img: NDImage, device: int = 0) -> NDImage:
+    """convert_image_to_lab (color.hpp:54-66): pixelwise sRGB (D65, values in
+    [0, 255]) to CIE-Lab, computed on the GPU; returns an fp64 NDImage.
+    Raises InvalidArgument unless the image has 3 channels."""
+    if img.channels != 3:
+        raise InvalidArgument("convert_image_to_lab: image must have 3 channels")
+    out = np.empty(img.pixel_count() * 3, np.float64)
+    _check(lib().sslic_convert_image_to_lab(C.byref(img._desc()), device, _p(out, C.c_double)))
+    return NDImage(img.dims, 3, out)
 
 
 def gradient_magnitude_sq(img: NDImage, coord, device: int = 0):

@@ -12,6 +12,7 @@
 #include <string>
 #include <vector>
 
+#include "color.cuh"
 #include "connectivity.cuh"
 #include "engine.cuh"
 
@@ -388,6 +389,28 @@ int sslic_perturb_centers(const sslic_image* img, double* centers, int64_t k, in
       SSLIC_CUDA_CHECK(cudaGetLastError());
     }
     SSLIC_CUDA_CHECK(cudaMemcpyAsync(centers, c.p, k * g.stride * sizeof(double),
+                                     cudaMemcpyDeviceToHost, st.s));
+    st.sync();
+    return SSLIC_OK;
+  });
+}
+
+int sslic_convert_image_to_lab(const sslic_image* img, int device, double* lab_out) {
+  return guarded([&] {
+    validate_image(img);
+    if (img->channels != 3)
+      throw Error(SSLIC_EINVAL, "convert_image_to_lab: image must have 3 channels");
+    Stream st(device);
+    auto dimg = upload_image(img, st);
+    const int64_t npix = pixel_count(*img);
+    double table[256];
+    sslic_b200::srgb_linear_table(table);
+    DeviceBuf dt(sizeof(table), st.s), dout(npix * 3 * sizeof(double), st.s);
+    SSLIC_CUDA_CHECK(cudaMemcpyAsync(dt.p, table, sizeof(table), cudaMemcpyHostToDevice, st.s));
+    sslic_b200::srgb_to_lab_device(dimg->p, img->dtype, npix, dt.as<double>(),
+                                   dout.as<double>(), st.s);
+    SSLIC_CUDA_CHECK(cudaGetLastError());
+    SSLIC_CUDA_CHECK(cudaMemcpyAsync(lab_out, dout.p, npix * 3 * sizeof(double),
                                      cudaMemcpyDeviceToHost, st.s));
     st.sync();
     return SSLIC_OK;

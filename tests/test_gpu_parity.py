@@ -217,3 +217,26 @@ def test_errors(sslic):
         s.run_slic(img, s.SlicParams(grid=[4, 4], weight_m=0.0))
     with pytest.raises(s.InvalidArgument):
         s.run_slic(img, s.SlicParams(grid=[4, 4]), workers=0)
+
+
+def test_convert_image_to_lab_matches_reference(sslic, reference_lib):
+    """GPU sRGB -> Lab against the unmodified reference:
+    u8 images, integral f64 and fractional f32 data. The transfer function
+    of integral inputs is the reference's bit for bit (host table); the cube
+    root is the device's, so Lab is compared at 1e-12 absolute."""
+    s = sslic
+    rng = np.random.default_rng(11)
+    dims = (37, 23, 5)
+    n = int(np.prod(dims))
+    cases = [rng.integers(0, 256, size=n * 3).astype(np.uint8),
+             rng.integers(0, 256, size=n * 3).astype(np.float64),
+             rng.uniform(0.0, 255.0, size=n * 3).astype(np.float32)]
+    for x in cases:
+        ours = s.convert_image_to_lab(s.NDImage(dims, 3, x))
+        ref = reference_lib.convert_to_lab(dims, x.astype(np.float64))
+        got = np.asarray(ours.data, np.float64).reshape(-1)
+        # (glibc's and the device's cbrt are each within 1 ulp, neither is
+        # correctly rounded, so ties to the last bit are not expected)
+        assert np.max(np.abs(got - ref)) < 1e-12
+    with pytest.raises(s.InvalidArgument):
+        s.convert_image_to_lab(s.NDImage((2, 2), 1, np.zeros(4)))

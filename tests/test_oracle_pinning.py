@@ -117,3 +117,21 @@ def test_oracle_sweep_known_answers(oracle_lib):
             mk[y * 6 + x] = 0
     out, _, nxt = o.sweep((6, 2), lab, mk, 4, 10)
     assert nxt == 11 and all(out[y * 6 + x] == 10 for y in range(2) for x in range(3, 6))
+
+
+def test_oracle_lab_pinned_and_known_answers(oracle_lib, reference_lib):
+    """sRGB -> CIE-Lab (color.hpp:21-66): the C restatement equals the
+    unmodified reference bitwise (integral and fractional inputs) and meets
+    the reference suite's anchors (test_color.cpp:11-83)."""
+    rng = np.random.default_rng(7)
+    xi = rng.integers(0, 256, size=(2000, 3)).astype(np.float64)
+    xf = rng.uniform(0.0, 255.0, size=(2000, 3))
+    for x in (xi, xf):
+        assert np.array_equal(oracle_lib.srgb_to_lab(x), reference_lib.convert_to_lab((2000,), x))
+    white, black, red = oracle_lib.srgb_to_lab(
+        np.array([[255.0, 255, 255], [0, 0, 0], [255, 0, 0]])).reshape(3, 3)
+    assert abs(white[0] - 100.0) < 0.01 and abs(white[1]) < 0.01 and abs(white[2]) < 0.01
+    assert abs(black[0]) < 1e-12 and black[1] == 0.0 and black[2] == 0.0
+    assert np.allclose(red, [53.24, 80.09, 67.20], atol=0.01)
+    grays = oracle_lib.srgb_to_lab(np.repeat(np.arange(256.0), 3)).reshape(256, 3)
+    assert np.all(np.abs(grays[:, 1:]) < 0.01) and np.all(np.diff(grays[:, 0]) > 0)
