@@ -98,6 +98,12 @@ int sslic_perturb_centers(const sslic_image* img, double* centers, int64_t k, in
  * root is the device's (Lab within ~1e-13 of the reference). */
 int sslic_convert_image_to_lab(const sslic_image* img, int device, double* lab_out);
 
+/* mask_label_contour (io.hpp:432-454): copy of the image (fp64, npix*c into
+ * out, host) with every voxel that has a face neighbour of a different label
+ * zeroed in all channels. SSLIC_EINVAL if the label dims differ. */
+int sslic_mask_label_contour(const sslic_image* img, int label_rank, const int64_t* label_dims,
+                             const uint32_t* labels, int device, double* out);
+
 /* gradient_magnitude_sq (color.hpp:71-102) at n coordinates (host, n*rank). */
 int sslic_gradient_sq(const sslic_image* img, const int64_t* coords, int64_t n, int device,
                       double* out);

@@ -154,5 +154,17 @@ inline NDImage convert_image_to_lab(const NDImage& img, int device = 0) {
   return out;
 }
 
+/// mask_label_contour (io.hpp:432-454) on a B200 (fp64 image out, same
+/// shape); std::invalid_argument when the label dims differ.
+inline NDImage mask_label_contour(const NDImage& img, const LabelMap& labels, int device = 0) {
+  detail::NativeImage nimg = detail::narrow(img);
+  const Shape& ld = labels.dims();
+  std::vector<std::int64_t> dims(ld.begin(), ld.end());
+  NDImage out = img;
+  detail::check(sslic_mask_label_contour(&nimg.desc, (int)dims.size(), dims.data(),
+                                         labels.data().data(), device, out.data().data()));
+  return out;
+}
+
 }  // namespace b200
 }  // namespace sslic

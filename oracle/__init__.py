@@ -74,6 +74,7 @@ class Oracle:
                                      C.c_int, C.c_double, _u32p, _f64p, _f64p,
                                      C.POINTER(C.c_int)]
         lib.orc_srgb_to_lab.argtypes = [C.c_int64, _f64p, _f64p]
+        lib.orc_mask_label_contour.argtypes = [C.c_int, _i64p, C.c_int, _f64p, _u32p, _f64p]
         lib.orc_size_threshold.restype = C.c_int64
         lib.orc_size_threshold.argtypes = [C.c_int, _i64p]
         lib.orc_finalize.argtypes = [C.c_int, _i64p, _u32p, _f64p, C.c_int, C.c_int64, _i64p,
@@ -188,6 +189,15 @@ class Oracle:
         if st == -1:
             raise RuntimeError("pixel with undefined label")
         return lab, cen.reshape(k, -1), res[: done.value]
+
+    def mask_label_contour(self, dims, channels, img, labels):
+        dims = _dims(dims)
+        d = np.ascontiguousarray(img, dtype=np.float64).reshape(-1)
+        lab = np.ascontiguousarray(labels, dtype=np.uint32).reshape(-1)
+        out = np.empty_like(d)
+        self.lib.orc_mask_label_contour(len(dims), _p(dims, _i64p), channels, _p(d, _f64p),
+                                        _p(lab, _u32p), _p(out, _f64p))
+        return out
 
     def srgb_to_lab(self, rgb):
         """orc_srgb_to_lab: interleaved RGB (n*3) -> Lab (n*3)."""

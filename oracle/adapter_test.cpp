@@ -61,6 +61,32 @@ int main() {
     } catch (const std::invalid_argument&) {
     }
   }
+  // mask_label_contour (io.hpp is not buildable here: no libpng), checked
+  // against a direct restatement of its rule on a SLIC label map
+  {
+    sslic::NDImage img = oracle::random_image(rng, 2, 24, 3);
+    sslic::SlicParams params;
+    params.grid = oracle::random_grid(rng, img.dims());
+    const sslic::SlicResult r = sslic::run_slic(img, params, 2);
+    const sslic::NDImage m = sslic::b200::mask_label_contour(img, r.labels);
+    const sslic::Shape& d = img.dims();
+    bool ok = true;
+    for (std::int64_t y = 0; y < d[1]; ++y)
+      for (std::int64_t x = 0; x < d[0]; ++x) {
+        const std::int64_t o = x + y * d[0];
+        const std::uint32_t l = r.labels[o];
+        const bool b = (x > 0 && r.labels[o - 1] != l) || (x + 1 < d[0] && r.labels[o + 1] != l) ||
+                       (y > 0 && r.labels[o - d[0]] != l) ||
+                       (y + 1 < d[1] && r.labels[o + d[0]] != l);
+        for (int c = 0; c < 3; ++c)
+          ok = ok && m.data()[3 * o + c] == (b ? 0.0 : img.data()[3 * o + c]);
+      }
+    if (!ok) {
+      std::printf("mask_label_contour differs\n");
+      ++failures;
+    }
+    ++cases;
+  }
   // exceptions keep the reference's classes
   try {
     sslic::SlicParams bad;

@@ -297,6 +297,29 @@ int orc_run_slic(int rank, const int64_t* dims, int channels, const double* data
 /* Connectivity                                                            */
 /* ---------------------------------------------------------------------- */
 
+/* io.hpp:432-454: boundary = any face neighbour (either side, every axis)
+ * with a different label. */
+void orc_mask_label_contour(int rank, const int64_t* dims, int channels, const double* img,
+                            const uint32_t* labels, double* out) {
+  int64_t n = 1, stride[4];
+  for (int a = 0; a < rank; ++a) {
+    stride[a] = n;
+    n *= dims[a];
+  }
+  for (int64_t off = 0; off < n; ++off) {
+    int boundary = 0;
+    int64_t rem = off;
+    for (int a = 0; a < rank; ++a) {
+      const int64_t c = rem % dims[a];
+      rem /= dims[a];
+      if (c > 0 && labels[off - stride[a]] != labels[off]) boundary = 1;
+      if (c + 1 < dims[a] && labels[off + stride[a]] != labels[off]) boundary = 1;
+    }
+    for (int ch = 0; ch < channels; ++ch)
+      out[off * channels + ch] = boundary ? 0.0 : img[off * channels + ch];
+  }
+}
+
 /* color.hpp:21-24: IEC 61966-2-1 transfer function on [0, 1]. */
 static double orc_linearize(double u) {
   return u <= 0.04045 ? u / 12.92 : pow((u + 0.055) / 1.055, 2.4);

@@ -78,6 +78,11 @@ int orc_run_slic(int rank, const int64_t* dims, int channels, const double* data
 /* size_threshold (connectivity.hpp:34-38) */
 int64_t orc_size_threshold(int rank, const int64_t* grid);
 
+/* mask_label_contour (io.hpp:432-454): pixels with a face neighbour of a
+ * different label are zeroed in every channel, the rest copied. */
+void orc_mask_label_contour(int rank, const int64_t* dims, int channels, const double* img,
+                            const uint32_t* labels, double* out);
+
 /* srgb_to_cielab (color.hpp:21-52) for n interleaved RGB pixels in [0, 255]. */
 void orc_srgb_to_lab(int64_t n, const double* rgb, double* lab);
 

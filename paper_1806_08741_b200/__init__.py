@@ -96,6 +96,7 @@ def lib():
         "sslic_perturb_centers": (C.c_int, [ip, f64p, C.c_int64, C.c_int]),
         "sslic_gradient_sq": (C.c_int, [ip, i64p, C.c_int64, C.c_int, f64p]),
         "sslic_convert_image_to_lab": (C.c_int, [ip, C.c_int, f64p]),
+        "sslic_mask_label_contour": (C.c_int, [ip, C.c_int, i64p, u32p, C.c_int, f64p]),
         "sslic_squared_distance": (C.c_int, [C.c_int, C.c_int, i64p, C.c_double, C.c_int64,
                                              f64p, f64p, i64p, C.c_int, f64p]),
         "sslic_assign_pass": (C.c_int, [ip, pp, f64p, C.c_int64, C.c_int, u32p, f64p]),
@@ -363,6 +364,21 @@ def convert_image_to_lab(img: NDImage, device: int = 0) -> NDImage:
     out = np.empty(img.pixel_count() * 3, np.float64)
     _check(lib().sslic_convert_image_to_lab(C.byref(img._desc()), device, _p(out, C.c_double)))
     return NDImage(img.dims, 3, out)
+
+
+def mask_label_contour(img: NDImage, labels: np.ndarray, label_dims=None,
+                       device: int = 0) -> NDImage:
+    """mask_label_contour (io.hpp:432-454): fp64 copy of the image with every
+    voxel on a label boundary (a face neighbour with a different label) zeroed
+    in all channels. Raises InvalidArgument when the label dims differ."""
+    ld = np.asarray(img.dims if label_dims is None else label_dims, np.int64)
+    lab = np.ascontiguousarray(labels, np.uint32).reshape(-1)
+    if lab.size != int(np.prod(ld)):
+        raise InvalidArgument("mask_label_contour: label map size does not match its dims")
+    out = np.empty(img.pixel_count() * img.channels, np.float64)
+    _check(lib().sslic_mask_label_contour(C.byref(img._desc()), len(ld), _p(ld, C.c_int64),
+                                          _p(lab, C.c_uint32), device, _p(out, C.c_double)))
+    return NDImage(img.dims, img.channels, out)
 
 
 def gradient_magnitude_sq(img: NDImage, coord, device: int = 0):

@@ -417,6 +417,39 @@ int sslic_convert_image_to_lab(const sslic_image* img, int device, double* lab_o
   });
 }
 
+int sslic_mask_label_contour(const sslic_image* img, int label_rank, const int64_t* label_dims,
+                             const uint32_t* labels, int device, double* out) {
+  return guarded([&] {
+    validate_image(img);
+    bool same = label_rank == img->rank && label_dims != nullptr;
+    for (int a = 0; same && a < img->rank; ++a) same = label_dims[a] == img->dims[a];
+    if (!same) throw Error(SSLIC_EINVAL, "mask_label_contour: image and label dims differ");
+    Stream st(device);
+    auto dimg = upload_image(img, st);
+    const int64_t n = pixel_count(*img);
+    sslic_b200::Geom g{};
+    g.rank = img->rank;
+    g.channels = img->channels;
+    g.dtype = img->dtype;
+    int64_t acc = 1;
+    for (int a = 0; a < kMaxRank; ++a) {
+      g.dims[a] = a < img->rank ? img->dims[a] : 1;
+      g.strides[a] = acc;
+      acc *= g.dims[a];
+    }
+    DeviceBuf dl(n * sizeof(uint32_t), st.s), dout(n * img->channels * sizeof(double), st.s);
+    SSLIC_CUDA_CHECK(cudaMemcpyAsync(dl.p, labels, n * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                                     st.s));
+    sslic_b200::mask_label_contour_device(g, dimg->p, dl.as<uint32_t>(),
+                                          dout.as<double>(), st.s);
+    SSLIC_CUDA_CHECK(cudaGetLastError());
+    SSLIC_CUDA_CHECK(cudaMemcpyAsync(out, dout.p, n * img->channels * sizeof(double),
+                                     cudaMemcpyDeviceToHost, st.s));
+    st.sync();
+    return SSLIC_OK;
+  });
+}
+
 int sslic_gradient_sq(const sslic_image* img, const int64_t* coords, int64_t n, int device,
                       double* out) {
   return guarded([&] {

@@ -53,7 +53,36 @@ __global__ void k_srgb_to_lab(const void* img, int dtype, int64_t npix, const do
   }
 }
 
+// one thread per voxel; coordinates decoded once, neighbours by stride
+__global__ void k_mask_label_contour(Geom g, const void* img, const uint32_t* labels,
+                                     double* out, int64_t n) {
+  for (int64_t off = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; off < n;
+       off += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t l = labels[off];
+    bool boundary = false;
+    int64_t rem = off;
+    for (int a = 0; a < g.rank; ++a) {
+      const int64_t c = rem % g.dims[a];
+      rem /= g.dims[a];
+      if (c > 0 && labels[off - g.strides[a]] != l) boundary = true;
+      if (c + 1 < g.dims[a] && labels[off + g.strides[a]] != l) boundary = true;
+    }
+    for (int ch = 0; ch < g.channels; ++ch)
+      out[off * g.channels + ch] = boundary ? 0.0 : load_value(img, g.dtype, off * g.channels + ch);
+  }
+}
+
 }  // namespace
+
+void mask_label_contour_device(const Geom& g, const void* img, const uint32_t* labels,
+                               double* out, cudaStream_t s) {
+  int64_t n = 1;
+  for (int a = 0; a < g.rank; ++a) n *= g.dims[a];
+  if (n <= 0) return;
+  const int64_t blocks = (n + 255) / 256;
+  k_mask_label_contour<<<(unsigned)(blocks < 148 * 16 ? blocks : 148 * 16), 256, 0, s>>>(
+      g, img, labels, out, n);
+}
 
 void srgb_to_lab_device(const void* img, int dtype, int64_t npix, const double* table,
                         double* out, cudaStream_t s) {

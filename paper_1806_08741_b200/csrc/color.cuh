@@ -19,4 +19,10 @@ void srgb_linear_table(double* table256);
 void srgb_to_lab_device(const void* img, int dtype, int64_t npix, const double* table,
                         double* out, cudaStream_t s);
 
+// mask_label_contour (io.hpp:432-454) on the GPU: out (fp64, c per voxel)
+// = 0 where any face neighbour has a different label, else the image value.
+// Integer label comparisons and exact value copies: bitwise the reference.
+void mask_label_contour_device(const Geom& g, const void* img, const uint32_t* labels,
+                               double* out, cudaStream_t s);
+
 }  // namespace sslic_b200

@@ -240,3 +240,21 @@ def test_convert_image_to_lab_matches_reference(sslic, reference_lib):
         assert np.max(np.abs(got - ref)) < 1e-12
     with pytest.raises(s.InvalidArgument):
         s.convert_image_to_lab(s.NDImage((2, 2), 1, np.zeros(4)))
+
+
+def test_mask_label_contour_matches_oracle(sslic, oracle_lib):
+    """GPU label-contour mask (io.hpp:432-454): bitwise equal to the oracle on
+    random 2-D/3-D label maps and native dtypes; label dims must match."""
+    s = sslic
+    rng = np.random.default_rng(13)
+    for dims, ch, dt in (((40, 30), 3, np.uint8), ((17, 9, 11), 1, np.uint16),
+                         ((12, 10, 6), 4, np.float32)):
+        n = int(np.prod(dims))
+        x = (rng.integers(0, 200, size=n * ch) if dt != np.float32
+             else rng.uniform(0, 1, size=n * ch)).astype(dt)
+        lab = rng.integers(0, 3, size=n).astype(np.uint32)
+        ours = s.mask_label_contour(s.NDImage(dims, ch, x), lab)
+        ref = oracle_lib.mask_label_contour(dims, ch, x.astype(np.float64), lab)
+        assert np.array_equal(np.asarray(ours.data, np.float64), ref)
+    with pytest.raises(s.InvalidArgument):
+        s.mask_label_contour(s.NDImage((2, 2), 1, np.zeros(4)), np.zeros(6, np.uint32), (3, 2))

@@ -135,3 +135,24 @@ def test_oracle_lab_pinned_and_known_answers(oracle_lib, reference_lib):
     assert np.allclose(red, [53.24, 80.09, 67.20], atol=0.01)
     grays = oracle_lib.srgb_to_lab(np.repeat(np.arange(256.0), 3)).reshape(256, 3)
     assert np.all(np.abs(grays[:, 1:]) < 0.01) and np.all(np.diff(grays[:, 0]) > 0)
+
+
+def test_oracle_mask_label_contour_known_answers(oracle_lib):
+    """mask_label_contour (io.hpp:432-454), the reference suite's cases
+    (test_io.cpp:212-262) restated: uniform labels copy through, a 2x1 split
+    blacks both pixels, a checkerboard blacks everything, a half split blacks
+    exactly the two boundary columns in every channel."""
+    rng = np.random.default_rng(5)
+    img = rng.integers(0, 256, size=4 * 4 * 3).astype(np.float64)
+    assert np.array_equal(oracle_lib.mask_label_contour((4, 4), 3, img, np.full(16, 2)), img)
+    assert list(oracle_lib.mask_label_contour((2, 1), 1, [5.0, 6.0], [0, 1])) == [0.0, 0.0]
+    x, y = np.meshgrid(np.arange(4), np.arange(4), indexing="xy")
+    cb = ((x + y) % 2).reshape(-1)
+    assert np.all(oracle_lib.mask_label_contour((4, 4), 1, np.full(16, 200.0), cb) == 0.0)
+    img = rng.integers(0, 256, size=8 * 8 * 3).astype(np.float64)
+    x, y = np.meshgrid(np.arange(8), np.arange(8), indexing="xy")
+    lab = (x >= 4).astype(np.uint32).reshape(-1)
+    out = oracle_lib.mask_label_contour((8, 8), 3, img, lab).reshape(64, 3)
+    boundary = ((x == 3) | (x == 4)).reshape(-1)
+    assert np.all(out[boundary] == 0.0)
+    assert np.array_equal(out[~boundary], img.reshape(64, 3)[~boundary])
