@@ -623,6 +623,16 @@ class Engine:
         p, n = self.partials()
         return _torch_view(p, n, "<i8", self.device)
 
+    def labels_tensor(self):
+        """This slab's labels (plain LabelMap values, int32 bit patterns of
+        the uint32 labels) in a new device tensor (sharded.gather_labels)."""
+        import torch
+        plane = int(np.prod(self.dims[:-1]))
+        t = torch.empty((self.slab[1] - self.slab[0]) * plane, dtype=torch.int32,
+                        device=f"cuda:{self.device}")
+        self.labels_to(t.data_ptr())
+        return t
+
     def set_exact(self, exact: bool = True):
         _check(lib().sslic_engine_set_exact(self.h, int(exact)))
 

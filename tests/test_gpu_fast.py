@@ -84,3 +84,29 @@ def test_fast_path_is_used(sslic):
     fast.assign()
     evals_late, _ = fast.eval_stats()
     assert evals_late > 0
+
+
+def test_engine_labels_tensor_and_gather_single_rank(sslic):
+    """Engine.labels_tensor and ShardedLoop.segment on one rank: the gathered
+    map is the engine's label map and connectivity over it equals
+    enforce_connectivity on the same labels."""
+    import torch
+    from paper_1806_08741_b200.sharded import ShardedLoop
+    s = sslic
+    cfg, dims, ch, dtype, grid, m, iters = CASES[3]
+    img, eng, _ = _engines(s, cfg, dims, ch, dtype, grid, m, iters, torch)
+    loop = ShardedLoop(eng, lambda t: None, 1)
+    loop.init()
+    for _ in range(iters):
+        loop.iterate()
+    plane = int(np.prod(dims[:-1]))
+    gather = lambda out, t: out[0].copy_(t)  # world size 1
+    full = loop.gather_labels(gather, dims[-1], plane).cpu().numpy().view(np.uint32)
+    ref = torch.empty(int(np.prod(dims)), dtype=torch.int32, device="cuda")
+    eng.labels_to(ref.data_ptr())
+    assert np.array_equal(full, ref.cpu().numpy().view(np.uint32))
+    p = s.SlicParams(grid=list(grid), weight_m=m, max_iterations=iters)
+    table = s.ClusterTable(ch, len(dims), eng.centers())
+    cc = loop.segment(gather, lambda f: s.enforce_connectivity(
+        f.cpu().numpy().view(np.uint32), dims, table, p), dims[-1], plane)
+    assert np.array_equal(cc, s.enforce_connectivity(full, dims, table, p))

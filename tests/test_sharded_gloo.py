@@ -77,6 +77,11 @@ class OracleSlabEngine:
     def partials_tensor(self):
         return self.partials
 
+    def labels_tensor(self):
+        plane = self.plane
+        return self.torch.from_numpy(
+            self.labels[self.slab[0] * plane: self.slab[1] * plane].astype(np.int64))
+
     def update(self):
         part = self.partials.numpy().reshape(self.k, self.stride + 1)
         sums = part[:, : self.stride].astype(np.float64)
@@ -109,15 +114,24 @@ def _worker(rank, world, port, q):
         for _ in range(iters):
             loop.iterate()
         plane = int(np.prod(dims[:-1]))
+        # connectivity over the gathered slabs (every rank gets the same map)
+        full = loop.gather_labels(dist.all_gather, dims[-1], plane, align=grid[-1])
+        cc = loop.segment(dist.all_gather,
+                          lambda f: o.enforce_connectivity(dims, f.numpy().astype(np.uint32),
+                                                           eng.centers.numpy().reshape(eng.k, -1),
+                                                           ch, grid),
+                          dims[-1], plane, align=grid[-1])
         mine = eng.labels[slab[0] * plane: slab[1] * plane].copy()
         parts = [None] * world
-        dist.all_gather_object(parts, (slab, mine, eng.centers.numpy().copy()))
+        dist.all_gather_object(parts, (slab, mine, eng.centers.numpy().copy(), cc))
         if rank == 0:
             labels = np.concatenate([p[1] for p in sorted(parts, key=lambda p: p[0][0])])
             ref_l, ref_c, _ = o.run_slic(data, dims, ch, grid, m, max_iterations=iters)
-            ok_l = np.array_equal(labels, ref_l)
+            ok_l = np.array_equal(labels, ref_l) and np.array_equal(full.numpy(), ref_l)
             ok_c = all(np.array_equal(p[2], ref_c.reshape(-1)) for p in parts)
-            q.put((ok_l, ok_c, [p[0] for p in parts]))
+            ref_cc = o.enforce_connectivity(dims, ref_l, ref_c, ch, grid)
+            ok_cc = all(np.array_equal(p[3], ref_cc) for p in parts)
+            q.put((ok_l and ok_cc, ok_c, [p[0] for p in parts]))
     finally:
         dist.destroy_process_group()
 
