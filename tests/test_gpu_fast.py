@@ -110,3 +110,40 @@ def test_engine_labels_tensor_and_gather_single_rank(sslic):
     cc = loop.segment(gather, lambda f: s.enforce_connectivity(
         f.cpu().numpy().view(np.uint32), dims, table, p), dims[-1], plane)
     assert np.array_equal(cc, s.enforce_connectivity(full, dims, table, p))
+
+
+def test_run_slic_overlapped_download_matches(sslic):
+    """sslic_run_slic into a pinned host label map of >= 2^24 voxels overlaps
+    the label download with the last iterations (snapshot + changed-voxel
+    patch written through the mapped pointer); the map and centres must equal
+    the same call into pageable memory (plain download) bit for bit."""
+    import ctypes as C
+    import torch
+    s = sslic
+    cfg, dims, ch, dtype, grid, m, iters = (3, (256, 256, 256), 1, np.uint16, (16, 16, 16), 10.0, 8)
+    n = int(np.prod(dims))
+    dev = torch.empty(n * ch, dtype=torch.int16, device="cuda")
+    s.synth_generate(cfg, dims, dtype, ch, 77, 0, dims[-1], dev.data_ptr())
+    torch.cuda.synchronize()
+    host = dev.cpu().numpy().view(np.uint16)
+    L = s.lib()
+    img = s.NDImage(dims, ch, host)
+    p = s.SlicParams(grid=list(grid), weight_m=m, max_iterations=iters)
+    k = s.cluster_count(dims, grid)
+
+    def call(labels_ptr):
+        cen = np.empty(k * (ch + len(dims)))
+        res = np.empty(iters)
+        done = C.c_int()
+        s._check(L.sslic_run_slic(C.byref(img._desc()), C.byref(p._c()), 0,
+                                  C.cast(C.c_void_p(labels_ptr), C.POINTER(C.c_uint32)),
+                                  cen.ctypes.data_as(C.POINTER(C.c_double)),
+                                  res.ctypes.data_as(C.POINTER(C.c_double)), C.byref(done)))
+        return cen, res
+
+    pinned = torch.empty(n, dtype=torch.int32, pin_memory=True)
+    c1, r1 = call(pinned.data_ptr())
+    pageable = np.empty(n, np.uint32)
+    c2, r2 = call(pageable.ctypes.data)
+    assert np.array_equal(pinned.numpy().view(np.uint32), pageable)
+    assert np.array_equal(c1, c2) and np.array_equal(r1, r2)
