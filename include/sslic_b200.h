@@ -35,6 +35,12 @@ extern "C" {
 #define SSLIC_ERANGE (-3) /* std::out_of_range (image.hpp:112-124) */
 #define SSLIC_ECUDA (-4)
 #define SSLIC_ENOMEM (-5)
+/* io_error (io.hpp:40-56) by io_errc */
+#define SSLIC_EIO_NOT_FOUND (-10) /* file_not_found */
+#define SSLIC_EIO_HEADER (-11)    /* malformed_header */
+#define SSLIC_EIO_SIZE (-12)      /* size_mismatch */
+#define SSLIC_EIO_TYPE (-13)      /* unsupported_type */
+#define SSLIC_EIO_WRITE (-14)     /* write_failed */
 
 #define SSLIC_UNDEFINED 0xffffffffu /* LabelMap::kUndefined (image.hpp:291) */
 
@@ -204,6 +210,32 @@ int sslic_engine_eval_stats(sslic_engine* e, double* evals, double* window_evals
 int sslic_synth_generate(int config, int rank, const int64_t* dims, int channels, int dtype,
                          uint64_t seed, int64_t z_begin, int64_t z_end, void* dev_out,
                          void* stream);
+
+/* ---- detached-header raw volumes (io.hpp:57-202, 337-428) ----------------
+ * Types uint8 / uint16 / float32 for images, uint32 for label maps; little
+ * endian. PNG paths fail with SSLIC_EIO_TYPE (this build has no libpng). */
+typedef struct {
+  int rank;
+  int64_t dims[4];
+  int channels;
+  int dtype;      /* sslic_dtype of an image volume; -1 for a label map */
+  int label_map;  /* type uint32 */
+} sslic_volume_info;
+
+/* parse_volume_header (io.hpp:123-190). */
+int sslic_volume_info_read(const char* header_path, sslic_volume_info* out);
+/* read_volume (io.hpp:337-360) without the fp64 widening: planes
+ * [plane_begin, plane_end) of the last axis, native dtype, into dst — host
+ * memory when device < 0, else device memory on that device, streamed from
+ * disk through pinned staging (a z-slab rank reads only its planes). */
+int sslic_volume_read(const char* header_path, int64_t plane_begin, int64_t plane_end, void* dst,
+                      int device);
+/* write_volume (io.hpp:362-392) in the image's own dtype (u8/u16/f32; host). */
+int sslic_volume_write(const char* header_path, const sslic_image* img);
+/* write_labels / read_labels (io.hpp:396-428): uint32 label maps (host). */
+int sslic_labels_write(const char* header_path, int rank, const int64_t* dims,
+                       const uint32_t* labels);
+int sslic_labels_read(const char* header_path, uint32_t* labels_out);
 
 #ifdef __cplusplus
 }

@@ -20,6 +20,8 @@
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <algorithm>
+#include <cmath>
 #include <vector>
 
 #include "sslic_b200.h"
@@ -164,6 +166,57 @@ inline NDImage mask_label_contour(const NDImage& img, const LabelMap& labels, in
   detail::check(sslic_mask_label_contour(&nimg.desc, (int)dims.size(), dims.data(),
                                          labels.data().data(), device, out.data().data()));
   return out;
+}
+
+/// read_volume (io.hpp:337-360) for the detached-header format (no PNG):
+/// values widened to fp64 exactly as the reference does.
+inline NDImage read_volume(const std::string& path) {
+  sslic_volume_info info{};
+  detail::check(sslic_volume_info_read(path.c_str(), &info));
+  if (info.label_map)
+    throw std::runtime_error("uint32 volumes are label maps; use read_labels");
+  Shape dims;
+  std::int64_t n = info.channels;
+  for (int a = 0; a < info.rank; ++a) {
+    dims.push_back(info.dims[a]);
+    n *= info.dims[a];
+  }
+  const int es = info.dtype == SSLIC_U8 ? 1 : info.dtype == SSLIC_U16 ? 2 : 4;
+  std::vector<unsigned char> raw(static_cast<std::size_t>(n * es));
+  detail::check(sslic_volume_read(path.c_str(), 0, info.dims[info.rank - 1], raw.data(), -1));
+  std::vector<double> v(static_cast<std::size_t>(n));
+  for (std::int64_t i = 0; i < n; ++i) {
+    if (info.dtype == SSLIC_U8) v[i] = raw[i];
+    else if (info.dtype == SSLIC_U16) v[i] = reinterpret_cast<const std::uint16_t*>(raw.data())[i];
+    else v[i] = reinterpret_cast<const float*>(raw.data())[i];
+  }
+  return NDImage(dims, info.channels, std::move(v));
+}
+
+/// write_volume (io.hpp:362-392): "uint8" (rounded, clamped) or "float32".
+inline void write_volume(const std::string& path, const NDImage& img,
+                         const std::string& type = "float32") {
+  const std::int64_t n = img.pixel_count() * img.channels();
+  std::vector<unsigned char> raw;
+  sslic_image d{};
+  d.rank = img.rank();
+  for (int a = 0; a < 4; ++a) d.dims[a] = a < img.rank() ? img.dims()[a] : 1;
+  d.channels = img.channels();
+  if (type == "uint8") {
+    raw.resize(static_cast<std::size_t>(n));
+    for (std::int64_t i = 0; i < n; ++i)
+      raw[i] = static_cast<unsigned char>(std::clamp(std::llround(img.data()[i]), 0ll, 255ll));
+    d.dtype = SSLIC_U8;
+  } else if (type == "float32") {
+    raw.resize(static_cast<std::size_t>(n) * 4);
+    float* f = reinterpret_cast<float*>(raw.data());
+    for (std::int64_t i = 0; i < n; ++i) f[i] = static_cast<float>(img.data()[i]);
+    d.dtype = SSLIC_F32;
+  } else {
+    detail::check(SSLIC_EIO_TYPE);
+  }
+  d.data = raw.data();
+  detail::check(sslic_volume_write(path.c_str(), &d));
 }
 
 }  // namespace b200

@@ -57,6 +57,23 @@ class CudaError(RuntimeError):
     """CUDA failure or no usable device (there is no CPU fallback)."""
 
 
+class IoError(OSError):
+    """io_error (io.hpp:40-56); ``code`` is the io_errc name."""
+
+    def __init__(self, code: str, msg: str):
+        super().__init__(msg)
+        self.code = code
+
+
+_IO_CODES = {-10: "file_not_found", -11: "malformed_header", -12: "size_mismatch",
+             -13: "unsupported_type", -14: "write_failed"}
+
+
+class _VolumeInfo(C.Structure):
+    _fields_ = [("rank", C.c_int), ("dims", C.c_int64 * 4), ("channels", C.c_int),
+                ("dtype", C.c_int), ("label_map", C.c_int)]
+
+
 class _Image(C.Structure):
     _fields_ = [("rank", C.c_int), ("dims", C.c_int64 * 4), ("channels", C.c_int),
                 ("dtype", C.c_int), ("data", C.c_void_p)]
@@ -97,6 +114,11 @@ def lib():
         "sslic_gradient_sq": (C.c_int, [ip, i64p, C.c_int64, C.c_int, f64p]),
         "sslic_convert_image_to_lab": (C.c_int, [ip, C.c_int, f64p]),
         "sslic_mask_label_contour": (C.c_int, [ip, C.c_int, i64p, u32p, C.c_int, f64p]),
+        "sslic_volume_info_read": (C.c_int, [C.c_char_p, C.POINTER(_VolumeInfo)]),
+        "sslic_volume_read": (C.c_int, [C.c_char_p, C.c_int64, C.c_int64, vp, C.c_int]),
+        "sslic_volume_write": (C.c_int, [C.c_char_p, ip]),
+        "sslic_labels_write": (C.c_int, [C.c_char_p, C.c_int, i64p, u32p]),
+        "sslic_labels_read": (C.c_int, [C.c_char_p, u32p]),
         "sslic_squared_distance": (C.c_int, [C.c_int, C.c_int, i64p, C.c_double, C.c_int64,
                                              f64p, f64p, i64p, C.c_int, f64p]),
         "sslic_assign_pass": (C.c_int, [ip, pp, f64p, C.c_int64, C.c_int, u32p, f64p]),
@@ -151,6 +173,8 @@ def _check(status: int) -> None:
         raise OutOfRange(msg)
     if status == -5:
         raise MemoryError(msg)
+    if status in _IO_CODES:
+        raise IoError(_IO_CODES[status], msg)
     raise CudaError(f"status {status}: {msg}")
 
 
@@ -379,6 +403,62 @@ def mask_label_contour(img: NDImage, labels: np.ndarray, label_dims=None,
     _check(lib().sslic_mask_label_contour(C.byref(img._desc()), len(ld), _p(ld, C.c_int64),
                                           _p(lab, C.c_uint32), device, _p(out, C.c_double)))
     return NDImage(img.dims, img.channels, out)
+
+
+_NP_OF_DT = {0: np.uint8, 1: np.uint16, 2: np.float32}
+
+
+def read_volume_info(path) -> dict:
+    """parse_volume_header (io.hpp:123-190) of a detached-header volume."""
+    info = _VolumeInfo()
+    _check(lib().sslic_volume_info_read(os.fsencode(path), C.byref(info)))
+    return {"dims": tuple(int(info.dims[a]) for a in range(info.rank)),
+            "channels": int(info.channels), "label_map": bool(info.label_map),
+            "dtype": None if info.label_map else _NP_OF_DT[info.dtype]}
+
+
+def read_volume(path) -> NDImage:
+    """read_volume (io.hpp:337-360) for the detached-header format, keeping
+    the stored type (uint8 / uint16 / float32) instead of widening to fp64
+    (the values are the same). uint32 files are label maps: IoError."""
+    info = read_volume_info(path)
+    if info["label_map"]:
+        raise IoError("unsupported_type", "uint32 volumes are label maps; use read_labels")
+    out = np.empty(int(np.prod(info["dims"])) * info["channels"], info["dtype"])
+    _check(lib().sslic_volume_read(os.fsencode(path), 0, info["dims"][-1],
+                                   C.c_void_p(out.ctypes.data), -1))
+    return NDImage(info["dims"], info["channels"], out)
+
+
+def read_volume_planes(path, plane_begin: int, plane_end: int, dst_ptr: int,
+                       device: int = 0) -> None:
+    """Planes [plane_begin, plane_end) of the last axis straight into device
+    memory (a z-slab rank's share), streamed through pinned staging."""
+    _check(lib().sslic_volume_read(os.fsencode(path), int(plane_begin), int(plane_end),
+                                   C.c_void_p(dst_ptr), int(device)))
+
+
+def write_volume(path, img: NDImage) -> None:
+    """write_volume (io.hpp:362-392) in the image's stored type."""
+    _check(lib().sslic_volume_write(os.fsencode(path), C.byref(img._desc())))
+
+
+def write_labels(path, labels: np.ndarray, dims) -> None:
+    """write_labels (io.hpp:396-412)."""
+    d = np.asarray(dims, np.int64)
+    lab = np.ascontiguousarray(labels, np.uint32).reshape(-1)
+    if lab.size != int(np.prod(d)):
+        raise InvalidArgument("write_labels: label count does not match dims")
+    _check(lib().sslic_labels_write(os.fsencode(path), len(d), _p(d, C.c_int64),
+                                    _p(lab, C.c_uint32)))
+
+
+def read_labels(path):
+    """read_labels (io.hpp:414-428): (flat uint32 labels, dims)."""
+    info = read_volume_info(path)
+    out = np.empty(int(np.prod(info["dims"])), np.uint32)
+    _check(lib().sslic_labels_read(os.fsencode(path), _p(out, C.c_uint32)))
+    return out, info["dims"]
 
 
 def gradient_magnitude_sq(img: NDImage, coord, device: int = 0):

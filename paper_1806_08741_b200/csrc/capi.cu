@@ -12,34 +12,21 @@
 #include <string>
 #include <vector>
 
+#include "capi_internal.cuh"
 #include "color.cuh"
 #include "connectivity.cuh"
 #include "engine.cuh"
 
 using namespace sslic_b200;
 
+namespace sslic_b200 {
+std::string& last_error() {
+  thread_local std::string msg;
+  return msg;
+}
+}  // namespace sslic_b200
+
 namespace {
-
-thread_local std::string g_last_error;
-
-int fail(int status, const std::string& msg) {
-  g_last_error = msg;
-  return status;
-}
-
-template <class F>
-int guarded(F&& f) {
-  try {
-    g_last_error.clear();
-    return f();
-  } catch (const Error& e) {
-    return fail(e.status, e.what());
-  } catch (const std::bad_alloc&) {
-    return fail(SSLIC_ENOMEM, "host allocation failed");
-  } catch (const std::exception& e) {
-    return fail(SSLIC_EINVAL, e.what());
-  }
-}
 
 size_t dtype_size(int dt) {
   switch (dt) {
@@ -325,7 +312,7 @@ struct sslic_engine {
 
 extern "C" {
 
-const char* sslic_last_error(void) { return g_last_error.c_str(); }
+const char* sslic_last_error(void) { return sslic_b200::last_error().c_str(); }
 const char* sslic_version(void) { return "sslic_b200 0.1 (sm_100a)"; }
 
 int64_t sslic_cluster_count(int rank, const int64_t* dims, const int64_t* grid) {
