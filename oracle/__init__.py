@@ -273,6 +273,14 @@ class Reference:
         lib.ref_random_grid.argtypes = [C.c_void_p, C.c_int, _i64p, _i64p]
         lib.ref_random_weight.restype = C.c_double
         lib.ref_random_weight.argtypes = [C.c_void_p]
+        lib.ref_scaling_report.restype = C.c_int
+        lib.ref_scaling_report.argtypes = [C.c_int, C.POINTER(C.c_int), _f64p, C.POINTER(C.c_int),
+                                           C.POINTER(C.c_double), _f64p, _f64p, C.c_char_p,
+                                           C.c_int64, C.c_char_p, C.c_int64]
+        lib.ref_amdahl_bound.restype = C.c_double
+        lib.ref_amdahl_bound.argtypes = [C.c_double, C.c_int]
+        lib.ref_amdahl_efficiency_bound.restype = C.c_double
+        lib.ref_amdahl_efficiency_bound.argtypes = [C.c_double, C.c_int]
         lib.ref_convert_to_lab.restype = C.c_int
         lib.ref_convert_to_lab.argtypes = [C.c_int, _i64p, _f64p, _f64p]
         lib.ref_time_iterations.restype = C.c_int
@@ -340,6 +348,23 @@ class Reference:
         if st != 0:
             raise RuntimeError(f"reference connectivity failed with status {st}")
         return out
+
+    def scaling_report(self, workers, times, conn):
+        """bench.hpp make_report + emit_scaling_csv/markdown of the reference."""
+        n = len(workers)
+        w = np.asarray(workers, np.int32)
+        t = np.asarray(times, np.float64)
+        c = np.asarray(conn, np.int32)
+        alpha = C.c_double()
+        sp, ef = np.empty(n), np.empty(n)
+        csv = C.create_string_buffer(1 << 16)
+        md = C.create_string_buffer(1 << 16)
+        st = self.lib.ref_scaling_report(n, w.ctypes.data_as(C.POINTER(C.c_int)), _p(t, _f64p),
+                                         c.ctypes.data_as(C.POINTER(C.c_int)), C.byref(alpha),
+                                         _p(sp, _f64p), _p(ef, _f64p), csv, 1 << 16, md, 1 << 16)
+        if st != 0:
+            raise ValueError(f"reference scaling report failed with status {st}")
+        return alpha.value, sp, ef, csv.value.decode(), md.value.decode()
 
     def convert_to_lab(self, dims, rgb):
         """convert_image_to_lab (color.hpp:54-66) of the unmodified reference."""

@@ -13,6 +13,8 @@
 #include <stdexcept>
 #include <vector>
 
+#include "sslic/bench.hpp"
+#include "sslic/color.hpp"
 #include "sslic/connectivity.hpp"
 #include "sslic/parallel.hpp"
 #include "sslic/slic.hpp"
@@ -136,6 +138,33 @@ int ref_enforce_connectivity(int rank, const int64_t* dims, const uint32_t* labe
     return status_of(std::current_exception());
   }
 }
+
+// Scaling-report analysis (bench.hpp:41-262) on caller-given records: the
+// fitted alpha and the CSV / markdown texts (written into buf, NUL-ended).
+int ref_scaling_report(int n, const int* workers, const double* times, const int* conn,
+                       double* alpha_out, double* speedups_out, double* eff_out, char* csv,
+                       int64_t csv_cap, char* md, int64_t md_cap) {
+  try {
+    std::vector<TimingRecord> recs;
+    for (int i = 0; i < n; ++i) recs.push_back(TimingRecord{workers[i], times[i], conn[i] != 0});
+    const ScalingReport r = detail::make_report(recs);
+    *alpha_out = r.alpha;
+    for (int i = 0; i < n; ++i) {
+      speedups_out[i] = r.speedups[i];
+      eff_out[i] = r.efficiencies[i];
+    }
+    const std::string c = emit_scaling_csv(r), m = emit_scaling_markdown(r);
+    if ((int64_t)c.size() >= csv_cap || (int64_t)m.size() >= md_cap) return -9;
+    std::memcpy(csv, c.c_str(), c.size() + 1);
+    std::memcpy(md, m.c_str(), m.size() + 1);
+    return 0;
+  } catch (...) {
+    return status_of(std::current_exception());
+  }
+}
+
+double ref_amdahl_bound(double alpha, int p) { return amdahl_bound(alpha, p); }
+double ref_amdahl_efficiency_bound(double alpha, int p) { return amdahl_efficiency_bound(alpha, p); }
 
 // convert_image_to_lab (color.hpp:54-66) on an interleaved 3-channel image.
 int ref_convert_to_lab(int rank, const int64_t* dims, const double* rgb, double* lab_out) {
