@@ -107,7 +107,15 @@ Engine::Engine(const sslic_image& img, const sslic_params& p, int device, int64_
     // absolute fp32 margin for the hi/lo centre split (DESIGN.md error bound)
     const double e = vmax_ * std::ldexp(1.0, -48);
     const double M = fast_margin(g_.channels);
-    abs_margin_ = (float)(8.0 * e * e / M + e * e + 1e-37);
+    double am = 8.0 * e * e / M + e * e + 1e-37;
+    if (g_.dtype == SSLIC_F64) {
+      // rounding of the f32 working copy (kernels_fast_main.cuh, fast margin)
+      const double ep = vmax_ * std::ldexp(1.0, -24);
+      const double eps0 = (g_.channels + 14) * std::ldexp(1.0, -24);
+      am += g_.channels * (1.0 / eps0 + 1.0) * ep * ep;
+      pix_err_ = ep;
+    }
+    abs_margin_ = (float)am;
     // key scale 2^-k: the largest possible fp32 distance of a covered
     // candidate, C (2 vmax + 1)^2 + m^2 rank 4, must map below 2^-67
     // (kernels_fast.cuh "Keys"). Exact power-of-two scaling.
@@ -121,6 +129,15 @@ Engine::Engine(const sslic_image& img, const sslic_params& p, int device, int64_
                                                                     : AssignPath::kExact;
   if (path_ == AssignPath::kFast)
     region_cand_ = dalloc<int>((size_t)fast_region_count(g_) * kRegionCandStride, s);
+  if (path_ == AssignPath::kFast && g_.dtype == SSLIC_F64) {
+    // f32 working copy of an fp64 image for the fast sweep (round to nearest;
+    // the rounding is in the fast margins)
+    const int64_t nvals = (g_.data_end - g_.data_begin) * g_.plane * g_.channels;
+    img32_ = dalloc<float>((size_t)nvals, s);
+    k_f64_to_f32<<<blocks_for(nvals, 256), 256, 0, s>>>(static_cast<const double*>(img_), img32_,
+                                                        nvals);
+    launch_check("f64 working copy");
+  }
 }
 
 Engine::~Engine() {
@@ -128,7 +145,7 @@ Engine::~Engine() {
   cudaStream_t s = stream_;
   void* ptrs[] = {centers_, labels_, dists_, acc_, anchors_, cell_of_, cell_count_,
                   cell_start_, cursor_, items_, scan_tmp_, block_partials_, residuals_,
-                  counters_, hist32_, chg_, sums_, region_cand_, update_done_};
+                  counters_, hist32_, chg_, sums_, region_cand_, update_done_, img32_};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, s);
   cudaStreamSynchronize(s);
@@ -246,7 +263,9 @@ void Engine::launch_assign_kernel(bool accumulate) {
   if (path_ == AssignPath::kFast && accumulate && !dist_mode_) {
     FastParams P{};
     P.g = g_;
-    P.img = img_;
+    P.img = img32_ ? static_cast<const void*>(img32_) : img_;
+    P.img_exact = img_;
+    P.pix_err = (float)(pix_err_ * key_scale_);
     P.centers = current_centers();
     P.history = hist;
     P.hist32 = hist32_;

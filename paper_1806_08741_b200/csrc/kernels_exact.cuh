@@ -586,6 +586,11 @@ static __global__ void k_residual_final(const double* block_partials, int nblock
   if (threadIdx.x == 0) *residual_out = sqrt(red[0]);
 }
 
+static __global__ void k_f64_to_f32(const double* in, float* out, int64_t n) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = __double2float_rn(in[i]);
+}
+
 static __global__ void k_fill_f64(double* p, int64_t n, double v) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) p[i] = v;

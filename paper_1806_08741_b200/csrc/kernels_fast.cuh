@@ -40,7 +40,9 @@ constexpr float kInf = __builtin_huge_valf();
 
 struct FastParams {
   Geom g;
-  const void* img;
+  const void* img;        // the sweep's image: native u8/u16/f32, or an f32 copy of f64 data
+  const void* img_exact;  // the caller's image in g.dtype (fp64 re-decisions, f64 deltas)
+  float pix_err;          // f64 inputs: bound of |v - fl32(v)| (scaled); 0 otherwise
   const double* centers;  // current table (fp64)
   const double* history;  // all tables, history[t * k * stride]
   const float2* hist32;   // hi/lo fp32 split of every table
@@ -165,7 +167,7 @@ static __device__ __noinline__ uint32_t exact_region_voxel(const FastParams& P, 
   const Geom& g = P.g;
   const int64_t coord[kMaxRank] = {x, y, z, 0};
   double pix[4];
-  for (int c = 0; c < g.channels; ++c) pix[c] = load_value(P.img, g.dtype, di + c);
+  for (int c = 0; c < g.channels; ++c) pix[c] = load_value(P.img_exact, g.dtype, di + c);
   double best_d = kInf;
   uint32_t best_k = kUndefined;
   if (full) {
@@ -220,7 +222,7 @@ __device__ __noinline__ void crowded_region(const FastParams& P, const int64_t* 
       uint32_t word = P.labels[li];
       old = P.codec.label(word);
       double pix[4];
-      for (int c = 0; c < C; ++c) pix[c] = load_value(P.img, g.dtype, di + c);
+      for (int c = 0; c < C; ++c) pix[c] = load_value(P.img_exact, g.dtype, di + c);
       double best_d = kInf;
       uint32_t best_k = kUndefined;
       int64_t clo[3], chi[3], cc[3];
@@ -270,8 +272,8 @@ __device__ __noinline__ void crowded_region(const FastParams& P, const int64_t* 
     }
     count_undefined(valid && lab == kUndefined, P.counters);
     const bool changed = valid && lab != old;
-    warp_accumulate(g, P.shift, lab, changed, +1, P.img, di, coord, P.acc);
-    warp_accumulate(g, P.shift, old, changed, -1, P.img, di, coord, P.acc);
+    warp_accumulate(g, P.shift, lab, changed, +1, P.img_exact, di, coord, P.acc);
+    warp_accumulate(g, P.shift, old, changed, -1, P.img_exact, di, coord, P.acc);
   }
 }
 

@@ -3,6 +3,8 @@
 // DESIGN.md "K2").
 #pragma once
 
+#include <type_traits>
+
 #include "kernels_fast.cuh"
 
 namespace sslic_b200 {
@@ -75,8 +77,13 @@ __device__ __forceinline__ void load_run(const T* src, bool vec, const bool* val
   }
 }
 
-template <int RANK, int C, typename T, int RXc, int RYc, int RZc>
+// T is the caller's storage type; T = double sweeps an f32 working copy (TW)
+// with the pixel rounding folded into the margins, and takes the exact f64
+// values for the re-decisions and the fixed-point deltas.
+template <int RANK, int C, typename TS, int RXc, int RYc, int RZc>
 __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_constant__ FastParams P) {
+  constexpr bool kF64 = std::is_same<TS, double>::value;
+  using T = typename std::conditional<kF64, float, TS>::type;  // working pixel type
   using Box = BoxShape<RANK>;
   constexpr int kStride = C + RANK;
   constexpr int kComp = kStride + 1;
@@ -134,6 +141,10 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
   const int64_t reg_off = org[0] + org[1] * g.strides[1] + (RANK == 3 ? org[2] * g.strides[2] : 0);
   uint32_t* const lab_r = P.labels + (reg_off - g.slab_begin * g.plane);
   const T* const img_r = static_cast<const T*>(P.img) + (reg_off - g.data_begin * g.plane) * C;
+  // f64 inputs: the caller's values, for the exact fixed-point deltas
+  const double* const imgx_r =
+      kF64 ? static_cast<const double*>(P.img_exact) + (reg_off - g.data_begin * g.plane) * C
+           : nullptr;
   const int s1 = (int)g.strides[1], s2 = RANK == 3 ? (int)g.strides[2] : 0;
   const int lane_rel = 4 * xq + yq * s1 + zq * s2;
   // [warp][v][lane][kS2]: each lane's entry is contiguous (16-byte cp.async)
@@ -420,6 +431,10 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
       }
       pmin[c] = __uint_as_float(lo) * ks;
       pmax[c] = __uint_as_float(hv) * ks;
+      if constexpr (kF64) {  // the true values lie within pix_err of the f32 copy
+        pmin[c] -= P.pix_err;
+        pmax[c] += P.pix_err;
+      }
     }
 
     // candidates covering this box and their lower bound over the box
@@ -706,8 +721,9 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
         unsigned long long* a = S >= 0 ? accs + S * kComp : P.acc + (uint64_t)L * kComp;
 #pragma unroll
         for (int c = 0; c < C; ++c) {
-          const long long val =
-              sizeof(T) < 4 ? (long long)pv[c] : (long long)__float2ll_rn(pv[c] * fscale);
+          long long val;
+          if constexpr (kF64) val = to_fixed(imgx_r[(rel + v) * C + c], P.shift);
+          else val = sizeof(T) < 4 ? (long long)pv[c] : (long long)__float2ll_rn(pv[c] * fscale);
           atomicAdd(a + c, (unsigned long long)(sgn * val));
         }
 #pragma unroll
@@ -751,7 +767,8 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
           szr += sgn * lz;
 #pragma unroll
           for (int c = 0; c < C; ++c) {
-            if (sizeof(T) < 4) sv32[c] += sgn * (int)p[v][c];
+            if constexpr (kF64) sv64[c] += sgn * to_fixed(imgx_r[(rel + v) * C + c], P.shift);
+            else if (sizeof(T) < 4) sv32[c] += sgn * (int)p[v][c];
             else sv64[c] += sgn * __float2ll_rn(p[v][c] * fscale);  // exact: |v| 2^s < 2^40
           }
         }
@@ -839,8 +856,10 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
 #pragma unroll
               for (int c = 0; c < C; ++c) {
                 const T raw = qpx[c];
-                const long long val = sizeof(T) < 4 ? (long long)raw
-                                                    : (long long)__float2ll_rn((float)raw * fscale);
+                long long val;
+                if constexpr (kF64) val = to_fixed(imgx_r[(int64_t)qrel * C + c], P.shift);
+                else val = sizeof(T) < 4 ? (long long)raw
+                                         : (long long)__float2ll_rn((float)raw * fscale);
                 atomicAdd(a + c, (unsigned long long)(sgn * val));
               }
 #pragma unroll
@@ -1009,7 +1028,10 @@ static __global__ void k_split32(const double* c, float2* out, int64_t k, int st
 inline bool fast_path_supported(const Geom& g) {
   if (g.rank != 2 && g.rank != 3) return false;
   if (g.channels < 1 || g.channels > 4) return false;
-  if (g.dtype != SSLIC_U8 && g.dtype != SSLIC_U16 && g.dtype != SSLIC_F32) return false;
+  // (f64 images sweep an f32 working copy, see k_assign_fast)
+  if (g.dtype != SSLIC_U8 && g.dtype != SSLIC_U16 && g.dtype != SSLIC_F32 &&
+      g.dtype != SSLIC_F64)
+    return false;
   for (int a = 0; a < g.rank; ++a)
     if (g.grid[a] > kFastMaxR) return false;
   if (g.k >= (int64_t)1 << 30) return false;
@@ -1034,7 +1056,8 @@ inline size_t fast_smem_bytes(const Geom& g, const int* R) {
   b += (size_t)kFastMaxCand * (g.stride + 1) * sizeof(unsigned long long);
   b += (size_t)warps * 4 * hist32_stride(g.stride) * 32 * sizeof(float2);
   b += (size_t)warps * 2 * 32 * 16;  // next-box label words
-  b += (size_t)warps * 2 * 32 * 4 * pf_pix_words(g.channels, dtype_size(g.dtype));
+  const int wsize = g.dtype == SSLIC_F64 ? 4 : dtype_size(g.dtype);  // working pixel size
+  b += (size_t)warps * 2 * 32 * 4 * pf_pix_words(g.channels, wsize);
   return b;
 }
 
@@ -1085,6 +1108,7 @@ void launch_fast_c(const FastParams& P, size_t smem, int64_t nb, cudaStream_t s)
   switch (P.g.dtype) {
     case SSLIC_U8: launch_fast_t<RANK, C, uint8_t>(P, smem, nb, s); break;
     case SSLIC_U16: launch_fast_t<RANK, C, uint16_t>(P, smem, nb, s); break;
+    case SSLIC_F64: launch_fast_t<RANK, C, double>(P, smem, nb, s); break;
     default: launch_fast_t<RANK, C, float>(P, smem, nb, s); break;
   }
 }
@@ -1125,7 +1149,11 @@ inline void launch_fast_assign(FastParams P, cudaStream_t s) {
     P.reg_z0 = 0;
     P.nreg[2] = 1;
   }
-  P.margin = fast_margin(g.channels);
+  // f64 inputs: the f32 working copy rounds each value by e <= |v| 2^-24. By
+  // 2|d|e <= eps0 d^2 + e^2/eps0 (eps0 = (C+14) u, the per-distance bound)
+  // each fp32 distance is then within 2 eps0 D + A + C (1/eps0 + 1) e^2, so
+  // the relative margin doubles (the engine adds the absolute part)
+  P.margin = fast_margin(g.channels) * (g.dtype == SSLIC_F64 ? 2.0f : 1.0f);
   // vector loads of 4-voxel runs need 4 | dims[0], 4 | RX and 16-byte bases
   P.aligned4 = (g.dims[0] % 4 == 0 && P.R[0] % 4 == 0 &&
                 reinterpret_cast<uintptr_t>(P.img) % 16 == 0 &&

@@ -147,3 +147,51 @@ def test_run_slic_overlapped_download_matches(sslic):
     c2, r2 = call(pageable.ctypes.data)
     assert np.array_equal(pinned.numpy().view(np.uint32), pageable)
     assert np.array_equal(c1, c2) and np.array_equal(r1, r2)
+
+
+@pytest.mark.parametrize("case", [
+    ((96, 80, 64), 4, (8, 8, 8), 20.0, 5, 4),    # config-4-like, values in [0, 1)
+    ((512, 384), 3, (16, 16), 10.0, 6, 2),       # Lab-like: L in [0, 100], a/b signed
+], ids=["3d-c4", "2d-lab"])
+def test_fast_f64_equals_exact(sslic, case):
+    """fp64 images (e.g. the Lab output of convert_image_to_lab, or any
+    reference NDImage that is not f32-representable) take the fast kernel
+    over an f32 working copy with the rounding folded into the margins; the
+    result must equal the exact fp64 kernel bit for bit at every iteration."""
+    import torch
+    s = sslic
+    dims, ch, grid, m, iters, cfg = case
+    n = int(np.prod(dims))
+    base = torch.empty(n * ch, dtype=torch.float32, device="cuda")
+    s.synth_generate(cfg, dims, np.float32, ch, 4321, 0, dims[-1] if len(dims) == 3 else 1,
+                     base.data_ptr())
+    rng = np.random.default_rng(3)
+    x = base.cpu().numpy().astype(np.float64)
+    if cfg == 2:  # Lab-like ranges and signs
+        x = x.reshape(-1, 3) * np.array([100.0, 160.0, 160.0]) - np.array([0.0, 80.0, 80.0])
+        x = x.reshape(-1)
+    x = x + rng.uniform(-1e-7, 1e-7, x.size)  # not representable in f32
+    dev = torch.from_numpy(x).cuda()
+    p = s.SlicParams(grid=list(grid), weight_m=m, max_iterations=iters)
+    fast = s.Engine(dims, ch, np.float64, dev.data_ptr(), p)
+    exact = s.Engine(dims, ch, np.float64, dev.data_ptr(), p)
+    exact.set_exact(True)
+    la = torch.empty(n, dtype=torch.int32, device="cuda")
+    lb = torch.empty(n, dtype=torch.int32, device="cuda")
+    for e in (fast, exact):
+        e.init()
+        e.commit()
+    fast.set_stats(True)
+    for it in range(iters):
+        fast.assign()
+        exact.assign()
+        amb, crowded, _ = fast.fast_stats()
+        fast.update()
+        exact.update()
+        fast.labels_to(la.data_ptr())
+        exact.labels_to(lb.data_ptr())
+        torch.cuda.synchronize()
+        assert int((la != lb).sum().item()) == 0, f"iteration {it} (fp64 re-decided {amb})"
+        assert np.array_equal(fast.centers(), exact.centers()), f"iteration {it}: centres"
+    evals, _ = fast.eval_stats()
+    assert evals > 0  # the fast kernel ran
