@@ -192,38 +192,44 @@ uint32_t sweep_host(const Geom& g, uint32_t* labels, uint8_t* markers, int64_t n
       comp.push_back(v);
       mk[off] |= 2;
     }
+    // explicit face neighbours (predictable control flow, no inner axis loops)
+    auto visit = [&](const Vox& v, int64_t adj, int a, int32_t c) {
+      const uint32_t la = labels[adj];
+      const uint8_t m = mk[adj];
+      if (la == label) {
+        if (!(m & 2)) {
+          mk[adj] = m | 2;
+          Vox w = v;
+          w.off = adj;
+          w.c[a] = c;
+          comp.push_back(w);
+        }
+      } else if (m & 1) {
+        if (adj < off) {
+          if (adj > best_before) {
+            best_before = adj;
+            label_before = la;
+          }
+        } else if (best_after < 0 || adj < best_after) {
+          best_after = adj;
+          label_after = la;
+        }
+      } else if (best_pending < 0 || adj < best_pending) {
+        best_pending = adj;
+        label_pending = la;
+      }
+    };
     for (size_t head = 0; head < comp.size(); ++head) {
       const Vox v = comp[head];
-      for (int a = 0; a < rank; ++a) {
-        for (int dir = -1; dir <= 1; dir += 2) {
-          const int64_t c = v.c[a] + dir;
-          if (c < 0 || c >= dim[a]) continue;
-          const int64_t adj = v.off + dir * str[a];
-          const uint32_t la = labels[adj];
-          const uint8_t m = mk[adj];
-          if (la == label) {
-            if (!(m & 2)) {
-              mk[adj] = m | 2;
-              Vox w = v;
-              w.off = adj;
-              w.c[a] = (int32_t)c;
-              comp.push_back(w);
-            }
-          } else if (m & 1) {
-            if (adj < off) {
-              if (adj > best_before) {
-                best_before = adj;
-                label_before = la;
-              }
-            } else if (best_after < 0 || adj < best_after) {
-              best_after = adj;
-              label_after = la;
-            }
-          } else if (best_pending < 0 || adj < best_pending) {
-            best_pending = adj;
-            label_pending = la;
-          }
-        }
+      if (v.c[0] > 0) visit(v, v.off - 1, 0, v.c[0] - 1);
+      if (v.c[0] + 1 < dim[0]) visit(v, v.off + 1, 0, v.c[0] + 1);
+      if (rank > 1) {
+        if (v.c[1] > 0) visit(v, v.off - str[1], 1, v.c[1] - 1);
+        if (v.c[1] + 1 < dim[1]) visit(v, v.off + str[1], 1, v.c[1] + 1);
+      }
+      if (rank > 2) {
+        if (v.c[2] > 0) visit(v, v.off - str[2], 2, v.c[2] - 1);
+        if (v.c[2] + 1 < dim[2]) visit(v, v.off + str[2], 2, v.c[2] + 1);
       }
     }
     uint32_t target;
