@@ -195,3 +195,58 @@ def test_fast_f64_equals_exact(sslic, case):
         assert np.array_equal(fast.centers(), exact.centers()), f"iteration {it}: centres"
     evals, _ = fast.eval_stats()
     assert evals > 0  # the fast kernel ran
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_slab_engines_sum_to_single_engine(sslic, world):
+    """The z-slab path on the GPU without NCCL: `world` engines in one process,
+    each owning one slab of the same device image (its data range includes
+    the perturbation halo), with the allreduces done by summing their
+    buffers. Labels (concatenated slabs), centres and residuals must equal a
+    single whole-volume engine bit for bit — the multi-GPU determinism
+    contract, with the real slab-bounded kernels."""
+    import torch
+    from paper_1806_08741_b200.sharded import all_slabs, data_bounds
+    s = sslic
+    cfg, dims, ch, dtype, grid, m, iters = CASES[2]  # config-3-like u16 volume
+    img, single, _ = _engines(s, cfg, dims, ch, dtype, grid, m, iters, torch)
+    plane = int(np.prod(dims[:-1]))
+    esize = np.dtype(dtype).itemsize * ch
+    p = s.SlicParams(grid=list(grid), weight_m=m, max_iterations=iters)
+    slabs = all_slabs(dims[-1], world, align=grid[-1])
+    engines = []
+    for sl in slabs:
+        dr = data_bounds(dims[-1], sl)
+        engines.append(s.Engine(dims, ch, dtype, img.data_ptr() + dr[0] * plane * esize, p,
+                                slab=sl, data_range=dr))
+
+    def allreduce(tensors):
+        total = tensors[0].clone()
+        for t in tensors[1:]:
+            total += t
+        for t in tensors:
+            t.copy_(total)
+
+    for e in engines:
+        e.init()
+    allreduce([e.centers_tensor() for e in engines])
+    for e in engines:
+        e.commit()
+    single.init()
+    single.commit()
+    for _ in range(iters):
+        for e in engines:
+            e.assign()
+        allreduce([e.partials_tensor() for e in engines])
+        for e in engines:
+            e.update()
+        single.assign()
+        single.update()
+    torch.cuda.synchronize()
+    full = torch.cat([e.labels_tensor() for e in engines]).cpu().numpy().view(np.uint32)
+    ref = torch.empty(int(np.prod(dims)), dtype=torch.int32, device="cuda")
+    single.labels_to(ref.data_ptr())
+    assert np.array_equal(full, ref.cpu().numpy().view(np.uint32))
+    for e in engines:
+        assert np.array_equal(e.centers(), single.centers())
+        np.testing.assert_array_equal(e.residuals(), single.residuals())
