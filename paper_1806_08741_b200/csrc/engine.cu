@@ -3,6 +3,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "engine.cuh"
@@ -129,6 +130,9 @@ Engine::Engine(const sslic_image& img, const sslic_params& p, int device, int64_
                                                                     : AssignPath::kExact;
   if (path_ == AssignPath::kFast)
     region_cand_ = dalloc<int>((size_t)fast_region_count(g_) * kRegionCandStride, s);
+  // test hook: SSLIC_FAST_MAX_CAND lowers the candidate capacity of a region
+  // (more regions take the exact crowded fallback)
+  if (const char* mc = std::getenv("SSLIC_FAST_MAX_CAND")) max_cand_ = std::atoi(mc);
   if (path_ == AssignPath::kFast && g_.dtype == SSLIC_F64) {
     // f32 working copy of an fp64 image for the fast sweep (round to nearest;
     // the rounding is in the fast margins)
@@ -286,6 +290,7 @@ void Engine::launch_assign_kernel(bool accumulate) {
     P.key_scale2 = key_scale_ * key_scale_;
     P.abs_margin = abs_margin_ * P.key_scale2;
     P.region_cand = region_cand_;
+    P.max_cand = max_cand_;
     launch_fast_assign(P, s);
     ++launches_;  // k_region_cand + k_assign_fast
     launch_check("assign_fast");

@@ -113,6 +113,7 @@ class Engine {
   float key_scale_ = 1.f;       // fast path: 2^-k operand scaling of the fp32 keys
   bool fast_ok_scale_ = true;
   unsigned* update_done_ = nullptr;  // last-block counter of k_update_fused
+  int max_cand_ = 0;                  // 0: kFastMaxCand
   float* img32_ = nullptr;            // fast path over an fp64 image: f32 working copy
   double pix_err_ = 0.0;              // bound of its rounding (|v| 2^-24)
   bool acc_zero_ = false;            // deltas already zero (fused update)

@@ -70,6 +70,7 @@ struct FastParams {
   const int* region_cand;   // per region: [count, ids...] (k_region_cand)
   int* region_cand_out;     // same buffer, written by k_region_cand
   int aligned4;       // dims[0] % 4 == 0: 4-voxel runs are vector-aligned
+  int max_cand;       // regions with more candidates take the exact crowded path
 };
 
 template <int RANK>

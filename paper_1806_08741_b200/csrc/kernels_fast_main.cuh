@@ -213,11 +213,12 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
   // ---- candidates of this region (precomputed by k_region_cand) ----
   const int* rc = P.region_cand + (int64_t)blockIdx.x * kRegionCandStride;
   const int total = __ldg(rc);
-  const int n = total < kFastMaxCand ? total : kFastMaxCand;
+  // (P.max_cand <= kFastMaxCand; tests lower it to exercise the fallback)
+  const int n = total < P.max_cand ? total : P.max_cand;
   for (int j = tid; j < n; j += kFastThreads) sm.id[j] = __ldg(rc + 1 + j);
   if (tid == 0) sm.n_cand = n;
   __syncthreads();
-  if (total > kFastMaxCand) {
+  if (total > P.max_cand) {
     cp_async_wait_all();
     if (tid == 0) atomicAdd(P.counters + 6, 1ull);
     crowded_region<RANK, C>(P, org, hi, zlo, zhi);
@@ -1153,6 +1154,7 @@ inline void launch_fast_assign(FastParams P, cudaStream_t s) {
   // 2|d|e <= eps0 d^2 + e^2/eps0 (eps0 = (C+14) u, the per-distance bound)
   // each fp32 distance is then within 2 eps0 D + A + C (1/eps0 + 1) e^2, so
   // the relative margin doubles (the engine adds the absolute part)
+  if (P.max_cand <= 0 || P.max_cand > kFastMaxCand) P.max_cand = kFastMaxCand;
   P.margin = fast_margin(g.channels) * (g.dtype == SSLIC_F64 ? 2.0f : 1.0f);
   // vector loads of 4-voxel runs need 4 | dims[0], 4 | RX and 16-byte bases
   P.aligned4 = (g.dims[0] % 4 == 0 && P.R[0] % 4 == 0 &&

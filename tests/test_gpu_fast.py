@@ -250,3 +250,36 @@ def test_slab_engines_sum_to_single_engine(sslic, world):
     for e in engines:
         assert np.array_equal(e.centers(), single.centers())
         np.testing.assert_array_equal(e.residuals(), single.residuals())
+
+
+def test_crowded_regions_fallback_equals_exact(sslic, monkeypatch):
+    """Regions with more candidates than the kernel's capacity take the
+    exact per-voxel fallback inside the fast kernel; with the capacity
+    lowered (test hook) most regions are crowded, and the results must still
+    equal the exact kernel bit for bit."""
+    import torch
+    monkeypatch.setenv("SSLIC_FAST_MAX_CAND", "12")
+    s = sslic
+    cfg, dims, ch, dtype, grid, m, iters = CASES[2]
+    img, fast, exact = _engines(s, cfg, dims, ch, dtype, grid, m, 4, torch)
+    n = int(np.prod(dims))
+    la = torch.empty(n, dtype=torch.int32, device="cuda")
+    lb = torch.empty(n, dtype=torch.int32, device="cuda")
+    for e in (fast, exact):
+        e.init()
+        e.commit()
+    fast.set_stats(True)
+    crowded_seen = 0
+    for it in range(4):
+        fast.assign()
+        exact.assign()
+        _, crowded, _ = fast.fast_stats()
+        crowded_seen += crowded
+        fast.update()
+        exact.update()
+        fast.labels_to(la.data_ptr())
+        exact.labels_to(lb.data_ptr())
+        torch.cuda.synchronize()
+        assert int((la != lb).sum().item()) == 0, f"iteration {it}"
+        assert np.array_equal(fast.centers(), exact.centers())
+    assert crowded_seen > 0
