@@ -100,10 +100,19 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
   // record: [sx | sy | sz | (c_hi, c_lo) x C | cluster id, chg], 16-byte rows
   const int RS = (HO + 2 * C + 2 + 3) & ~3;
   float* rec = reinterpret_cast<float*>(smem_raw + sizeof(FastSmem));  // [cand+1][RS]
-  unsigned long long* accs =
-      reinterpret_cast<unsigned long long*>(rec + (size_t)(kFastMaxCand + 1) * RS);
+  // CTA delta slots per candidate, 32-bit words (native shared atomics; a
+  // 64-bit shared atomic is a CAS loop): [intensity low x C | coords | count |
+  // intensity high x C]. Coordinates are region-local (|sum| < 2^25). u8/u16
+  // intensities are exact in the low word (|slot sum| <= region voxels x max
+  // value < 2^31); u16 regions of more than 32768 voxels split them into a
+  // low byte and the rest. Fixed-point float intensities are 64-bit values
+  // kept as (low word, high word) with the carry of each add.
+  constexpr bool kFloatAcc = sizeof(TS) >= 4;
+  using AccT = int;
+  constexpr int kCompA = kComp + C;
+  AccT* accs = reinterpret_cast<AccT*>(rec + (size_t)(kFastMaxCand + 1) * RS);
   // per-warp staging of the carried-over centres: [warp][v][lane][kS2] float2
-  float2* stage = reinterpret_cast<float2*>(accs + kFastMaxCand * kComp);
+  float2* stage = reinterpret_cast<float2*>(accs + kFastMaxCand * kCompA);
   // next-box prefetch: label words [warp][2][lane] (16 B), pixel runs [warp][2][lane][kPW]
   uint4* pf_words = reinterpret_cast<uint4*>(stage + kWarps * 4 * kS2 * 32);
   uint32_t* pf_pix = reinterpret_cast<uint32_t*>(pf_words + kWarps * 2 * 32);
@@ -155,6 +164,24 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
   const uint32_t lmask = P.codec.label_mask;
   const int lbits = P.codec.label_bits;
   const uint32_t tag_now_bits = P.tag_now << lbits;
+  // slot of a record offset: (roff * rs_m) >> 16 == roff / RS exactly (RS < 1024, slot <= 64)
+  const uint32_t rs_m = (65536u + (uint32_t)RS - 1u) / (uint32_t)RS;
+  const bool split16 = sizeof(TS) == 2 && RX * RY * RZ > 32768;
+  auto slot_add = [&](AccT* a, int comp, long long v) { atomicAdd(a + comp, (int)v); };
+  auto slot_add_val = [&](AccT* a, int c, long long v) {  // intensity component
+    if constexpr (kFloatAcc) {
+      const unsigned long long u = (unsigned long long)v;
+      const uint32_t l = (uint32_t)u;
+      const uint32_t before = atomicAdd(reinterpret_cast<unsigned*>(a) + c, l);
+      const uint32_t carry = before + l < before ? 1u : 0u;
+      atomicAdd(reinterpret_cast<unsigned*>(a) + kComp + c, (uint32_t)(u >> 32) + carry);
+    } else if (split16) {
+      atomicAdd(a + c, (int)(v & 255));
+      atomicAdd(a + kComp + c, (int)(v >> 8));
+    } else {
+      atomicAdd(a + c, (int)v);
+    }
+  };
 
   // The label words (and, when small, the pixels) of a warp's next box are
   // prefetched with cp.async into a per-lane double buffer while the current
@@ -254,7 +281,9 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
       for (int c = 0; c < 2 * C + 2; ++c) r[HO + c] = 0.f;
     }
   }
-  for (int i = tid; i < n * kComp; i += kFastThreads) accs[i] = 0ull;
+  // (slot block: 64 * kCompA words, a multiple of 16 bytes)
+  for (int i = tid; i < kFastMaxCand * kCompA / 4; i += kFastThreads)
+    reinterpret_cast<int4*>(accs)[i] = make_int4(0, 0, 0, 0);
   for (int i = tid; i < kSlotHash; i += kFastThreads) sm.htab[i] = 0xffff;
   // compaction lists start as valid record offsets: a voxel without any kept
   // candidate still reads a (never used) winner record
@@ -681,15 +710,14 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
       const unsigned tu = __reduce_add_sync(0xffffffffu, undef);
       if (lane == 0) atomicAdd(P.counters, (unsigned long long)tu);  // slic.hpp:330-331
     }
-    // Sparse deltas (the common case after the first iterations): each lane
-    // adds its own contributions straight into the CTA slots. Dense deltas
-    // (first iterations): warp-aggregate per label first.
+    // Per-lane deltas (the common case): each lane adds its contributions
+    // into the CTA slots, consecutive voxels of one label merged into one
+    // run (the +new slot is the winner's record, no lookup). A box dominated
+    // by one label (uniform regions) is warp-aggregated per label instead.
     const unsigned npend = __reduce_add_sync(0xffffffffu, (unsigned)__popc(pending));
-    bool sparse = npend <= kSparseDeltas;
-    if (!sparse) {
-      // Many contributions: aggregate per label when the box is dominated by
-      // few labels (uniform regions), else per-lane atomics (noisy label
-      // maps: aggregation would take one warp round per distinct label).
+    if (npend != 0) {  // uniform: most boxes have no change after the first iterations
+    bool per_lane = npend <= kSparseDeltas;
+    if (!per_lane) {
       const int fb = pending ? __ffs(pending) - 1 : 0;
       uint32_t first = fb < 4 ? newl[0] : oldl[0];
 #pragma unroll
@@ -698,40 +726,83 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
       const unsigned anyp = __ballot_sync(0xffffffffu, pending != 0);
       const uint32_t l0 = __shfl_sync(0xffffffffu, first, __ffs(anyp) - 1);
       const unsigned same = __ballot_sync(0xffffffffu, pending != 0 && first == l0);
-      sparse = 4 * __popc(same) < 3 * __popc(anyp);
+      per_lane = 4 * __popc(same) < 3 * __popc(anyp);
     }
-    if (sparse) {
-      while (pending) {
-        const int q = __ffs(pending) - 1;
-        pending &= pending - 1;
-        const int v = q & 3;
-        const long long sgn = q < 4 ? 1 : -1;
-        uint32_t L = q < 4 ? newl[0] : oldl[0];
-        float pv[C];
+    if (per_lane) {
+      // one flush site in a rolled loop (compact code: this runs rarely
+      // after the first iterations)
+      bool open = false;
+      int run_sg = 0, run_s = -1, rx = 0, ry = 0, rz = 0, rc = 0;
+      uint32_t run_l = 0;
+      long long rv[C];
 #pragma unroll
-        for (int c = 0; c < C; ++c) pv[c] = p[0][c];
+      for (int c = 0; c < C; ++c) rv[c] = 0;
+#pragma unroll 1
+      for (;;) {
+        const bool have = pending != 0;
+        int q = 0, v = 0, sg = 0;
+        uint32_t L = 0;
+        if (have) {
+          q = __ffs(pending) - 1;
+          v = q & 3;
+          sg = q >> 2;
+          L = sg ? oldl[0] : newl[0];
 #pragma unroll
-        for (int u = 1; u < 4; ++u)
-          if (v == u) {
-            L = q < 4 ? newl[u] : oldl[u];
+          for (int u = 1; u < 4; ++u)
+            if (v == u) L = sg ? oldl[u] : newl[u];
+        }
+        if (open && (!have || sg != run_sg || L != run_l)) {
+          const long long sgn = run_sg ? -1 : 1;
+          if (run_s >= 0) {
+            AccT* a = accs + run_s * kCompA;
 #pragma unroll
-            for (int c = 0; c < C; ++c) pv[c] = p[u][c];
+            for (int c = 0; c < C; ++c) slot_add_val(a, c, sgn * rv[c]);
+            slot_add(a, C, sgn * rx);
+            slot_add(a, C + 1, sgn * ry);
+            if (RANK == 3) slot_add(a, C + 2, sgn * rz);
+            slot_add(a, kStride, sgn * rc);
+          } else {  // label outside the region's candidates: global, absolute coordinates
+            unsigned long long* a = P.acc + (uint64_t)run_l * kComp;
+#pragma unroll
+            for (int c = 0; c < C; ++c) atomicAdd(a + c, (unsigned long long)(sgn * rv[c]));
+            atomicAdd(a + C, (unsigned long long)(sgn * (rx + rc * org[0])));
+            atomicAdd(a + C + 1, (unsigned long long)(sgn * (ry + rc * org[1])));
+            if (RANK == 3) atomicAdd(a + C + 2, (unsigned long long)(sgn * (rz + rc * org[2])));
+            atomicAdd(a + kStride, (unsigned long long)(sgn * rc));
           }
-        const int S = slot_of(sm, L);
-        const long long co[3] = {lx0 + v, ly, lz};
-        unsigned long long* a = S >= 0 ? accs + S * kComp : P.acc + (uint64_t)L * kComp;
+          open = false;
+        }
+        if (!have) break;
+        pending &= pending - 1;
+        if (!open) {
+          open = true;
+          run_sg = sg;
+          run_l = L;
+          int js = jst[0];
 #pragma unroll
-        for (int c = 0; c < C; ++c) {
-          long long val;
-          if constexpr (kF64) val = to_fixed(imgx_r[(rel + v) * C + c], P.shift);
-          else val = sizeof(T) < 4 ? (long long)pv[c] : (long long)__float2ll_rn(pv[c] * fscale);
-          atomicAdd(a + c, (unsigned long long)(sgn * val));
+          for (int u = 1; u < 4; ++u)
+            if (v == u) js = jst[u];
+          run_s = sg ? slot_of(sm, L) : (int)(((uint32_t)js * rs_m) >> 16);
+          rx = ry = rz = rc = 0;
+#pragma unroll
+          for (int c = 0; c < C; ++c) rv[c] = 0;
         }
 #pragma unroll
-        for (int ax = 0; ax < RANK; ++ax)
-          atomicAdd(a + C + ax, (unsigned long long)(sgn * (co[ax] + (S >= 0 ? 0 : org[ax]))));
-        atomicAdd(a + kStride, (unsigned long long)sgn);
+        for (int c = 0; c < C; ++c) {
+          float pv = p[0][c];
+#pragma unroll
+          for (int u = 1; u < 4; ++u)
+            if (v == u) pv = p[u][c];
+          if constexpr (kF64) rv[c] += to_fixed(imgx_r[(rel + v) * C + c], P.shift);
+          else if (sizeof(T) < 4) rv[c] += (long long)(int)pv;
+          else rv[c] += __float2ll_rn(pv * fscale);  // exact: |v| 2^s < 2^40
+        }
+        rx += lx0 + v;
+        ry += ly;
+        rz += lz;
+        ++rc;
       }
+      pending = 0;
     }
 #pragma unroll 1
     for (;;) {
@@ -802,14 +873,14 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
       if (lane == leader) {
         const int S = slot_of(sm, L);
         if (S >= 0) {
-          unsigned long long* a = accs + S * kComp;
+          AccT* a = accs + S * kCompA;
 #pragma unroll
           for (int c = 0; c < C; ++c)
-            if (tvs[c]) atomicAdd(a + c, (unsigned long long)tvs[c]);
-          if (tx) atomicAdd(a + C, (unsigned long long)(long long)tx);
-          if (ty) atomicAdd(a + C + 1, (unsigned long long)(long long)ty);
-          if (RANK == 3 && tz) atomicAdd(a + C + 2, (unsigned long long)(long long)tz);
-          if (tc) atomicAdd(a + kStride, (unsigned long long)(long long)tc);
+            if (tvs[c]) slot_add_val(a, c, tvs[c]);
+          if (tx) slot_add(a, C, tx);
+          if (ty) slot_add(a, C + 1, ty);
+          if (RANK == 3 && tz) slot_add(a, C + 2, tz);
+          if (tc) slot_add(a, kStride, tc);
         } else {
           // label outside the region's candidates: global, absolute coordinates
           unsigned long long* a = P.acc + (uint64_t)L * kComp;
@@ -823,6 +894,8 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
         }
       }
     }
+
+    }  // npend != 0
 
     // ---- deferred fp64 re-decisions of this box (one queued voxel per lane) ----
     __syncwarp();
@@ -853,21 +926,30 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
               if (L == lmask) continue;
               const long long sgn = sg == 0 ? 1 : -1;
               const int S = slot_of(sm, L);
-              unsigned long long* a = S >= 0 ? accs + S * kComp : P.acc + (uint64_t)L * kComp;
+              long long val[C];
 #pragma unroll
               for (int c = 0; c < C; ++c) {
                 const T raw = qpx[c];
-                long long val;
-                if constexpr (kF64) val = to_fixed(imgx_r[(int64_t)qrel * C + c], P.shift);
-                else val = sizeof(T) < 4 ? (long long)raw
-                                         : (long long)__float2ll_rn((float)raw * fscale);
-                atomicAdd(a + c, (unsigned long long)(sgn * val));
+                if constexpr (kF64) val[c] = to_fixed(imgx_r[(int64_t)qrel * C + c], P.shift);
+                else val[c] = sizeof(T) < 4 ? (long long)raw
+                                            : (long long)__float2ll_rn((float)raw * fscale);
               }
+              if (S >= 0) {
+                AccT* a = accs + S * kCompA;
 #pragma unroll
-              for (int ax = 0; ax < RANK; ++ax)
-                atomicAdd(a + C + ax,
-                          (unsigned long long)(sgn * (co[ax] + (S >= 0 ? 0 : org[ax]))));
-              atomicAdd(a + kStride, (unsigned long long)sgn);
+                for (int c = 0; c < C; ++c) slot_add_val(a, c, sgn * val[c]);
+#pragma unroll
+                for (int ax = 0; ax < RANK; ++ax) slot_add(a, C + ax, sgn * co[ax]);
+                slot_add(a, kStride, sgn);
+              } else {
+                unsigned long long* a = P.acc + (uint64_t)L * kComp;
+#pragma unroll
+                for (int c = 0; c < C; ++c) atomicAdd(a + c, (unsigned long long)(sgn * val[c]));
+#pragma unroll
+                for (int ax = 0; ax < RANK; ++ax)
+                  atomicAdd(a + C + ax, (unsigned long long)(sgn * (co[ax] + org[ax])));
+                atomicAdd(a + kStride, (unsigned long long)sgn);
+              }
             }
           }
         }
@@ -889,8 +971,15 @@ __global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_co
   // ---- flush CTA slots (one global atomic per non-zero component) ----
   for (int j = warp; j < n; j += kWarps) {
     if (lane < kComp) {
-      long long v = (long long)accs[j * kComp + lane];
-      if (lane >= C && lane < kStride) v += (long long)accs[j * kComp + kStride] * org[lane - C];
+      long long v = (long long)accs[j * kCompA + lane];
+      if (lane < C) {
+        const int h = accs[j * kCompA + kComp + lane];
+        if constexpr (kFloatAcc)
+          v = (long long)((unsigned long long)(uint32_t)v | (unsigned long long)(uint32_t)h << 32);
+        else
+          v += 256LL * (long long)h;
+      }
+      if (lane >= C && lane < kStride) v += (long long)accs[j * kCompA + kStride] * org[lane - C];
       if (v) atomicAdd(P.acc + (uint64_t)sm.id[j] * kComp + lane, (unsigned long long)v);
     }
   }
@@ -1054,7 +1143,8 @@ inline size_t fast_smem_bytes(const Geom& g, const int* R) {
   const int warps = kFastThreads / 32;
   size_t b = sizeof(FastSmem);
   b += (size_t)(kFastMaxCand + 1) * RS * sizeof(float);
-  b += (size_t)kFastMaxCand * (g.stride + 1) * sizeof(unsigned long long);
+  // CTA delta slots (see k_assign_fast): 32-bit words, C extra per candidate
+  b += (size_t)kFastMaxCand * (g.stride + 1 + g.channels) * sizeof(int);
   b += (size_t)warps * 4 * hist32_stride(g.stride) * 32 * sizeof(float2);
   b += (size_t)warps * 2 * 32 * 16;  // next-box label words
   const int wsize = g.dtype == SSLIC_F64 ? 4 : dtype_size(g.dtype);  // working pixel size
