@@ -9,7 +9,9 @@
 #include <cstring>
 #include <memory>
 #include <new>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "capi_internal.cuh"
@@ -204,17 +206,144 @@ __global__ void k_patch_labels_host(int64_t n, const uint32_t* before, const uin
 // iterations on a second stream; afterwards the voxels whose label changed
 // since (~0.1-1 %) are written straight into the mapped host map. Same result
 // as downloading the final map.
+// Labels that differ between the snapshot and the final map, as (index,
+// label) pairs written through a mapped pinned staging buffer (coalesced
+// 8-byte stores; PCIe handles these far better than scattered 4-byte
+// writes into the caller's map). Each block walks 4096-label tiles and
+// reserves its tile's entries with one atomic; entries past `cap` are
+// counted but not written (the caller then copies the whole map).
+__global__ void k_change_list(int64_t n, const uint32_t* before, const uint32_t* after,
+                              unsigned long long* count, int64_t cap, uint2* out) {
+  constexpr int kPer = 16;
+  __shared__ unsigned long long base;
+  __shared__ int warp_tot[8];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int64_t tile = blockIdx.x * (int64_t)(256 * kPer); tile < n;
+       tile += (int64_t)gridDim.x * 256 * kPer) {
+    uint32_t chg = 0;
+    uint32_t val[kPer];
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int64_t i = tile + j * 256 + tid;
+      val[j] = 0;
+      if (i < n) {
+        const uint32_t a = after[i];
+        val[j] = a;
+        if (a != before[i]) chg |= 1u << j;
+      }
+    }
+    const int mine = __popc(chg);
+    int incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (lane == 31) warp_tot[warp] = incl;
+    __syncthreads();
+    int before_w = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      before_w += w < warp ? warp_tot[w] : 0;
+      tot += warp_tot[w];
+    }
+    if (tid == 0) base = tot ? atomicAdd(count, (unsigned long long)tot) : 0ull;
+    __syncthreads();
+    int64_t pos = (int64_t)base + before_w + incl - mine;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j)
+      if (chg >> j & 1u) {
+        if (pos < cap) out[pos] = make_uint2((uint32_t)(tile + j * 256 + tid), val[j]);
+        ++pos;
+      }
+    __syncthreads();  // warp_tot / base reuse
+  }
+}
+
+// Page-locked, device-mapped host staging kept across calls (grown on demand).
+struct MappedStage {
+  std::mutex mu;
+  void* p = nullptr;
+  size_t bytes = 0;
+  void* get(size_t want) {
+    if (want > bytes) {
+      if (p) cudaFreeHost(p);
+      p = nullptr;
+      bytes = 0;
+      SSLIC_CUDA_CHECK(cudaHostAlloc(&p, want, cudaHostAllocMapped | cudaHostAllocPortable));
+      bytes = want;
+    }
+    return p;
+  }
+};
+MappedStage& mapped_stage() {
+  static MappedStage* s = new MappedStage();  // never destroyed (exit-order safe)
+  return *s;
+}
+
+// Apply (index, label) pairs to the host map with the host's threads.
+void apply_change_list(uint32_t* labels, const uint2* list, int64_t cnt) {
+  int t = (int)std::thread::hardware_concurrency();
+  t = t < 1 ? 1 : (t > 32 ? 32 : t);
+  if (cnt < ((int64_t)1 << 16)) t = 1;
+  std::vector<std::thread> th;
+  for (int w = 0; w < t; ++w)
+    th.emplace_back([=] {
+      const int64_t a = cnt * w / t, b = cnt * (w + 1) / t;
+      for (int64_t i = a; i < b; ++i) {
+        if (i + 32 < b) __builtin_prefetch(labels + list[i + 32].x, 1, 0);
+        labels[list[i].x] = list[i].y;
+      }
+    });
+  for (auto& x : th) x.join();
+}
+
+// SSLIC_TIMING: device-event marks on the streams (no host syncs in between)
+struct EventMarks {
+  bool on = std::getenv("SSLIC_TIMING") != nullptr;
+  std::vector<std::pair<std::string, cudaEvent_t>> ev;
+  void mark(cudaStream_t s, const std::string& what) {
+    if (!on) return;
+    cudaEvent_t e;
+    SSLIC_CUDA_CHECK(cudaEventCreate(&e));
+    SSLIC_CUDA_CHECK(cudaEventRecord(e, s));
+    ev.emplace_back(what, e);
+  }
+  ~EventMarks() {
+    if (!on || ev.empty()) return;
+    cudaEventSynchronize(ev.back().second);
+    std::string line;
+    for (size_t i = 1; i < ev.size(); ++i) {
+      float ms = 0.f;
+      cudaEventSynchronize(ev[i].second);
+      cudaEventElapsedTime(&ms, ev[0].second, ev[i].second);
+      char buf[96];
+      std::snprintf(buf, sizeof buf, " %s@%.1f", ev[i].first.c_str(), ms);
+      line += buf;
+    }
+    for (auto& p : ev) cudaEventDestroy(p.second);
+    std::fprintf(stderr, "[sslic] overlapped loop (ms from start):%s\n", line.c_str());
+  }
+};
+
 int run_loop_overlapped(Engine& e, Stream& st, uint32_t* labels_out, int64_t n) {
+  EventMarks em;
+  em.mark(st.s, "start");
   e.init(true);
   e.commit();
+  em.mark(st.s, "init");
   const int iters = e.max_iterations();
+  // snapshot early enough that its D2H copy (~n x 4 B at PCIe speed) hides
+  // behind the remaining iterations; later changes travel as a change list
   const int snap = iters - 4;
   for (int it = 0; it < snap; ++it) {
     e.assign(true);
     e.update();
+    em.mark(st.s, "it" + std::to_string(it));
   }
   DeviceBuf snapbuf(n * sizeof(uint32_t), st.s);
   e.unpack_labels(snapbuf.as<uint32_t>());
+  em.mark(st.s, "snap");
   cudaEvent_t ready;
   SSLIC_CUDA_CHECK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
   SSLIC_CUDA_CHECK(cudaEventRecord(ready, st.s));
@@ -226,17 +355,55 @@ int run_loop_overlapped(Engine& e, Stream& st, uint32_t* labels_out, int64_t n) 
   cudaEvent_t copied;
   SSLIC_CUDA_CHECK(cudaEventCreateWithFlags(&copied, cudaEventDisableTiming));
   SSLIC_CUDA_CHECK(cudaEventRecord(copied, cs));
+  em.mark(cs, "copied");
   for (int it = snap; it < iters; ++it) {
     e.assign(true);
     e.update();
+    em.mark(st.s, "it" + std::to_string(it));
   }
   DeviceBuf fin(n * sizeof(uint32_t), st.s);
   e.unpack_labels(fin.as<uint32_t>());
-  SSLIC_CUDA_CHECK(cudaStreamWaitEvent(st.s, copied, 0));  // snapshot landed first
-  k_patch_labels_host<<<148 * 8, 256, 0, st.s>>>(n, snapbuf.as<uint32_t>(),
-                                                  fin.as<uint32_t>(), labels_out);
-  SSLIC_CUDA_CHECK(cudaGetLastError());
-  st.sync();
+  em.mark(st.s, "unpack");
+  if (n < ((int64_t)1 << 32)) {
+    // change list in device memory (up to 5% of the map; more -> whole-map
+    // copy), DMA'd into pinned staging behind the snapshot, applied on the host
+    const int64_t cap = n / 20 + 1024;
+    DeviceBuf dlist((size_t)cap * sizeof(uint2), st.s);
+    DeviceBuf cntb(sizeof(unsigned long long), st.s);
+    SSLIC_CUDA_CHECK(cudaMemsetAsync(cntb.p, 0, sizeof(unsigned long long), st.s));
+    k_change_list<<<148 * 8, 256, 0, st.s>>>(n, snapbuf.as<uint32_t>(), fin.as<uint32_t>(),
+                                              cntb.as<unsigned long long>(), cap,
+                                              dlist.as<uint2>());
+    SSLIC_CUDA_CHECK(cudaGetLastError());
+    unsigned long long cnt = 0;
+    SSLIC_CUDA_CHECK(cudaMemcpyAsync(&cnt, cntb.p, sizeof(cnt), cudaMemcpyDeviceToHost, st.s));
+    em.mark(st.s, "list");
+    st.sync();
+    if ((int64_t)cnt <= cap) {
+      MappedStage& ms = mapped_stage();
+      std::lock_guard<std::mutex> lock(ms.mu);
+      uint2* list = static_cast<uint2*>(ms.get((size_t)cap * sizeof(uint2)));
+      SSLIC_CUDA_CHECK(cudaMemcpyAsync(list, dlist.p, cnt * sizeof(uint2),
+                                       cudaMemcpyDeviceToHost, cs));  // after the snapshot
+      em.mark(cs, "list-d2h");
+      SSLIC_CUDA_CHECK(cudaStreamSynchronize(cs));
+      apply_change_list(labels_out, list, (int64_t)cnt);
+    } else {
+      SSLIC_CUDA_CHECK(cudaStreamSynchronize(cs));
+      SSLIC_CUDA_CHECK(cudaMemcpyAsync(labels_out, fin.p, n * sizeof(uint32_t),
+                                       cudaMemcpyDeviceToHost, st.s));
+      st.sync();
+    }
+    if (em.on) std::fprintf(stderr, "[sslic] change list: %llu entries (%.2f%% of the map)\n",
+                            cnt, 100.0 * (double)cnt / (double)n);
+  } else {
+    SSLIC_CUDA_CHECK(cudaStreamWaitEvent(st.s, copied, 0));  // snapshot landed first
+    k_patch_labels_host<<<148 * 8, 256, 0, st.s>>>(n, snapbuf.as<uint32_t>(),
+                                                    fin.as<uint32_t>(), labels_out);
+    SSLIC_CUDA_CHECK(cudaGetLastError());
+    em.mark(st.s, "patched");
+    st.sync();
+  }
   cudaStreamDestroy(cs);
   cudaEventDestroy(ready);
   cudaEventDestroy(copied);

@@ -77,11 +77,16 @@ __device__ __forceinline__ void load_run(const T* src, bool vec, const bool* val
   }
 }
 
+// CTAs per SM the register budget targets: 5 (96 registers) where the
+// shared-memory footprint allows it (1-2 channels; measured +2% on config 3),
+// else 4 (128 registers; 5 costs config 4 7% through spills)
+__host__ __device__ constexpr int fast_min_blocks(int C) { return C <= 2 ? 5 : 4; }
+
 // T is the caller's storage type; T = double sweeps an f32 working copy (TW)
 // with the pixel rounding folded into the margins, and takes the exact f64
 // values for the re-decisions and the fixed-point deltas.
 template <int RANK, int C, typename TS, int RXc, int RYc, int RZc>
-__global__ void __launch_bounds__(kFastThreads, 4) k_assign_fast(const __grid_constant__ FastParams P) {
+__global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fast(const __grid_constant__ FastParams P) {
   constexpr bool kF64 = std::is_same<TS, double>::value;
   using T = typename std::conditional<kF64, float, TS>::type;  // working pixel type
   using Box = BoxShape<RANK>;

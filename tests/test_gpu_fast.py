@@ -112,15 +112,18 @@ def test_engine_labels_tensor_and_gather_single_rank(sslic):
     assert np.array_equal(cc, s.enforce_connectivity(full, dims, table, p))
 
 
-def test_run_slic_overlapped_download_matches(sslic):
+@pytest.mark.parametrize("iters", [8, 4], ids=["change-list", "list-overflow"])
+def test_run_slic_overlapped_download_matches(sslic, iters):
     """sslic_run_slic into a pinned host label map of >= 2^24 voxels overlaps
-    the label download with the last iterations (snapshot + changed-voxel
-    patch written through the mapped pointer); the map and centres must equal
-    the same call into pageable memory (plain download) bit for bit."""
+    the label download with the last iterations (snapshot copy, then the
+    labels changed since as an (index, label) list applied on the host, or a
+    whole-map copy when more than 5% changed: 4 iterations snapshot after
+    the first); the map and centres must equal the same call into pageable
+    memory (plain download) bit for bit."""
     import ctypes as C
     import torch
     s = sslic
-    cfg, dims, ch, dtype, grid, m, iters = (3, (256, 256, 256), 1, np.uint16, (16, 16, 16), 10.0, 8)
+    cfg, dims, ch, dtype, grid, m = (3, (256, 256, 256), 1, np.uint16, (16, 16, 16), 10.0)
     n = int(np.prod(dims))
     dev = torch.empty(n * ch, dtype=torch.int16, device="cuda")
     s.synth_generate(cfg, dims, dtype, ch, 77, 0, dims[-1], dev.data_ptr())
