@@ -127,6 +127,10 @@ __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fas
   uint32_t* pf_pix = reinterpret_cast<uint32_t*>(pf_words + kWarps * 2 * 32);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // hi/lo centre coordinates of the candidates for the spatial tables, in the
+  // history staging area (free until the sweep): [cand][3]
+  float2* const cxy = stage;
+  static_assert(kFastMaxCand * 3 <= 4 * 32 * 2, "cxy fits the staging area of one warp");
   // ---- region ----
   unsigned rb = blockIdx.x;  // 32-bit region index math
   const int rxi = (int)(rb % (unsigned)P.nreg[0]);
@@ -283,6 +287,7 @@ __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fas
         if (a < RANK) {
           const float2 cp = __ldg(c32 + C + a);
           sm.cpl[j][a] = (cp.x - (float)org[a]) + cp.y;
+          cxy[j * 3 + a] = cp;
         }
       }
     } else {
@@ -319,14 +324,13 @@ __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fas
       }
       float v = kSentinel;
       if (j < n) {
-        const int kid = sm.id[j];
         const int an = a == 0 ? sm.anc[j][0] : (a == 1 ? sm.anc[j][1] : sm.anc[j][2]);
         const int s = g.grid[a];
         const int dx = r - an;
         if (dx >= -s && dx <= s) {
           const float x = (float)((a == 0 ? org[0] : (a == 1 ? org[1] : org[2])) + r);
           // fp32 filter table from the hi/lo centre split (error in the margin)
-          const float2 cc = __ldg(P.cur32 + (int64_t)kid * kS2 + C + a);
+          const float2 cc = cxy[j * 3 + a];
           const float t = ((cc.x - x) + cc.y) * P.inv_grid[a];
           v = (float)g.m_sq * (t * t) * P.key_scale2;
         }
@@ -343,7 +347,8 @@ __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fas
   }
   // per axis and box index: the candidates whose window overlaps the box's
   // (clipped) extent on that axis; a box's covering set is the AND of three
-  for (int t = tid; t < nbx + nby + nbz; t += kFastThreads) {
+  // (one warp per (axis, box index); lanes over candidates j and j + 32)
+  for (int t = warp; t < nbx + nby + nbz; t += kWarps) {
     const int a = t < nbx ? 0 : (t < nbx + nby ? 1 : 2);
     const int i = a == 0 ? t : (a == 1 ? t - nbx : t - nbx - nby);
     int lo, hi;
@@ -357,17 +362,19 @@ __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fas
       lo = max(i * Box::Z, ez_lo);
       hi = min(i * Box::Z + Box::Z - 1, ez_hi);
     }
-    unsigned long long m = 0ull;
-    if (a < RANK) {
-      const int s = g.grid[a];
-      for (int j = 0; j < n; ++j) {
+    unsigned m2[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = lane + 32 * h;
+      bool c = a >= RANK;
+      if (a < RANK && j < n) {
+        const int s = g.grid[a];
         const int an = sm.anc[j][a];
-        if (an + s >= lo && an - s <= hi) m |= 1ull << j;
+        c = an + s >= lo && an - s <= hi;
       }
-    } else {
-      m = ~0ull;
+      m2[h] = __ballot_sync(0xffffffffu, c);
     }
-    sm.bmask[a][i] = m;
+    if (lane == 0) sm.bmask[a][i] = (unsigned long long)m2[1] << 32 | m2[0];
   }
   __syncthreads();
 
