@@ -255,10 +255,11 @@ __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fas
   const int total = __ldg(rc);
   // (P.max_cand <= kFastMaxCand; tests lower it to exercise the fallback)
   const int n = total < P.max_cand ? total : P.max_cand;
+  // (no barrier: the staging loop below reads sm.id[j] from the thread that
+  // wrote it, same j -> thread mapping)
   for (int j = tid; j < n; j += kFastThreads) sm.id[j] = __ldg(rc + 1 + j);
   if (tid == 0) sm.n_cand = n;
-  __syncthreads();
-  if (total > P.max_cand) {
+  if (total > P.max_cand) {  // uniform over the CTA
     cp_async_wait_all();
     if (tid == 0) atomicAdd(P.counters + 6, 1ull);
     crowded_region<RANK, C>(P, org, hi, zlo, zhi);
