@@ -116,6 +116,26 @@ __device__ __forceinline__ int slot_of(const FastSmem& sm, uint32_t id) {
   }
 }
 
+// x[i & 3] through predicated selects (inline PTX: a select chain written in
+// C++ is turned into an indexed local-memory array by the compiler)
+__device__ __forceinline__ uint32_t sel4(uint32_t x0, uint32_t x1, uint32_t x2, uint32_t x3,
+                                         int i) {
+  uint32_t r;
+  asm("{\n\t.reg .pred p0, p1;\n\t.reg .b32 t0, t1;\n\t"
+      "and.b32 t0, %5, 1;\n\tsetp.ne.b32 p0, t0, 0;\n\t"
+      "and.b32 t1, %5, 2;\n\tsetp.ne.b32 p1, t1, 0;\n\t"
+      "selp.b32 t0, %2, %1, p0;\n\tselp.b32 t1, %4, %3, p0;\n\t"
+      "selp.b32 %0, t1, t0, p1;\n\t}"
+      : "=r"(r)
+      : "r"(x0), "r"(x1), "r"(x2), "r"(x3), "r"(i));
+  return r;
+}
+// (a[i & 3] for the 8 delta bits: i < 4 -> a, else b)
+__device__ __forceinline__ uint32_t sel8(const uint32_t (&a)[4], const uint32_t (&b)[4], int i) {
+  const uint32_t x = sel4(a[0], a[1], a[2], a[3], i), y = sel4(b[0], b[1], b[2], b[3], i);
+  return i < 4 ? x : y;
+}
+
 // ---- fp32x2 (sm_100a paired FP32) --------------------------------------------
 typedef unsigned long long f2;
 __device__ __forceinline__ f2 pk2(float lo, float hi) {

@@ -736,10 +736,7 @@ __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fas
     bool per_lane = npend <= kSparseDeltas;
     if (!per_lane) {
       const int fb = pending ? __ffs(pending) - 1 : 0;
-      uint32_t first = fb < 4 ? newl[0] : oldl[0];
-#pragma unroll
-      for (int u = 1; u < 4; ++u)
-        if ((fb & 3) == u) first = fb < 4 ? newl[u] : oldl[u];
+      const uint32_t first = sel8(newl, oldl, fb);
       const unsigned anyp = __ballot_sync(0xffffffffu, pending != 0);
       const uint32_t l0 = __shfl_sync(0xffffffffu, first, __ffs(anyp) - 1);
       const unsigned same = __ballot_sync(0xffffffffu, pending != 0 && first == l0);
@@ -763,10 +760,7 @@ __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fas
           q = __ffs(pending) - 1;
           v = q & 3;
           sg = q >> 2;
-          L = sg ? oldl[0] : newl[0];
-#pragma unroll
-          for (int u = 1; u < 4; ++u)
-            if (v == u) L = sg ? oldl[u] : newl[u];
+          L = sel8(newl, oldl, q);
         }
         if (open && (!have || sg != run_sg || L != run_l)) {
           const long long sgn = run_sg ? -1 : 1;
@@ -795,10 +789,7 @@ __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fas
           open = true;
           run_sg = sg;
           run_l = L;
-          int js = jst[0];
-#pragma unroll
-          for (int u = 1; u < 4; ++u)
-            if (v == u) js = jst[u];
+          const int js = (int)sel4(jst[0], jst[1], jst[2], jst[3], v);
           run_s = sg ? slot_of(sm, L) : (int)(((uint32_t)js * rs_m) >> 16);
           rx = ry = rz = rc = 0;
 #pragma unroll
@@ -806,10 +797,8 @@ __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fas
         }
 #pragma unroll
         for (int c = 0; c < C; ++c) {
-          float pv = p[0][c];
-#pragma unroll
-          for (int u = 1; u < 4; ++u)
-            if (v == u) pv = p[u][c];
+          const float pv = __uint_as_float(sel4(__float_as_uint(p[0][c]), __float_as_uint(p[1][c]),
+                                                __float_as_uint(p[2][c]), __float_as_uint(p[3][c]), v));
           if constexpr (kF64) rv[c] += to_fixed(imgx_r[(rel + v) * C + c], P.shift);
           else if (sizeof(T) < 4) rv[c] += (long long)(int)pv;
           else rv[c] += __float2ll_rn(pv * fscale);  // exact: |v| 2^s < 2^40
@@ -898,10 +887,7 @@ __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fas
       uint32_t mylab = 0;
       if (pending) {
         const int bit = __ffs(pending) - 1;
-        mylab = bit < 4 ? newl[0] : oldl[0];
-#pragma unroll
-        for (int v = 1; v < 4; ++v)
-          if ((bit & 3) == v) mylab = bit < 4 ? newl[v] : oldl[v];
+        mylab = sel8(newl, oldl, bit);
       }
       const uint32_t L = __shfl_sync(0xffffffffu, mylab, leader);
       int cnt = 0, sxr = 0, syr = 0, szr = 0;
