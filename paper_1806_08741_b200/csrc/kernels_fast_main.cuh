@@ -675,8 +675,9 @@ __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fas
     const float M1 = 1.0f + M;
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
+      // (bitwise & / | on the conditions: no short-circuit branches)
       oldl[v] = word[v] & lmask;  // undefined -> lmask (never a label)
-      const bool live = valid[v] && best[v] < kSentKey;  // else: keep (nothing kept beats d_old)
+      const bool live = valid[v] & (best[v] < kSentKey);  // else: keep (nothing kept beats d_old)
       const int roff = sm.wl[warp][grp[v] + (best[v] & 7u)];  // winner's record
       const int2 ic = *reinterpret_cast<const int2*>(rec + roff + HO + 2 * C);
       const uint32_t kid = (uint32_t)ic.x;
@@ -684,12 +685,14 @@ __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fas
       const float thr = fmaf(bv, M1, A);
       const bool amb = kval(second[v]) <= thr;
       // same centre as when the label was set: D* == d_old exactly -> keep
-      const bool same = kid == oldl[v] && ic.y <= (int)(word[v] >> lbits);
-      const bool upd = !amb && !same && thr < dold[v];
-      const bool keep = !amb && (same || bv > fmaf(dold[v], M1, A));
-      nword[v] = live && upd ? (tag_now_bits | kid) : word[v];
-      if (live && !upd && !keep) exact_mask |= 1u << v;
-      if (amb) amb_mask |= 1u << v;
+      const bool same = (kid == oldl[v]) & (ic.y <= (int)(word[v] >> lbits));
+      const bool below = thr < dold[v];
+      const bool above = bv > fmaf(dold[v], M1, A);
+      const bool upd = !amb & !same & below;
+      const bool keep = !amb & (same | above);
+      nword[v] = live & upd ? (tag_now_bits | kid) : word[v];
+      exact_mask |= (unsigned)(live & !upd & !keep) << v;
+      amb_mask |= (unsigned)amb << v;
       jst[v] = roff;
     }
     // undecided voxels are queued in the warp's (now free) history staging
