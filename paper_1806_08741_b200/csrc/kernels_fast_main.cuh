@@ -17,6 +17,13 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gsrc) : "memory");
 }
+__device__ __forceinline__ void cp_async16_if(void* smem_dst, const void* gsrc, bool p) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
+               "@q cp.async.cg.shared.global [%0], [%1], 16;\n\t}" ::"r"(d),
+               "l"(gsrc), "r"((int)p)
+               : "memory");
+}
 __device__ __forceinline__ void cp_async4(void* smem_dst, const void* gsrc) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(gsrc) : "memory");
@@ -441,15 +448,15 @@ __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fas
     bool any_undef = false;
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
-      rep[v] = v;
-      if (v > 0 && word[v] == word[v - 1]) rep[v] = rep[v - 1];
-      any_undef |= valid[v] && word[v] == kUndefined;
-      if (rep[v] == v && valid[v] && word[v] != kUndefined) {
+      rep[v] = v > 0 && word[v] == word[v - 1] ? rep[v - 1] : v;
+      any_undef |= valid[v] & (word[v] == kUndefined);
+      {  // predicated copies (no branch per voxel)
+        const bool need = (rep[v] == v) & valid[v] & (word[v] != kUndefined);
         const uint32_t L = word[v] & lmask, Tg = word[v] >> lbits;
         // (history rows < 2^32: tag mode caps the tables at 8 GB)
         const float2* hc = P.hist32 + (size_t)(Tg * (uint32_t)g.k + L) * kS2;
 #pragma unroll
-        for (int i = 0; i < kS2; i += 2) cp_async16(my_stage + v * 32 * kS2 + i, hc + i);
+        for (int i = 0; i < kS2; i += 2) cp_async16_if(my_stage + v * 32 * kS2 + i, hc + i, need);
       }
     }
     cp_async_commit();
@@ -494,7 +501,7 @@ __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fas
       const int j = lane + 32 * h;
       const bool c = (uint32_t)(bmask >> (32 * h)) >> lane & 1u;
       float lb = 0.f;
-      if (c) {
+      {  // (computed for every lane, j < kFastMaxCand records exist; masked by c)
         const float* r = rec + j * RS;
 #pragma unroll
         for (int cc = 0; cc < C; ++cc) {
@@ -717,14 +724,12 @@ __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fas
     unsigned pending = 0;  // bit v: +new[v]; bit 4+v: -old[v]
     unsigned undef = 0;
 #pragma unroll
-    for (int v = 0; v < 4; ++v) {
-      if (!valid[v]) continue;
-      undef += newl[v] == lmask && !(exact_mask >> v & 1u);
-      if (newl[v] != oldl[v]) {
-        pending |= 1u << v;
-        if (oldl[v] != lmask) pending |= 1u << (4 + v);
-        ++n_changed;
-      }
+    for (int v = 0; v < 4; ++v) {  // (bitwise: no branches)
+      const bool ch = valid[v] & (newl[v] != oldl[v]);
+      undef += (unsigned)(valid[v] & (newl[v] == lmask) & !(exact_mask >> v & 1u));
+      pending |= (unsigned)ch << v;
+      pending |= (unsigned)(ch & (oldl[v] != lmask)) << (4 + v);
+      n_changed += (unsigned)ch;
     }
     if (__any_sync(0xffffffffu, undef != 0)) {
       const unsigned tu = __reduce_add_sync(0xffffffffu, undef);
