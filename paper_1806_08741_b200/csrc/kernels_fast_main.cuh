@@ -317,39 +317,36 @@ __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fas
       h = (h + 1) & (kSlotHash - 1);
   }
   {
-    // spatial tables: one warp per candidate, lanes over the table entries
-    const int per = RX + RY + (RANK == 3 ? RZ : 0);
-    for (int j = warp; j <= n; j += kWarps)
-    for (int r0 = lane; r0 < per; r0 += 32) {
-      int r = r0, a = 0;
-      if (r >= RX) {
-        r -= RX;
-        a = 1;
-        if (r >= RY) {
-          r -= RY;
-          a = 2;
-        }
-      }
-      float v = kSentinel;
-      if (j < n) {
-        const int an = a == 0 ? sm.anc[j][0] : (a == 1 ? sm.anc[j][1] : sm.anc[j][2]);
-        const int s = g.grid[a];
-        const int dx = r - an;
-        if (dx >= -s && dx <= s) {
-          const float x = (float)((a == 0 ? org[0] : (a == 1 ? org[1] : org[2])) + r);
-          // fp32 filter table from the hi/lo centre split (error in the margin)
-          const float2 cc = cxy[j * 3 + a];
-          const float t = ((cc.x - x) + cc.y) * P.inv_grid[a];
-          v = (float)g.m_sq * (t * t) * P.key_scale2;
-        }
-      }
+    // spatial tables: one warp per candidate, lanes over the entries of the x
+    // segment, then of the y|z segment (z entries follow y: both sit at
+    // RXp + r0). Per-axis values are warp-uniform scalars (no dynamic
+    // indexing of the axis arrays).
+    const float msq = (float)g.m_sq * P.key_scale2;
+    const int ox32 = (int)org[0], oy32 = (int)org[1], oz32 = RANK == 3 ? (int)org[2] : 0;
+    const int sgx = (int)g.grid[0], sgy = (int)g.grid[1], sgz = RANK == 3 ? (int)g.grid[2] : 0;
+    const float ivx = P.inv_grid[0], ivy = P.inv_grid[1], ivz = P.inv_grid[2];
+    const int per_yz = RY + (RANK == 3 ? RZ : 0);
+    for (int j = warp; j <= n; j += kWarps) {
       float* rj = rec + (size_t)j * RS;
-      if (a == 0) {
-        rj[r] = v;
-      } else if (a == 1) {
-        rj[RXp + r] = v;
-      } else {
-        rj[RXp + RY + r] = v;
+      const bool real = j < n;
+      const int jj = real ? j : 0;
+      const int anx = sm.anc[jj][0], any_ = sm.anc[jj][1], anz = sm.anc[jj][2];
+      const float2 ccx = cxy[jj * 3], ccy = cxy[jj * 3 + 1], ccz = cxy[jj * 3 + 2];
+      for (int r = lane; r < RX; r += 32) {
+        const int dx = r - anx;
+        const float x = (float)(ox32 + r);
+        const float t = ((ccx.x - x) + ccx.y) * ivx;
+        rj[r] = real & (dx >= -sgx) & (dx <= sgx) ? msq * (t * t) : kSentinel;
+      }
+      for (int r0 = lane; r0 < per_yz; r0 += 32) {
+        const bool isz = RANK == 3 && r0 >= RY;
+        const int r = isz ? r0 - RY : r0;
+        const int dx = r - (isz ? anz : any_);
+        const int sg = isz ? sgz : sgy;
+        const float x = (float)((isz ? oz32 : oy32) + r);
+        const float2 cc = isz ? ccz : ccy;
+        const float t = ((cc.x - x) + cc.y) * (isz ? ivz : ivy);
+        rj[RXp + r0] = real & (dx >= -sg) & (dx <= sg) ? msq * (t * t) : kSentinel;
       }
     }
   }
