@@ -33,7 +33,8 @@ __all__ = [
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsslic_b200.so")
+# (SSLIC_B200_LIB: another in-tree build of the same library, for A/B timing)
+LIB_PATH = os.environ.get("SSLIC_B200_LIB") or os.path.join(HERE, "libsslic_b200.so")
 UNDEFINED = 0xFFFFFFFF  # LabelMap::kUndefined (image.hpp:291)
 
 U8, U16, F32, F64 = 0, 1, 2, 3

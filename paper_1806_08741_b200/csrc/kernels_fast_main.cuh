@@ -89,6 +89,86 @@ __device__ __forceinline__ void load_run(const T* src, bool vec, const bool* val
 // else 4 (128 registers; 5 costs config 4 7% through spills)
 __host__ __device__ constexpr int fast_min_blocks(int C) { return C <= 2 ? 5 : 4; }
 
+// fp64 re-decision of one queued voxel of the fast kernel (entry: old label
+// word, region-local coordinates | amb | winner slot): writes the label word
+// and adds the voxel's deltas to the CTA slots (layout: k_assign_fast).
+// Returns 1 if the label value changed.
+template <int RANK, int C, typename TS>
+__device__ __noinline__ unsigned redecide_queued(const FastParams& P, const FastSmem& sm, int* accs,
+                                                 const int64_t* org, uint32_t* lab_r,
+                                                 const void* img_rv, const double* imgx_r, int s1,
+                                                 int s2, bool split16, const uint2 e) {
+  constexpr bool kF64 = std::is_same<TS, double>::value;
+  using T = typename std::conditional<kF64, float, TS>::type;
+  constexpr bool kFloatAcc = sizeof(TS) >= 4;
+  constexpr int kStride = C + RANK, kComp = kStride + 1, kCompA = kComp + C;
+  const T* img_r = static_cast<const T*>(img_rv);
+  const uint32_t lmask = P.codec.label_mask;
+  const int qx = (int)(e.y & 63u), qy = (int)(e.y >> 6 & 63u), qz = (int)(e.y >> 12 & 63u);
+  const bool qamb = e.y >> 18 & 1u;
+  const int qj = (int)(e.y >> 19 & 63u);
+  const int qrel = qx + qy * s1 + qz * s2;
+  const T* qpx = img_r + (size_t)qrel * C;
+  const uint32_t nw = exact_region_voxel(P, sm, org[0] + qx, org[1] + qy, org[2] + qz,
+                                         qpx - static_cast<const T*>(P.img), e.x, qamb, qj, org);
+  const uint32_t ol = e.x & lmask, nl2 = nw & lmask;
+  if (nw != e.x) lab_r[qrel] = nw;
+  if (nl2 == lmask) atomicAdd(P.counters, 1ull);  // slic.hpp:330-331
+  if (nl2 == ol) return 0u;
+  const float fscale = ldexpf(1.0f, P.shift);
+  const long long co[3] = {qx, qy, qz};
+#pragma unroll 1
+  for (int sg = 0; sg < 2; ++sg) {
+    const uint32_t L = sg == 0 ? nl2 : ol;
+    if (L == lmask) continue;
+    const long long sgn = sg == 0 ? 1 : -1;
+    const int S = slot_of(sm, L);
+    long long val[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      if constexpr (kF64) val[c] = to_fixed(imgx_r[(int64_t)qrel * C + c], P.shift);
+      else val[c] = sizeof(T) < 4 ? (long long)qpx[c]
+                                  : (long long)__float2ll_rn((float)qpx[c] * fscale);
+    }
+    if (S >= 0) {
+      int* a = accs + S * kCompA;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const long long v = sgn * val[c];
+        if constexpr (kFloatAcc) {
+          const unsigned long long u = (unsigned long long)v;
+          const uint32_t l = (uint32_t)u;
+          const uint32_t before = atomicAdd(reinterpret_cast<unsigned*>(a) + c, l);
+          const uint32_t carry = before + l < before ? 1u : 0u;
+          atomicAdd(reinterpret_cast<unsigned*>(a) + kComp + c, (uint32_t)(u >> 32) + carry);
+        } else if (split16) {
+          atomicAdd(a + c, (int)(v & 255));
+          atomicAdd(a + kComp + c, (int)(v >> 8));
+        } else {
+          atomicAdd(a + c, (int)v);
+        }
+      }
+#pragma unroll
+      for (int ax = 0; ax < RANK; ++ax) atomicAdd(a + C + ax, (int)(sgn * co[ax]));
+      atomicAdd(a + kStride, (int)sgn);
+    } else {
+      unsigned long long* a = P.acc + (uint64_t)L * kComp;
+#pragma unroll
+      for (int c = 0; c < C; ++c) atomicAdd(a + c, (unsigned long long)(sgn * val[c]));
+#pragma unroll
+      for (int ax = 0; ax < RANK; ++ax)
+        atomicAdd(a + C + ax, (unsigned long long)(sgn * (co[ax] + org[ax])));
+      atomicAdd(a + kStride, (unsigned long long)sgn);
+    }
+  }
+  return 1u;
+}
+
+// per-warp capacity of the batched fp64 re-decision queue (entries)
+// (3 channels only: the call of the non-inlined re-decision costs the 96-register
+// 1-2 channel kernels spills, and config 4's shared memory has no room)
+__host__ __device__ constexpr int fast_queue_cap(int C) { return C == 3 ? 32 : 0; }
+
 // T is the caller's storage type; T = double sweeps an f32 working copy (TW)
 // with the pixel rounding folded into the margins, and takes the exact f64
 // values for the re-decisions and the fixed-point deltas.
@@ -124,6 +204,7 @@ __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fas
   // intensities, unrolled over the 4 voxels for integer volumes (measured:
   // config 4 f32 x4 vs config 3 u16)
   constexpr bool kRolledDeltas = kFloatAcc;
+  constexpr int kQCap = fast_queue_cap(C);
   using AccT = int;
   constexpr int kCompA = kComp + C;
   AccT* accs = reinterpret_cast<AccT*>(rec + (size_t)(kFastMaxCand + 1) * RS);
@@ -383,6 +464,11 @@ __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fas
   }
   __syncthreads();
 
+  // persistent per-warp queue of fp64 re-decisions (3 channels, see
+  // fast_queue_cap; the others drain per box, inline)
+  [[maybe_unused]] uint2* const pq =
+      reinterpret_cast<uint2*>(pf_pix + kWarps * 2 * 32 * kPW) + (size_t)warp * kQCap;
+  [[maybe_unused]] int pqn = 0;
   // ---- per-warp sweep over the region's boxes ----
   int buf = 0;
 #pragma unroll 1
@@ -974,6 +1060,41 @@ __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fas
 
     }  // npend != 0
 
+    if constexpr (kQCap > 0) {
+      // (the fp64 re-decision is a non-inlined call: rare, and kept out of
+      // the sweep's register allocation)
+      auto drain = [&](const uint2* q, int cnt) {
+        for (int i0 = 0; i0 < cnt; i0 += 32) {
+          const int i = i0 + lane;
+          if (i < cnt) {
+            n_changed += redecide_queued<RANK, C, TS>(P, sm, accs, org, lab_r, img_r, imgx_r, s1,
+                                                      s2, split16, q[i]);
+            ++n_redecided;
+          }
+        }
+      };
+    // ---- deferred fp64 re-decisions of this box (batched per warp) ----
+    // The box's queued voxels move to the warp's persistent queue, which is
+    // re-decided one voxel per lane once it holds a full warp (or at the end
+    // of the region): one fp64 pass serves up to 32 voxels instead of the
+    // one or two a box typically has.
+    __syncwarp();
+    const int nq = *xcnt;
+    if (nq > 0) {  // uniform
+      if (kQCap > 0 && pqn + nq <= kQCap) {
+        for (int i = lane; i < nq; i += 32) pq[pqn + i] = xqueue[i];
+        pqn += nq;
+        if (pqn >= 32) {
+          __syncwarp();
+          drain(pq, pqn);
+          pqn = 0;
+        }
+      } else {
+        drain(xqueue, nq);
+      }
+      __syncwarp();
+    }
+    } else {
     // ---- deferred fp64 re-decisions of this box (one queued voxel per lane) ----
     __syncwarp();
     const int nq = *xcnt;
@@ -1032,6 +1153,23 @@ __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fas
         }
       }
     }
+    }
+  }
+  if constexpr (kQCap > 0) {
+      auto drain = [&](const uint2* q, int cnt) {
+        for (int i0 = 0; i0 < cnt; i0 += 32) {
+          const int i = i0 + lane;
+          if (i < cnt) {
+            n_changed += redecide_queued<RANK, C, TS>(P, sm, accs, org, lab_r, img_r, imgx_r, s1,
+                                                      s2, split16, q[i]);
+            ++n_redecided;
+          }
+        }
+      };
+      if (pqn > 0) {
+        __syncwarp();
+        drain(pq, pqn);
+      }
   }
   cp_async_wait_all();
   if (P.eval_count) {
@@ -1226,6 +1364,7 @@ inline size_t fast_smem_bytes(const Geom& g, const int* R) {
   b += (size_t)warps * 2 * 32 * 16;  // next-box label words
   const int wsize = g.dtype == SSLIC_F64 ? 4 : dtype_size(g.dtype);  // working pixel size
   b += (size_t)warps * 2 * 32 * 4 * pf_pix_words(g.channels, wsize);
+  b += (size_t)warps * fast_queue_cap(g.channels) * sizeof(uint2);
   return b;
 }
 
