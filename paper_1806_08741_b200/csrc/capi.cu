@@ -6,6 +6,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -326,17 +327,79 @@ struct EventMarks {
   }
 };
 
-int run_loop_overlapped(Engine& e, Stream& st, uint32_t* labels_out, int64_t n) {
+// Pipelined start of a whole-volume run (Engine::pipeline_ok): the image
+// travels host -> device in z chunks on a copy stream, and each chunk's
+// arrival releases the perturbation of the clusters whose gradient hood it
+// completes and iteration 0's assign of the region rows whose planes and
+// candidate centres are then all present; iteration 0's update closes it.
+// The H2D copy thus overlaps init + iteration 0 instead of preceding them.
+void pipelined_start(Engine& e, const sslic_image* img, void* dev, Stream& st, EventMarks& em) {
+  const int64_t d = img->dims[2];
+  const size_t plane_bytes =
+      (size_t)img->dims[0] * img->dims[1] * img->channels * dtype_size(img->dtype);
+  const int64_t S = e.geom().grid[2], cells = e.geom().cells[2];
+  const int64_t RZ = e.region_z(), rows = e.region_rows();
+  constexpr int kChunks = 8;
+  cudaStream_t cs = nullptr;
+  SSLIC_CUDA_CHECK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  cudaEvent_t ev[kChunks + 1];
+  for (auto& x : ev) SSLIC_CUDA_CHECK(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+  SSLIC_CUDA_CHECK(cudaEventRecord(ev[kChunks], st.s));  // the device buffer exists
+  SSLIC_CUDA_CHECK(cudaStreamWaitEvent(cs, ev[kChunks], 0));
+  e.init_pipeline();
+  int64_t z_init = 0, rows_done = 0;
+  for (int c = 0; c < kChunks; ++c) {
+    const int64_t p0 = d * c / kChunks, p1 = d * (c + 1) / kChunks;
+    const bool last = c == kChunks - 1;
+    if (p1 > p0)
+      SSLIC_CUDA_CHECK(cudaMemcpyAsync(static_cast<char*>(dev) + p0 * plane_bytes,
+                                       static_cast<const char*>(img->data) + p0 * plane_bytes,
+                                       (p1 - p0) * plane_bytes, cudaMemcpyHostToDevice, cs));
+    SSLIC_CUDA_CHECK(cudaEventRecord(ev[c], cs));
+    SSLIC_CUDA_CHECK(cudaStreamWaitEvent(st.s, ev[c], 0));
+    // a cluster's perturbation reads planes [z - 2, z + 2] of its initial z
+    const int64_t zi = last ? d : std::max(z_init, p1 - 2);
+    e.init_range(z_init, zi);
+    z_init = zi;
+    // region rows whose planes have arrived and whose candidate clusters
+    // (anchor cells up to (zhi + S) / S, k_region_cand) are perturbed
+    int64_t r = rows_done;
+    while (r < rows && !last) {
+      const int64_t zhi = std::min((r + 1) * RZ, d) - 1;
+      const int64_t chi = std::min((zhi + S) / S, cells - 1);
+      const int64_t zc = std::min(chi * S + S / 2, d - 1);
+      if (zhi >= p1 || zc >= z_init) break;
+      ++r;
+    }
+    if (last) r = rows;
+    e.assign_rows(rows_done, r);
+    rows_done = r;
+    em.mark(st.s, "chunk" + std::to_string(c));
+  }
+  e.update();
+  em.mark(st.s, "it0");
+  SSLIC_CUDA_CHECK(cudaStreamSynchronize(cs));
+  cudaStreamDestroy(cs);
+  for (auto& x : ev) cudaEventDestroy(x);
+}
+
+int run_loop_overlapped(Engine& e, Stream& st, uint32_t* labels_out, int64_t n,
+                        const sslic_image* pipelined_img = nullptr, void* dev = nullptr) {
   EventMarks em;
   em.mark(st.s, "start");
-  e.init(true);
-  e.commit();
-  em.mark(st.s, "init");
+  if (pipelined_img) {
+    pipelined_start(e, pipelined_img, dev, st, em);
+  } else {
+    e.init(true);
+    e.commit();
+    em.mark(st.s, "init");
+  }
   const int iters = e.max_iterations();
-  // snapshot early enough that its D2H copy (~n x 4 B at PCIe speed) hides
-  // behind the remaining iterations; later changes travel as a change list
-  const int snap = iters - 4;
-  for (int it = 0; it < snap; ++it) {
+  // the labels after iteration iters - 5 (iters - 4 for short runs) are
+  // copied while the last iterations run (4.3 GB at PCIe speed take ~6 of
+  // config 3's iterations); later changes travel as a change list
+  const int snap = iters >= 8 ? iters - 5 : iters - 4;
+  for (int it = e.iterations_done(); it < snap; ++it) {
     e.assign(true);
     e.update();
     em.mark(st.s, "it" + std::to_string(it));
@@ -356,7 +419,7 @@ int run_loop_overlapped(Engine& e, Stream& st, uint32_t* labels_out, int64_t n) 
   SSLIC_CUDA_CHECK(cudaEventCreateWithFlags(&copied, cudaEventDisableTiming));
   SSLIC_CUDA_CHECK(cudaEventRecord(copied, cs));
   em.mark(cs, "copied");
-  for (int it = snap; it < iters; ++it) {
+  for (int it = std::max(snap, e.iterations_done()); it < iters; ++it) {
     e.assign(true);
     e.update();
     em.mark(st.s, "it" + std::to_string(it));
@@ -505,18 +568,35 @@ int sslic_run_slic(const sslic_image* img, const sslic_params* params, int devic
     validate_params(params, img);
     PhaseTimer pt("run_slic");
     Stream st(device);
-    auto dimg = upload_image(img, st);
-    pt.mark(st, "upload");
-    const sslic_image v = device_view(img, dimg->p);
-    const int64_t last = img->dims[img->rank - 1];
-    Engine e(v, *params, device, 0, last, 0, last, st.s);
-    pt.mark(st, "engine");
     const int64_t n = pixel_count(*img);
+    const int64_t last = img->dims[img->rank - 1];
+    const bool overlapped = !params->has_residual_threshold && n >= ((int64_t)1 << 24) &&
+                            host_pinned_mapped(labels_out);
+    // pipelined upload (u8/u16 volumes: no image-wide pre-pass before init)
+    const size_t img_bytes = (size_t)n * img->channels * dtype_size(img->dtype);
+    std::unique_ptr<DeviceBuf> dimg;
+    bool pipelined = false;
+    if (overlapped && img->rank == 3 && (img->dtype == SSLIC_U8 || img->dtype == SSLIC_U16) &&
+        std::getenv("SSLIC_NO_PIPELINED_UPLOAD") == nullptr) {
+      dimg = std::make_unique<DeviceBuf>(img_bytes, st.s);
+      pipelined = true;
+    } else {
+      dimg = upload_image(img, st);
+      pt.mark(st, "upload");
+    }
+    const sslic_image v = device_view(img, dimg->p);
+    Engine e(v, *params, device, 0, last, 0, last, st.s);
+    if (pipelined && !(e.pipeline_ok() && !e.dist_mode() && e.max_iterations() >= 4)) {
+      SSLIC_CUDA_CHECK(
+          cudaMemcpyAsync(dimg->p, img->data, img_bytes, cudaMemcpyHostToDevice, st.s));
+      pipelined = false;
+    }
+    pt.mark(st, "engine");
     int done = 0;
-    if (!e.dist_mode() && !params->has_residual_threshold && e.max_iterations() >= 4 &&
-        n >= ((int64_t)1 << 24) && host_pinned_mapped(labels_out)) {
-      done = run_loop_overlapped(e, st, labels_out, n);
-      pt.mark(st, "iterations + overlapped label download");
+    if (!e.dist_mode() && overlapped && e.max_iterations() >= 4) {
+      done = run_loop_overlapped(e, st, labels_out, n, pipelined ? img : nullptr, dimg->p);
+      pt.mark(st, pipelined ? "pipelined upload + iterations + overlapped label download"
+                            : "iterations + overlapped label download");
     } else {
       done = run_loop(e, params, st);
       pt.mark(st, "iterations");

@@ -227,6 +227,55 @@ void Engine::commit() {
   }
 }
 
+bool Engine::pipeline_ok() const {
+  if (g_.rank != 3 || dist_mode_ || path_ != AssignPath::kFast || g_.k != g_.ncells) return false;
+  if (g_.slab_begin != 0 || g_.slab_end != g_.dims[2] || g_.data_begin != 0) return false;
+  if (g_.dtype != SSLIC_U8 && g_.dtype != SSLIC_U16) return false;  // no image-wide pre-pass
+  for (int a = 0; a < g_.rank; ++a)
+    if (g_.grid[a] < 3 || g_.dims[a] % g_.grid[a] == 1) return false;
+  return true;
+}
+
+int Engine::region_z() const {
+  int R[3];
+  region_extents(g_, R);
+  return R[2];
+}
+
+int64_t Engine::region_rows() const { return (g_.dims[2] + region_z() - 1) / region_z(); }
+
+void Engine::init_pipeline() {
+  if (!pipeline_ok()) throw Error(SSLIC_EINVAL, "engine: pipelined start not applicable");
+  k_identity_bins<<<blocks_for(g_.ncells + 1, 256), 256, 0, stream_>>>(g_.ncells, cell_start_,
+                                                                       items_);
+  launch_check("identity_bins");
+  SSLIC_CUDA_CHECK(cudaMemsetAsync(cell_count_, 0, (g_.ncells + 1) * sizeof(int), stream_));
+  SSLIC_CUDA_CHECK(cudaMemsetAsync(cursor_, 0, g_.ncells * sizeof(int), stream_));
+  SSLIC_CUDA_CHECK(cudaMemsetAsync(counters_, 0, 8 * sizeof(unsigned long long), stream_));
+  if (!acc_zero_)
+    SSLIC_CUDA_CHECK(
+        cudaMemsetAsync(acc_, 0, partials_count() * sizeof(unsigned long long), stream_));
+  acc_zero_ = false;
+}
+
+void Engine::init_range(int64_t z0, int64_t z1) {
+  if (z1 <= z0) return;
+  k_init_perturb<<<blocks_for(g_.k, 128), 128, 0, stream_>>>(g_, img_, current_centers(), 1, z0,
+                                                             z1);
+  launch_check("init_perturb(range)");
+  const int s2 = hist32_stride(g_.stride);
+  k_anchors_split_range<<<blocks_for(g_.k, 256), 256, 0, stream_>>>(
+      g_, current_centers(), anchors_, hist32_ + (size_t)iter_ * g_.k * s2, s2, z0, z1);
+  launch_check("anchors_split(range)");
+}
+
+void Engine::assign_rows(int64_t r0, int64_t r1) {
+  if (r1 <= r0) return;
+  launch_fast_assign(fast_params(), stream_, r0, r1);
+  ++launches_;
+  launch_check("assign_fast(rows)");
+}
+
 void Engine::assign(bool accumulate) {
   if (!dist_mode_ && iter_ >= max_iter_)
     throw Error(SSLIC_EINVAL, "engine: iteration budget exhausted (history tables)");
@@ -265,6 +314,16 @@ void Engine::launch_assign_kernel(bool accumulate) {
   const int64_t nv = slab_voxels();
   const double* hist = dist_mode_ ? nullptr : centers_;
   if (path_ == AssignPath::kFast && accumulate && !dist_mode_) {
+    launch_fast_assign(fast_params(), s);
+    ++launches_;  // k_region_cand + k_assign_fast
+    launch_check("assign_fast");
+    return;
+  }
+  launch_exact_kernel(accumulate, nv, hist);
+}
+
+FastParams Engine::fast_params() {
+    const double* hist = dist_mode_ ? nullptr : centers_;
     FastParams P{};
     P.g = g_;
     P.img = img32_ ? static_cast<const void*>(img32_) : img_;
@@ -291,11 +350,11 @@ void Engine::launch_assign_kernel(bool accumulate) {
     P.abs_margin = abs_margin_ * P.key_scale2;
     P.region_cand = region_cand_;
     P.max_cand = max_cand_;
-    launch_fast_assign(P, s);
-    ++launches_;  // k_region_cand + k_assign_fast
-    launch_check("assign_fast");
-    return;
-  }
+    return P;
+}
+
+void Engine::launch_exact_kernel(bool accumulate, int64_t nv, const double* hist) {
+  cudaStream_t s = stream_;
   const unsigned nb = blocks_for(nv, 256);
   if (dist_mode_) {
     if (accumulate)

@@ -9,6 +9,7 @@
 namespace sslic_b200 {
 
 enum class AssignPath { kExact = 0, kFast = 1 };
+struct FastParams;  // kernels_fast.cuh
 
 class Engine {
  public:
@@ -27,6 +28,20 @@ class Engine {
   void set_centers_host(const double* h);
   // Anchors + candidate bins of the current table.
   void commit();
+  // Pipelined start (whole-volume rank-3 fast path, used by run_slic while
+  // the image is still arriving in z chunks): pipeline_ok() holds when
+  // perturbation cannot move an anchor out of its initial cell (S >= 3 and
+  // no 1-plane last cell on every axis), so iteration 0's bins are the
+  // identity; init_pipeline() sets them, init_range(z0, z1) perturbs the
+  // clusters whose initial centre lies in planes [z0, z1) and publishes
+  // their anchors and fp32 split, assign_rows(r0, r1) runs iteration 0's
+  // fused assign on region rows [r0, r1). Then update() as usual.
+  bool pipeline_ok() const;
+  void init_pipeline();
+  void init_range(int64_t z0, int64_t z1);
+  void assign_rows(int64_t r0, int64_t r1);
+  int region_z() const;
+  int64_t region_rows() const;
   // One map phase: fused assign + accumulate into partials (zeroed first).
   void assign(bool accumulate = true);
   // Accumulate only (labels as given).
@@ -75,6 +90,8 @@ class Engine {
  private:
   void launch_check(const char* what);
   void launch_assign_kernel(bool accumulate);
+  FastParams fast_params();
+  void launch_exact_kernel(bool accumulate, int64_t nv, const double* hist);
   void compute_shift();
 
   Geom g_{};

@@ -45,9 +45,20 @@ static __device__ inline double gradient_sq_at(const Geom& g, const void* img, c
   return acc;
 }
 
-static __global__ void k_init_perturb(Geom g, const void* img, double* centers, int perturb) {
+// (z0 <= z1: only the clusters whose initial centre lies in planes [z0, z1)
+// are written, the others are left as they are -- the pipelined start of
+// run_slic perturbs the clusters chunk by chunk as the image arrives)
+static __global__ void k_init_perturb(Geom g, const void* img, double* centers, int perturb,
+                                      int64_t z0 = 0, int64_t z1 = -1) {
   const int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (id >= g.k) return;
+  if (z0 <= z1) {
+    const int last = g.rank - 1;
+    const int64_t zc = id / (g.k / g.cells[last]);
+    int64_t z = zc * g.grid[last] + g.grid[last] / 2;
+    if (z > g.dims[last] - 1) z = g.dims[last] - 1;
+    if (z < z0 || z >= z1) return;
+  }
   double* ctr = centers + id * g.stride;
   int64_t coord[kMaxRank];
   int64_t rem = id;
@@ -178,6 +189,41 @@ static __global__ void k_anchors(Geom g, const double* centers, int* anchors, in
   for (int a = g.rank; a < kMaxRank; ++a) anchors[id * kMaxRank + a] = 0;
   cell_of[id] = (int)cell;
   atomicAdd(cell_count + cell, 1);
+}
+
+// Identity anchor-cell bins (cluster k in cell k, one per cell): the bins
+// commit() builds at iteration 0 whenever perturbation cannot move an anchor
+// out of its initial cell (Engine::pipeline_ok).
+static __global__ void k_identity_bins(int64_t ncells, int* cell_start, int* items) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c > ncells) return;
+  cell_start[c] = (int)c;
+  if (c < ncells) items[c] = (int)c;
+}
+
+// Anchors and the hi/lo fp32 split (padded rows of s2 float2) of the clusters
+// whose initial centre lies in planes [z0, z1) (pipelined start).
+static __global__ void k_anchors_split_range(Geom g, const double* centers, int* anchors,
+                                             float2* split, int s2, int64_t z0, int64_t z1) {
+  const int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (id >= g.k) return;
+  const int last = g.rank - 1;
+  const int64_t zc = id / (g.k / g.cells[last]);
+  int64_t z = zc * g.grid[last] + g.grid[last] / 2;
+  if (z > g.dims[last] - 1) z = g.dims[last] - 1;
+  if (z < z0 || z >= z1) return;
+  for (int a = 0; a < kMaxRank; ++a)
+    anchors[id * kMaxRank + a] =
+        a < g.rank ? (int)anchor_of(centers[id * g.stride + g.channels + a]) : 0;
+  for (int i = 0; i < s2; ++i) {
+    if (i >= g.stride) {
+      split[id * s2 + i] = make_float2(0.f, 0.f);
+      continue;
+    }
+    const double v = centers[id * g.stride + i];
+    const float h = __double2float_rn(v);
+    split[id * s2 + i] = make_float2(h, __double2float_rn(v - (double)h));
+  }
 }
 
 static __global__ void k_bin_fill(int64_t k, const int* cell_of, const int* cell_start, int* cursor,

@@ -1439,7 +1439,9 @@ inline float fast_margin(int channels) {
   return (float)(1.5 * 2.0 * (channels + 14) * u);
 }
 
-inline void launch_fast_assign(FastParams P, cudaStream_t s) {
+// (row0 < row1: only region rows [row0, row1) of the slab, z-ordered)
+inline void launch_fast_assign(FastParams P, cudaStream_t s, int64_t row0 = 0,
+                               int64_t row1 = -1) {
   const Geom& g = P.g;
   region_extents(g, P.R);
   for (int a = 0; a < 3; ++a) {
@@ -1452,6 +1454,12 @@ inline void launch_fast_assign(FastParams P, cudaStream_t s) {
     const int64_t z0 = g.slab_begin / P.R[2] * P.R[2];
     P.reg_z0 = z0;
     P.nreg[2] = (int)((g.slab_end - z0 + P.R[2] - 1) / P.R[2]);
+    if (row0 < row1) {
+      if (row1 > P.nreg[2]) row1 = P.nreg[2];
+      P.reg_z0 = z0 + row0 * P.R[2];
+      P.nreg[2] = (int)(row1 - row0);
+      if (P.nreg[2] <= 0) return;
+    }
   } else {
     P.reg_z0 = 0;
     P.nreg[2] = 1;

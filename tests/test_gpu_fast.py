@@ -112,18 +112,24 @@ def test_engine_labels_tensor_and_gather_single_rank(sslic):
     assert np.array_equal(cc, s.enforce_connectivity(full, dims, table, p))
 
 
-@pytest.mark.parametrize("iters", [8, 4], ids=["change-list", "list-overflow"])
-def test_run_slic_overlapped_download_matches(sslic, iters):
-    """sslic_run_slic into a pinned host label map of >= 2^24 voxels overlaps
-    the label download with the last iterations (snapshot copy, then the
-    labels changed since as an (index, label) list applied on the host, or a
-    whole-map copy when more than 5% changed: 4 iterations snapshot after
-    the first); the map and centres must equal the same call into pageable
-    memory (plain download) bit for bit."""
+@pytest.mark.parametrize("dims,iters", [
+    ((256, 256, 256), 8), ((256, 256, 256), 4), ((256, 256, 264), 8), ((257, 256, 257), 6)],
+    ids=["change-list", "list-overflow", "partial-region-row", "no-pipeline"])
+def test_run_slic_overlapped_download_matches(sslic, dims, iters):
+    """sslic_run_slic into a pinned host label map of >= 2^24 voxels
+    * uploads the image in z chunks, overlapped with the chunk-wise centre
+      perturbation and iteration 0's assign (Engine::pipeline_ok; not for a
+      1-plane last cell, the no-pipeline case);
+    * overlaps the label download with the last iterations: a snapshot copy,
+      then the labels changed since as an (index, label) list applied on the
+      host, or a whole-map copy when more than 5% changed (4 iterations
+      snapshot after the first).
+    The map, centres and residuals must equal the same call into pageable
+    memory (plain upload and download) bit for bit."""
     import ctypes as C
     import torch
     s = sslic
-    cfg, dims, ch, dtype, grid, m = (3, (256, 256, 256), 1, np.uint16, (16, 16, 16), 10.0)
+    cfg, ch, dtype, grid, m = (3, 1, np.uint16, (16, 16, 16), 10.0)
     n = int(np.prod(dims))
     dev = torch.empty(n * ch, dtype=torch.int16, device="cuda")
     s.synth_generate(cfg, dims, dtype, ch, 77, 0, dims[-1], dev.data_ptr())
