@@ -1184,18 +1184,38 @@ __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fas
   }
   __syncthreads();
   // ---- flush CTA slots (one global atomic per non-zero component) ----
-  for (int j = warp; j < n; j += kWarps) {
-    if (lane < kComp) {
-      long long v = (long long)accs[j * kCompA + lane];
-      if (lane < C) {
-        const int h = accs[j * kCompA + kComp + lane];
+  // 128-register kernels: one (candidate, component) pair per thread (every
+  // lane busy; config 4 -4 %); the 96-register ones keep one warp per
+  // candidate (the pair loop costs them spills)
+  if constexpr (fast_min_blocks(C) == 4) {
+    for (int t = tid; t < n * kComp; t += kFastThreads) {
+      const int j = t / kComp, cp = t - j * kComp;
+      long long v = (long long)accs[j * kCompA + cp];
+      if (cp < C) {
+        const int h = accs[j * kCompA + kComp + cp];
         if constexpr (kFloatAcc)
           v = (long long)((unsigned long long)(uint32_t)v | (unsigned long long)(uint32_t)h << 32);
         else
           v += 256LL * (long long)h;
+      } else if (cp < kStride) {
+        v += (long long)accs[j * kCompA + kStride] * org[cp - C];
       }
-      if (lane >= C && lane < kStride) v += (long long)accs[j * kCompA + kStride] * org[lane - C];
-      if (v) atomicAdd(P.acc + (uint64_t)sm.id[j] * kComp + lane, (unsigned long long)v);
+      if (v) atomicAdd(P.acc + (uint64_t)sm.id[j] * kComp + cp, (unsigned long long)v);
+    }
+  } else {
+    for (int j = warp; j < n; j += kWarps) {
+      if (lane < kComp) {
+        long long v = (long long)accs[j * kCompA + lane];
+        if (lane < C) {
+          const int h = accs[j * kCompA + kComp + lane];
+          if constexpr (kFloatAcc)
+            v = (long long)((unsigned long long)(uint32_t)v | (unsigned long long)(uint32_t)h << 32);
+          else
+            v += 256LL * (long long)h;
+        }
+        if (lane >= C && lane < kStride) v += (long long)accs[j * kCompA + kStride] * org[lane - C];
+        if (v) atomicAdd(P.acc + (uint64_t)sm.id[j] * kComp + lane, (unsigned long long)v);
+      }
     }
   }
 }
