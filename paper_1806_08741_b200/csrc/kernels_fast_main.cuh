@@ -804,19 +804,25 @@ __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fas
     }
 
     // ---- delta accumulation: +new / -old for voxels whose label changed ----
-    unsigned pending = 0;  // bit v: +new[v]; bit 4+v: -old[v]
-    unsigned undef = 0;
+    // bit v: +new[v]; bit 4+v: -old[v]. A voxel whose old word is defined
+    // has -old exactly when it has +new; an undefined word (new or old) can
+    // only occur where the lane saw an undefined old word (any_undef), so
+    // the undefined-label bookkeeping runs only in such boxes.
+    unsigned chm = 0;
 #pragma unroll
-    for (int v = 0; v < 4; ++v) {  // (bitwise: no branches)
-      const bool ch = valid[v] & (newl[v] != oldl[v]);
-      undef += (unsigned)(valid[v] & (newl[v] == lmask) & !(exact_mask >> v & 1u));
-      pending |= (unsigned)ch << v;
-      pending |= (unsigned)(ch & (oldl[v] != lmask)) << (4 + v);
-      n_changed += (unsigned)ch;
-    }
-    if (__any_sync(0xffffffffu, undef != 0)) {
+    for (int v = 0; v < 4; ++v) chm |= (unsigned)(valid[v] & (newl[v] != oldl[v])) << v;
+    n_changed += (unsigned)__popc(chm);
+    unsigned pending = chm | chm << 4;
+    if (__any_sync(0xffffffffu, any_undef)) {
+      unsigned undef = 0, olddef = 0;
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        undef += (unsigned)(valid[v] & (newl[v] == lmask) & !(exact_mask >> v & 1u));
+        olddef |= (unsigned)(oldl[v] != lmask) << v;
+      }
+      pending = chm | (chm & olddef) << 4;
       const unsigned tu = __reduce_add_sync(0xffffffffu, undef);
-      if (lane == 0) atomicAdd(P.counters, (unsigned long long)tu);  // slic.hpp:330-331
+      if (lane == 0 && tu) atomicAdd(P.counters, (unsigned long long)tu);  // slic.hpp:330-331
     }
     // Per-lane deltas (the common case): each lane adds its contributions
     // into the CTA slots, consecutive voxels of one label merged into one
