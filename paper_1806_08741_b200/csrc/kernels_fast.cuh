@@ -82,7 +82,7 @@ struct alignas(16) FastSmem {
   int n_cand;
   int id[kFastMaxCand];
   short anc[kFastMaxCand][3];  // region-local anchors
-  unsigned short wl[kFastThreads / 32][kFastMaxCand + 8];   // record offsets (floats)
+  alignas(8) uint32_t wl[kFastThreads / 32][kFastMaxCand + 8];  // record offsets (floats)
   unsigned short htab[2 * kFastMaxCand];                               // cluster id -> slot
   float cpl[kFastMaxCand][3];        // centre coordinates relative to the region origin
   unsigned long long bmask[3][16];   // per axis and box index: candidates whose window overlaps

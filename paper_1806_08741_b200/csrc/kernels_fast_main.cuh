@@ -655,15 +655,15 @@ __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fas
       const unsigned lt = (1u << lane) - 1u;
       if (keep[0]) {
         const int pos = __popc(m0 & lt);
-        sm.wl[warp][pos] = (unsigned short)(lane * RS);
+        sm.wl[warp][pos] = (uint32_t)(lane * RS);
       }
       if (keep[1]) {
         const int pos = __popc(m0) + __popc(m1 & lt);
-        sm.wl[warp][pos] = (unsigned short)((lane + 32) * RS);
+        sm.wl[warp][pos] = (uint32_t)((lane + 32) * RS);
       }
       nl = __popc(m0) + __popc(m1);
       if (lane == 0 && (nl & 1)) {  // pad to a pair: sentinel record
-        sm.wl[warp][nl] = (unsigned short)(n * RS);
+        sm.wl[warp][nl] = (uint32_t)(n * RS);
       }
       __syncwarp();
     }
@@ -692,8 +692,8 @@ __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fas
     }
     // the next pair of record offsets is loaded one step ahead (the list is
     // padded, so reading one pair past the end stays inside wl)
-    const uint32_t* wl2 = reinterpret_cast<const uint32_t*>(sm.wl[warp]);
-    uint32_t pr = wl2[0];
+    const uint2* wl2 = reinterpret_cast<const uint2*>(sm.wl[warp]);
+    uint2 pr = wl2[0];
 #pragma unroll 1
     for (int g0 = 0; g0 < nlp; g0 += 8) {
       uint32_t before[4];
@@ -704,11 +704,11 @@ __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fas
       for (int jj = g0; jj < g1; jj += 2) {
         uint32_t key[2][4];
         const uint32_t jl0 = (uint32_t)(jj & 7);
-        const uint32_t cur = pr;
+        const uint2 cur = pr;
         pr = wl2[(jj >> 1) + 1];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const float* r = rec + (h ? cur >> 16 : cur & 0xffffu);
+          const float* r = rec + (h ? cur.y : cur.x);
           const ulonglong2 sxv = *reinterpret_cast<const ulonglong2*>(r + ox);
           float syz = r[oy];
           if (RANK == 3) syz += r[oz];
