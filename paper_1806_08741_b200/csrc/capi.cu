@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -214,7 +215,8 @@ __global__ void k_patch_labels_host(int64_t n, const uint32_t* before, const uin
 // reserves its tile's entries with one atomic; entries past `cap` are
 // counted but not written (the caller then copies the whole map).
 __global__ void k_change_list(int64_t n, const uint32_t* before, const uint32_t* after,
-                              unsigned long long* count, int64_t cap, uint2* out) {
+                              unsigned long long* count, int64_t cap, uint2* out,
+                              uint32_t idx0 = 0) {
   constexpr int kPer = 16;
   __shared__ unsigned long long base;
   __shared__ int warp_tot[8];
@@ -254,11 +256,17 @@ __global__ void k_change_list(int64_t n, const uint32_t* before, const uint32_t*
 #pragma unroll
     for (int j = 0; j < kPer; ++j)
       if (chg >> j & 1u) {
-        if (pos < cap) out[pos] = make_uint2((uint32_t)(tile + j * 256 + tid), val[j]);
+        if (pos < cap) out[pos] = make_uint2(idx0 + (uint32_t)(tile + j * 256 + tid), val[j]);
         ++pos;
       }
     __syncthreads();  // warp_tot / base reuse
   }
+}
+
+// The per-piece list counts into mapped host memory (read by the host as
+// soon as the lists are built, without queueing behind the snapshot DMA).
+__global__ void k_copy_counts(const unsigned long long* cnt, int k, unsigned long long* host_cnt) {
+  if ((int)threadIdx.x < k) host_cnt[threadIdx.x] = cnt[threadIdx.x];
 }
 
 // Page-locked, device-mapped host staging kept across calls (grown on demand).
@@ -298,6 +306,40 @@ void apply_change_list(uint32_t* labels, const uint2* list, int64_t cnt) {
     });
   for (auto& x : th) x.join();
 }
+
+// Host threads applying per-chunk change lists as the chunks become ready
+// (the main thread calls ready(c) once chunk c's snapshot copy and list have
+// landed); chunks touch disjoint label ranges, so they may overlap.
+struct ChunkApplier {
+  uint32_t* labels;
+  std::vector<const uint2*> lists;
+  std::vector<int64_t> counts;
+  std::atomic<int> n_ready{0};
+  std::vector<std::thread> th;
+  ChunkApplier(uint32_t* l, int chunks) : labels(l), lists(chunks), counts(chunks, 0) {}
+  void start() {
+    int t = (int)std::thread::hardware_concurrency();
+    t = t < 1 ? 1 : (t > 32 ? 32 : t);
+    const int K = (int)lists.size();
+    for (int w = 0; w < t; ++w)
+      th.emplace_back([this, w, t, K] {
+        for (int c = 0; c < K; ++c) {
+          while (n_ready.load(std::memory_order_acquire) <= c) std::this_thread::yield();
+          const uint2* list = lists[c];
+          const int64_t cnt = counts[c], a = cnt * w / t, b = cnt * (w + 1) / t;
+          for (int64_t i = a; i < b; ++i) {
+            if (i + 32 < b) __builtin_prefetch(labels + list[i + 32].x, 1, 0);
+            labels[list[i].x] = list[i].y;
+          }
+        }
+      });
+  }
+  void ready(int c) { n_ready.store(c + 1, std::memory_order_release); }
+  void join() {
+    for (auto& x : th) x.join();
+    th.clear();
+  }
+};
 
 // SSLIC_TIMING: device-event marks on the streams (no host syncs in between)
 struct EventMarks {
@@ -407,18 +449,19 @@ int run_loop_overlapped(Engine& e, Stream& st, uint32_t* labels_out, int64_t n,
   DeviceBuf snapbuf(n * sizeof(uint32_t), st.s);
   e.unpack_labels(snapbuf.as<uint32_t>());
   em.mark(st.s, "snap");
+  // The snapshot goes down in kPieces pieces on the DMA engine, submitted by
+  // the host two at a time, so that the change lists (built on the device
+  // after the last iteration) jump the queue as soon as they exist. Host
+  // threads apply each piece's list once that piece and the lists have
+  // landed, overlapping the remaining pieces' copies.
+  constexpr int kPieces = 32, kInFlight = 2;
+  const bool listed = n < ((int64_t)1 << 32);
   cudaEvent_t ready;
   SSLIC_CUDA_CHECK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
   SSLIC_CUDA_CHECK(cudaEventRecord(ready, st.s));
   cudaStream_t cs = nullptr;
   SSLIC_CUDA_CHECK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
   SSLIC_CUDA_CHECK(cudaStreamWaitEvent(cs, ready, 0));
-  SSLIC_CUDA_CHECK(cudaMemcpyAsync(labels_out, snapbuf.p, n * sizeof(uint32_t),
-                                   cudaMemcpyDeviceToHost, cs));
-  cudaEvent_t copied;
-  SSLIC_CUDA_CHECK(cudaEventCreateWithFlags(&copied, cudaEventDisableTiming));
-  SSLIC_CUDA_CHECK(cudaEventRecord(copied, cs));
-  em.mark(cs, "copied");
   for (int it = std::max(snap, e.iterations_done()); it < iters; ++it) {
     e.assign(true);
     e.update();
@@ -427,49 +470,123 @@ int run_loop_overlapped(Engine& e, Stream& st, uint32_t* labels_out, int64_t n,
   DeviceBuf fin(n * sizeof(uint32_t), st.s);
   e.unpack_labels(fin.as<uint32_t>());
   em.mark(st.s, "unpack");
-  if (n < ((int64_t)1 << 32)) {
-    // change list in device memory (up to 5% of the map; more -> whole-map
-    // copy), DMA'd into pinned staging behind the snapshot, applied on the host
-    const int64_t cap = n / 20 + 1024;
-    DeviceBuf dlist((size_t)cap * sizeof(uint2), st.s);
-    DeviceBuf cntb(sizeof(unsigned long long), st.s);
-    SSLIC_CUDA_CHECK(cudaMemsetAsync(cntb.p, 0, sizeof(unsigned long long), st.s));
-    k_change_list<<<148 * 8, 256, 0, st.s>>>(n, snapbuf.as<uint32_t>(), fin.as<uint32_t>(),
-                                              cntb.as<unsigned long long>(), cap,
-                                              dlist.as<uint2>());
-    SSLIC_CUDA_CHECK(cudaGetLastError());
-    unsigned long long cnt = 0;
-    SSLIC_CUDA_CHECK(cudaMemcpyAsync(&cnt, cntb.p, sizeof(cnt), cudaMemcpyDeviceToHost, st.s));
-    em.mark(st.s, "list");
-    st.sync();
-    if ((int64_t)cnt <= cap) {
-      MappedStage& ms = mapped_stage();
-      std::lock_guard<std::mutex> lock(ms.mu);
-      uint2* list = static_cast<uint2*>(ms.get((size_t)cap * sizeof(uint2)));
-      SSLIC_CUDA_CHECK(cudaMemcpyAsync(list, dlist.p, cnt * sizeof(uint2),
-                                       cudaMemcpyDeviceToHost, cs));  // after the snapshot
-      em.mark(cs, "list-d2h");
-      SSLIC_CUDA_CHECK(cudaStreamSynchronize(cs));
-      apply_change_list(labels_out, list, (int64_t)cnt);
-    } else {
-      SSLIC_CUDA_CHECK(cudaStreamSynchronize(cs));
-      SSLIC_CUDA_CHECK(cudaMemcpyAsync(labels_out, fin.p, n * sizeof(uint32_t),
-                                       cudaMemcpyDeviceToHost, st.s));
-      st.sync();
-    }
-    if (em.on) std::fprintf(stderr, "[sslic] change list: %llu entries (%.2f%% of the map)\n",
-                            cnt, 100.0 * (double)cnt / (double)n);
-  } else {
-    SSLIC_CUDA_CHECK(cudaStreamWaitEvent(st.s, copied, 0));  // snapshot landed first
+  if (!listed) {  // >= 2^32 voxels: snapshot, then the changed labels via the mapped map
+    cudaEvent_t copied;
+    SSLIC_CUDA_CHECK(cudaEventCreateWithFlags(&copied, cudaEventDisableTiming));
+    SSLIC_CUDA_CHECK(cudaMemcpyAsync(labels_out, snapbuf.p, n * sizeof(uint32_t),
+                                     cudaMemcpyDeviceToHost, cs));
+    SSLIC_CUDA_CHECK(cudaEventRecord(copied, cs));
+    SSLIC_CUDA_CHECK(cudaStreamWaitEvent(st.s, copied, 0));
     k_patch_labels_host<<<148 * 8, 256, 0, st.s>>>(n, snapbuf.as<uint32_t>(),
                                                     fin.as<uint32_t>(), labels_out);
     SSLIC_CUDA_CHECK(cudaGetLastError());
-    em.mark(st.s, "patched");
     st.sync();
+    cudaStreamDestroy(cs);
+    cudaEventDestroy(ready);
+    cudaEventDestroy(copied);
+    if (e.undefined_seen())
+      throw Error(SSLIC_ELOGIC, "accumulate_region: pixel with undefined label");
+    return e.iterations_done();
   }
+  const int K = kPieces;
+  std::vector<int64_t> c0(K + 1), cap(K), off(K, 0);
+  for (int c = 0; c <= K; ++c) c0[c] = n * c / K;
+  int64_t total_cap = 0;
+  for (int c = 0; c < K; ++c) {
+    cap[c] = (c0[c + 1] - c0[c]) / 20 + 1024;  // up to 5% (more -> the piece is copied whole)
+    off[c] = total_cap;
+    total_cap += cap[c];
+  }
+  DeviceBuf dlist((size_t)total_cap * sizeof(uint2), st.s);
+  DeviceBuf cntb(K * sizeof(unsigned long long), st.s);
+  SSLIC_CUDA_CHECK(cudaMemsetAsync(cntb.p, 0, K * sizeof(unsigned long long), st.s));
+  for (int c = 0; c < K; ++c) {
+    k_change_list<<<148 * 2, 256, 0, st.s>>>(
+        c0[c + 1] - c0[c], snapbuf.as<uint32_t>() + c0[c], fin.as<uint32_t>() + c0[c],
+        cntb.as<unsigned long long>() + c, cap[c], dlist.as<uint2>() + off[c], (uint32_t)c0[c]);
+    SSLIC_CUDA_CHECK(cudaGetLastError());
+  }
+  MappedStage& ms = mapped_stage();
+  std::lock_guard<std::mutex> lock(ms.mu);
+  char* stage = static_cast<char*>(ms.get((size_t)total_cap * sizeof(uint2) + 64 * 8));
+  auto* cnt_h = reinterpret_cast<unsigned long long*>(stage);
+  uint2* list_h = reinterpret_cast<uint2*>(stage + 64 * 8);
+  k_copy_counts<<<1, 32, 0, st.s>>>(cntb.as<unsigned long long>(), K, cnt_h);
+  SSLIC_CUDA_CHECK(cudaGetLastError());
+  cudaEvent_t built, lists_in;
+  SSLIC_CUDA_CHECK(cudaEventCreateWithFlags(&built, cudaEventDisableTiming));
+  SSLIC_CUDA_CHECK(cudaEventCreateWithFlags(&lists_in, cudaEventDisableTiming));
+  SSLIC_CUDA_CHECK(cudaEventRecord(built, st.s));
+  em.mark(st.s, "lists");
+  std::vector<cudaEvent_t> copied(K);
+  for (auto& x : copied) SSLIC_CUDA_CHECK(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+  ChunkApplier ap(labels_out, K);
+  for (int c = 0; c < K; ++c) ap.lists[c] = list_h + off[c];
+  ap.start();
+  std::vector<char> whole(K, 0);
+  bool lists_sent = false;
+  unsigned long long total = 0;
+  auto send_lists = [&]() {  // counts are in host memory once `built` completed
+    for (int c = 0; c < K; ++c) {
+      total += cnt_h[c];
+      if ((int64_t)cnt_h[c] <= cap[c]) {
+        ap.counts[c] = (int64_t)cnt_h[c];
+        if (cnt_h[c])
+          SSLIC_CUDA_CHECK(cudaMemcpyAsync(list_h + off[c], dlist.as<uint2>() + off[c],
+                                           cnt_h[c] * sizeof(uint2), cudaMemcpyDeviceToHost,
+                                           cs));
+      } else {
+        whole[c] = 1;
+      }
+    }
+    SSLIC_CUDA_CHECK(cudaEventRecord(lists_in, cs));
+    em.mark(cs, "lists-d2h");
+    lists_sent = true;
+  };
+  SSLIC_CUDA_CHECK(cudaEventSynchronize(ready));  // the snapshot exists
+  int submitted = 0, landed = 0, applied = 0;
+  while (applied < K) {
+    while (submitted < K && submitted - landed < kInFlight) {
+      const int c = submitted++;
+      SSLIC_CUDA_CHECK(cudaMemcpyAsync(labels_out + c0[c], snapbuf.as<uint32_t>() + c0[c],
+                                       (c0[c + 1] - c0[c]) * sizeof(uint32_t),
+                                       cudaMemcpyDeviceToHost, cs));
+      SSLIC_CUDA_CHECK(cudaEventRecord(copied[c], cs));
+    }
+    if (!lists_sent && cudaEventQuery(built) == cudaSuccess) send_lists();
+    if (landed < submitted) {
+      SSLIC_CUDA_CHECK(cudaEventSynchronize(copied[landed]));
+      ++landed;
+    }
+    if (lists_sent && landed > applied && cudaEventQuery(lists_in) == cudaSuccess) {
+      while (applied < landed) ap.ready(applied++);
+    } else if (landed == K) {
+      if (!lists_sent) {
+        SSLIC_CUDA_CHECK(cudaEventSynchronize(built));
+        send_lists();
+      }
+      SSLIC_CUDA_CHECK(cudaEventSynchronize(lists_in));
+    }
+  }
+  ap.join();
+  bool any_whole = false;
+  for (int c = 0; c < K; ++c)
+    if (whole[c]) {  // too many changes in this piece: its final labels, whole
+      any_whole = true;
+      SSLIC_CUDA_CHECK(cudaMemcpyAsync(labels_out + c0[c], fin.as<uint32_t>() + c0[c],
+                                       (c0[c + 1] - c0[c]) * sizeof(uint32_t),
+                                       cudaMemcpyDeviceToHost, cs));
+    }
+  SSLIC_CUDA_CHECK(cudaStreamSynchronize(cs));
+  st.sync();
+  if (em.on)
+    std::fprintf(stderr, "[sslic] change lists: %llu entries (%.2f%% of the map)%s\n", total,
+                 100.0 * (double)total / (double)n, any_whole ? ", some pieces copied whole" : "");
   cudaStreamDestroy(cs);
   cudaEventDestroy(ready);
-  cudaEventDestroy(copied);
+  cudaEventDestroy(built);
+  cudaEventDestroy(lists_in);
+  for (auto& x : copied) cudaEventDestroy(x);
   if (e.undefined_seen())
     throw Error(SSLIC_ELOGIC, "accumulate_region: pixel with undefined label");
   return e.iterations_done();
