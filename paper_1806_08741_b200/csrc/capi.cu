@@ -315,8 +315,14 @@ struct ChunkApplier {
   std::vector<const uint2*> lists;
   std::vector<int64_t> counts;
   std::atomic<int> n_ready{0};
+  std::atomic<bool> cancel{false};
   std::vector<std::thread> th;
   ChunkApplier(uint32_t* l, int chunks) : labels(l), lists(chunks), counts(chunks, 0) {}
+  // an exception between start() and join() must not leave joinable threads
+  ~ChunkApplier() {
+    cancel.store(true, std::memory_order_release);
+    join();
+  }
   void start() {
     int t = (int)std::thread::hardware_concurrency();
     t = t < 1 ? 1 : (t > 32 ? 32 : t);
@@ -324,7 +330,10 @@ struct ChunkApplier {
     for (int w = 0; w < t; ++w)
       th.emplace_back([this, w, t, K] {
         for (int c = 0; c < K; ++c) {
-          while (n_ready.load(std::memory_order_acquire) <= c) std::this_thread::yield();
+          while (n_ready.load(std::memory_order_acquire) <= c) {
+            if (cancel.load(std::memory_order_acquire)) return;
+            std::this_thread::yield();
+          }
           const uint2* list = lists[c];
           const int64_t cnt = counts[c], a = cnt * w / t, b = cnt * (w + 1) / t;
           for (int64_t i = a; i < b; ++i) {
