@@ -350,6 +350,29 @@ struct ChunkApplier {
   }
 };
 
+// Owned non-blocking stream / timing-free event (released on every exit path).
+struct OwnedStream {
+  cudaStream_t s = nullptr;
+  OwnedStream() { SSLIC_CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)); }
+  ~OwnedStream() {
+    if (s) {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
+  }
+  OwnedStream(const OwnedStream&) = delete;
+  OwnedStream& operator=(const OwnedStream&) = delete;
+};
+struct OwnedEvent {
+  cudaEvent_t e = nullptr;
+  OwnedEvent() { SSLIC_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming)); }
+  ~OwnedEvent() {
+    if (e) cudaEventDestroy(e);
+  }
+  OwnedEvent(const OwnedEvent&) = delete;
+  OwnedEvent& operator=(const OwnedEvent&) = delete;
+};
+
 // SSLIC_TIMING: device-event marks on the streams (no host syncs in between)
 struct EventMarks {
   bool on = std::getenv("SSLIC_TIMING") != nullptr;
@@ -391,10 +414,11 @@ void pipelined_start(Engine& e, const sslic_image* img, void* dev, Stream& st, E
   const int64_t S = e.geom().grid[2], cells = e.geom().cells[2];
   const int64_t RZ = e.region_z(), rows = e.region_rows();
   constexpr int kChunks = 8;
-  cudaStream_t cs = nullptr;
-  SSLIC_CUDA_CHECK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  OwnedStream copy_stream;
+  const cudaStream_t cs = copy_stream.s;
+  OwnedEvent evs[kChunks + 1];
   cudaEvent_t ev[kChunks + 1];
-  for (auto& x : ev) SSLIC_CUDA_CHECK(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+  for (int i = 0; i <= kChunks; ++i) ev[i] = evs[i].e;
   SSLIC_CUDA_CHECK(cudaEventRecord(ev[kChunks], st.s));  // the device buffer exists
   SSLIC_CUDA_CHECK(cudaStreamWaitEvent(cs, ev[kChunks], 0));
   e.init_pipeline();
@@ -430,8 +454,6 @@ void pipelined_start(Engine& e, const sslic_image* img, void* dev, Stream& st, E
   e.update();
   em.mark(st.s, "it0");
   SSLIC_CUDA_CHECK(cudaStreamSynchronize(cs));
-  cudaStreamDestroy(cs);
-  for (auto& x : ev) cudaEventDestroy(x);
 }
 
 int run_loop_overlapped(Engine& e, Stream& st, uint32_t* labels_out, int64_t n,
@@ -465,11 +487,11 @@ int run_loop_overlapped(Engine& e, Stream& st, uint32_t* labels_out, int64_t n,
   // landed, overlapping the remaining pieces' copies.
   constexpr int kPieces = 32, kInFlight = 2;
   const bool listed = n < ((int64_t)1 << 32);
-  cudaEvent_t ready;
-  SSLIC_CUDA_CHECK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  OwnedEvent ready_ev;
+  const cudaEvent_t ready = ready_ev.e;
   SSLIC_CUDA_CHECK(cudaEventRecord(ready, st.s));
-  cudaStream_t cs = nullptr;
-  SSLIC_CUDA_CHECK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  OwnedStream copy_stream;
+  const cudaStream_t cs = copy_stream.s;
   SSLIC_CUDA_CHECK(cudaStreamWaitEvent(cs, ready, 0));
   for (int it = std::max(snap, e.iterations_done()); it < iters; ++it) {
     e.assign(true);
@@ -480,8 +502,8 @@ int run_loop_overlapped(Engine& e, Stream& st, uint32_t* labels_out, int64_t n,
   e.unpack_labels(fin.as<uint32_t>());
   em.mark(st.s, "unpack");
   if (!listed) {  // >= 2^32 voxels: snapshot, then the changed labels via the mapped map
-    cudaEvent_t copied;
-    SSLIC_CUDA_CHECK(cudaEventCreateWithFlags(&copied, cudaEventDisableTiming));
+    OwnedEvent copied_ev;
+    const cudaEvent_t copied = copied_ev.e;
     SSLIC_CUDA_CHECK(cudaMemcpyAsync(labels_out, snapbuf.p, n * sizeof(uint32_t),
                                      cudaMemcpyDeviceToHost, cs));
     SSLIC_CUDA_CHECK(cudaEventRecord(copied, cs));
@@ -490,9 +512,6 @@ int run_loop_overlapped(Engine& e, Stream& st, uint32_t* labels_out, int64_t n,
                                                     fin.as<uint32_t>(), labels_out);
     SSLIC_CUDA_CHECK(cudaGetLastError());
     st.sync();
-    cudaStreamDestroy(cs);
-    cudaEventDestroy(ready);
-    cudaEventDestroy(copied);
     if (e.undefined_seen())
       throw Error(SSLIC_ELOGIC, "accumulate_region: pixel with undefined label");
     return e.iterations_done();
@@ -522,13 +541,13 @@ int run_loop_overlapped(Engine& e, Stream& st, uint32_t* labels_out, int64_t n,
   uint2* list_h = reinterpret_cast<uint2*>(stage + 64 * 8);
   k_copy_counts<<<1, 32, 0, st.s>>>(cntb.as<unsigned long long>(), K, cnt_h);
   SSLIC_CUDA_CHECK(cudaGetLastError());
-  cudaEvent_t built, lists_in;
-  SSLIC_CUDA_CHECK(cudaEventCreateWithFlags(&built, cudaEventDisableTiming));
-  SSLIC_CUDA_CHECK(cudaEventCreateWithFlags(&lists_in, cudaEventDisableTiming));
+  OwnedEvent built_ev, lists_in_ev;
+  const cudaEvent_t built = built_ev.e, lists_in = lists_in_ev.e;
   SSLIC_CUDA_CHECK(cudaEventRecord(built, st.s));
   em.mark(st.s, "lists");
+  std::vector<OwnedEvent> copied_evs(K);
   std::vector<cudaEvent_t> copied(K);
-  for (auto& x : copied) SSLIC_CUDA_CHECK(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+  for (int c = 0; c < K; ++c) copied[c] = copied_evs[c].e;
   ChunkApplier ap(labels_out, K);
   for (int c = 0; c < K; ++c) ap.lists[c] = list_h + off[c];
   ap.start();
@@ -591,11 +610,6 @@ int run_loop_overlapped(Engine& e, Stream& st, uint32_t* labels_out, int64_t n,
   if (em.on)
     std::fprintf(stderr, "[sslic] change lists: %llu entries (%.2f%% of the map)%s\n", total,
                  100.0 * (double)total / (double)n, any_whole ? ", some pieces copied whole" : "");
-  cudaStreamDestroy(cs);
-  cudaEventDestroy(ready);
-  cudaEventDestroy(built);
-  cudaEventDestroy(lists_in);
-  for (auto& x : copied) cudaEventDestroy(x);
   if (e.undefined_seen())
     throw Error(SSLIC_ELOGIC, "accumulate_region: pixel with undefined label");
   return e.iterations_done();
