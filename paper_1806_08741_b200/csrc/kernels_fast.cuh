@@ -73,9 +73,21 @@ struct FastParams {
   int max_cand;       // regions with more candidates take the exact crowded path
 };
 
+#ifndef SSLIC_BOX3_X  // (build-time override for layout experiments)
+#define SSLIC_BOX3_X 8
+#define SSLIC_BOX3_Y 4
+#define SSLIC_BOX3_Z 4
+#endif
 template <int RANK>
-struct BoxShape {
-  static constexpr int X = 8, Y = RANK == 3 ? 4 : 16, Z = RANK == 3 ? 4 : 1;
+struct BoxShape;
+template <>
+struct BoxShape<2> {
+  static constexpr int X = 8, Y = 16, Z = 1;
+};
+template <>
+struct BoxShape<3> {
+  static constexpr int X = SSLIC_BOX3_X, Y = SSLIC_BOX3_Y, Z = SSLIC_BOX3_Z;
+  static_assert(X * Y * Z == 128 && X % 4 == 0, "a warp box is 32 lanes x 4 voxels along x");
 };
 
 struct alignas(16) FastSmem {

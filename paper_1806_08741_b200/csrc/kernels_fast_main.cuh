@@ -239,9 +239,11 @@ __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fas
   const int nbx = (RX + Box::X - 1) / Box::X, nby = (RY + Box::Y - 1) / Box::Y;
   const int nbz = RANK == 3 ? (RZ + Box::Z - 1) / Box::Z : 1;
   const int nbox = nbx * nby * nbz;
-  const int xq = lane & 1;
-  const int yq = RANK == 3 ? (lane >> 1) & 3 : lane >> 1;
-  const int zq = RANK == 3 ? lane >> 3 : 0;
+  // lane -> (x run, y, z) inside the box: Box::X / 4 runs of 4 voxels along x
+  constexpr int kXL = Box::X / 4;
+  const int xq = lane % kXL;
+  const int yq = RANK == 3 ? (lane / kXL) % Box::Y : lane / kXL;
+  const int zq = RANK == 3 ? lane / (kXL * Box::Y) : 0;
   const float M = P.margin;
   const float A = P.abs_margin;
   const float fscale = ldexpf(1.0f, P.shift);
