@@ -113,9 +113,14 @@ constexpr int kSlotHash = 2 * kFastMaxCand;
 constexpr int kRegionCandStride = kFastMaxCand + 1;  // [count, ids...] per region
 // float2 entries per hi/lo history row, padded to a 16-byte multiple
 __host__ __device__ constexpr int hist32_stride(int stride) { return (stride + 1) & ~1; }
-// up to this many delta contributions per warp box, lanes add their own
-// contributions directly (sparse path); above it, warp-aggregate per label
-constexpr unsigned kSparseDeltas = 24;
+// Up to this many delta contributions per warp box, lanes add their own
+// contributions (per-lane path); above it, a box dominated by one label is
+// warp-aggregated per label. Measured per channel count: with native 32-bit
+// shared atomics, 128 is faster for 1 and 4 channels (config 3 iteration 0
+// 16.9 -> 16.6 ms, config 4 4.46 -> 4.15 ms), while the RGB configs, whose
+// iteration 0 has many one-label boxes, keep 24 (config 2 iteration 0:
+// 0.17 ms at 24, 0.41 ms at 128; config 5: 355 vs 372 ms).
+__host__ __device__ constexpr unsigned sparse_deltas(int C) { return C == 3 ? 24u : 128u; }
 __device__ __forceinline__ int slot_hash(uint32_t id) { return (int)((id * 0x9E3779B1u) >> 25); }
 // Slot of cluster `id` in the region's candidate list, -1 if absent.
 __device__ __forceinline__ int slot_of(const FastSmem& sm, uint32_t id) {

@@ -832,7 +832,7 @@ __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fas
     // by one label (uniform regions) is warp-aggregated per label instead.
     const unsigned npend = __reduce_add_sync(0xffffffffu, (unsigned)__popc(pending));
     if (npend != 0) {  // uniform: most boxes have no change after the first iterations
-    bool per_lane = npend <= kSparseDeltas;
+    bool per_lane = npend <= sparse_deltas(C);
     if (!per_lane) {
       const int fb = pending ? __ffs(pending) - 1 : 0;
       const uint32_t first = sel8(newl, oldl, fb);
