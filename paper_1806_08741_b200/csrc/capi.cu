@@ -290,22 +290,6 @@ MappedStage& mapped_stage() {
   return *s;
 }
 
-// Apply (index, label) pairs to the host map with the host's threads.
-void apply_change_list(uint32_t* labels, const uint2* list, int64_t cnt) {
-  int t = (int)std::thread::hardware_concurrency();
-  t = t < 1 ? 1 : (t > 32 ? 32 : t);
-  if (cnt < ((int64_t)1 << 16)) t = 1;
-  std::vector<std::thread> th;
-  for (int w = 0; w < t; ++w)
-    th.emplace_back([=] {
-      const int64_t a = cnt * w / t, b = cnt * (w + 1) / t;
-      for (int64_t i = a; i < b; ++i) {
-        if (i + 32 < b) __builtin_prefetch(labels + list[i + 32].x, 1, 0);
-        labels[list[i].x] = list[i].y;
-      }
-    });
-  for (auto& x : th) x.join();
-}
 
 // Host threads applying per-chunk change lists as the chunks become ready
 // (the main thread calls ready(c) once chunk c's snapshot copy and list have
