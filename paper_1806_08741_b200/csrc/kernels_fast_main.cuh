@@ -172,7 +172,7 @@ __host__ __device__ constexpr int fast_queue_cap(int C) { return C == 3 ? 32 : 0
 // T is the caller's storage type; T = double sweeps an f32 working copy (TW)
 // with the pixel rounding folded into the margins, and takes the exact f64
 // values for the re-decisions and the fixed-point deltas.
-template <int RANK, int C, typename TS, int RXc, int RYc, int RZc>
+template <int RANK, int C, typename TS, int RXc, int RYc, int RZc, int CAPc = 0>
 __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fast(const __grid_constant__ FastParams P) {
   constexpr bool kF64 = std::is_same<TS, double>::value;
   using T = typename std::conditional<kF64, float, TS>::type;  // working pixel type
@@ -207,9 +207,11 @@ __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fas
   constexpr int kQCap = fast_queue_cap(C);
   using AccT = int;
   constexpr int kCompA = kComp + C;
-  AccT* accs = reinterpret_cast<AccT*>(rec + (size_t)(kFastMaxCand + 1) * RS);
+  // candidate capacity of the record/slot arrays (P.max_cand <= kCap)
+  constexpr int kCap = CAPc ? CAPc : kFastMaxCand;
+  AccT* accs = reinterpret_cast<AccT*>(rec + (size_t)(kCap + 1) * RS);
   // per-warp staging of the carried-over centres: [warp][v][lane][kS2] float2
-  float2* stage = reinterpret_cast<float2*>(accs + kFastMaxCand * kCompA);
+  float2* stage = reinterpret_cast<float2*>(accs + kCap * kCompA);
   // next-box prefetch: label words [warp][2][lane] (16 B), pixel runs [warp][2][lane][kPW]
   uint4* pf_words = reinterpret_cast<uint4*>(stage + kWarps * 4 * kS2 * 32);
   uint32_t* pf_pix = reinterpret_cast<uint32_t*>(pf_words + kWarps * 2 * 32);
@@ -387,7 +389,7 @@ __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fas
     }
   }
   // (slot block: 64 * kCompA words, a multiple of 16 bytes)
-  for (int i = tid; i < kFastMaxCand * kCompA / 4; i += kFastThreads)
+  for (int i = tid; i < kCap * kCompA / 4; i += kFastThreads)
     reinterpret_cast<int4*>(accs)[i] = make_int4(0, 0, 0, 0);
   for (int i = tid; i < kSlotHash; i += kFastThreads) sm.htab[i] = 0xffff;
   // compaction lists start as valid record offsets: a voxel without any kept
@@ -1379,15 +1381,23 @@ inline bool fast_path_supported(const Geom& g) {
 }
 
 
-inline size_t fast_smem_bytes(const Geom& g, const int* R) {
+// Candidate capacity a region's CTA needs: 1.5x the anchor cells it draws
+// from (prod (R_a / S_a + 2)), rounded up to 4.
+inline int fast_cand_need(const Geom& g, const int* R) {
+  int cells = 1;
+  for (int a = 0; a < g.rank; ++a) cells *= R[a] / g.grid[a] + 2;
+  return (cells + cells / 2 + 3) & ~3;
+}
+
+inline size_t fast_smem_bytes(const Geom& g, const int* R, int cap = kFastMaxCand) {
   const int RXp = (R[0] + 3) & ~3;
   const int HO = (RXp + R[1] + (g.rank == 3 ? R[2] : 0) + 1) & ~1;
   const int RS = (HO + 2 * g.channels + 2 + 3) & ~3;
   const int warps = kFastThreads / 32;
   size_t b = sizeof(FastSmem);
-  b += (size_t)(kFastMaxCand + 1) * RS * sizeof(float);
+  b += (size_t)(cap + 1) * RS * sizeof(float);
   // CTA delta slots (see k_assign_fast): 32-bit words, C extra per candidate
-  b += (size_t)kFastMaxCand * (g.stride + 1 + g.channels) * sizeof(int);
+  b += (size_t)cap * (g.stride + 1 + g.channels) * sizeof(int);
   b += (size_t)warps * 4 * hist32_stride(g.stride) * 32 * sizeof(float2);
   b += (size_t)warps * 2 * 32 * 16;  // next-box label words
   const int wsize = g.dtype == SSLIC_F64 ? 4 : dtype_size(g.dtype);  // working pixel size
@@ -1396,9 +1406,9 @@ inline size_t fast_smem_bytes(const Geom& g, const int* R) {
   return b;
 }
 
-template <int RANK, int C, typename T, int RXc, int RYc, int RZc>
+template <int RANK, int C, typename T, int RXc, int RYc, int RZc, int CAPc = 0>
 void launch_fast_shape(const FastParams& P, size_t smem, int64_t nblocks, cudaStream_t s) {
-  auto kern = k_assign_fast<RANK, C, T, RXc, RYc, RZc>;
+  auto kern = k_assign_fast<RANK, C, T, RXc, RYc, RZc, CAPc>;
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -1424,8 +1434,17 @@ void launch_fast_t(const FastParams& P, size_t smem, int64_t nblocks, cudaStream
       return launch_fast_shape<RANK, C, T, 16, 16, 8>(P, smem, nblocks, s);  // config 4
   }
   if constexpr (RANK == 3 && C == 3 && sizeof(T) == 1) {
-    if (R[0] == 32 && R[1] == 32 && R[2] == 32)
-      return launch_fast_shape<RANK, C, T, 32, 32, 32>(P, smem, nblocks, s);  // config 5
+    if (R[0] == 32 && R[1] == 32 && R[2] == 32) {  // config 5
+      // 32^3 regions of one cell (S = 32) draw from 27 anchor cells: a
+      // capacity of 40 records instead of 64 lets 4 CTAs share an SM, not 3
+      if (fast_cand_need(P.g, R) <= 40) {
+        FastParams Q = P;
+        if (Q.max_cand > 40) Q.max_cand = 40;
+        return launch_fast_shape<RANK, C, T, 32, 32, 32, 40>(Q, fast_smem_bytes(P.g, R, 40),
+                                                            nblocks, s);
+      }
+      return launch_fast_shape<RANK, C, T, 32, 32, 32>(P, smem, nblocks, s);
+    }
   }
   if constexpr (RANK == 2 && C == 3 && sizeof(T) == 4) {
     if (R[0] == 64 && R[1] == 32)
