@@ -8,7 +8,7 @@ SSLIC_TIMING=1 python bench.py > gpurun_out/${T}_bench_c3.log 2> gpurun_out/${T}
 python bench.py --impl reference > gpurun_out/${T}_ref_c3.log 2>&1
 python bench.py --config 1 > gpurun_out/${T}_bench_c1.log 2>&1
 python bench.py --config 2 > gpurun_out/${T}_bench_c2.log 2>&1
-python bench.py --config 4 --no-e2e > gpurun_out/${T}_bench_c4.log 2>&1
+python bench.py --config 4 > gpurun_out/${T}_bench_c4.log 2>&1
 python bench.py --config 5 --steps 2 --warmup 3 --no-e2e > gpurun_out/${T}_bench_c5.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${T}_launches_c3.csv python bench.py --steps 7 --warmup 3 --no-e2e --no-cpu > gpurun_out/${T}_ncu_launches.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_assign_fast -s 9 -c 1 -o gpurun_out/${T}_assign_c3 python bench.py --steps 7 --warmup 3 --no-e2e --no-cpu > gpurun_out/${T}_ncu_c3.log 2>&1
