@@ -292,3 +292,69 @@ def test_crowded_regions_fallback_equals_exact(sslic, monkeypatch):
         assert int((la != lb).sum().item()) == 0, f"iteration {it}"
         assert np.array_equal(fast.centers(), exact.centers())
     assert crowded_seen > 0
+
+
+def _fuzz_cases(n=48, seed=20261020):
+    rng = np.random.default_rng(seed)
+    cases = []
+    for i in range(n):
+        rank = int(rng.integers(2, 4))
+        ch = int(rng.choice([1, 2, 3, 4]))
+        dtype = [np.uint8, np.uint16, np.float32][int(rng.integers(0, 3))]
+        if rank == 2:
+            dims = (int(rng.integers(20, 300)), int(rng.integers(20, 300)))
+        else:
+            dims = tuple(int(x) for x in rng.integers(12, 90, size=3))
+        grid = tuple(int(rng.integers(3, min(d, 24) + 1)) for d in dims)
+        m = float(rng.choice([1.0, 5.0, 10.0, 20.0, 40.0]))
+        iters = int(rng.integers(2, 6))
+        cfg = {1: 3, 2: 3, 3: 5, 4: 4}[ch] if rank == 3 else (1 if dtype != np.float32 else 2)
+        cases.append((cfg, dims, ch, dtype, grid, m, iters))
+    return cases
+
+
+@pytest.mark.parametrize("case", _fuzz_cases(), ids=lambda c: f"r{len(c[1])}c{c[2]}-"
+                         f"{np.dtype(c[3]).name}-{'x'.join(map(str, c[1]))}-S{'x'.join(map(str, c[4]))}")
+def test_fast_equals_exact_fuzz(sslic, case):
+    """Seeded random geometries (odd extents, grid sizes that do not divide
+    the dims, 1-4 channels, u8/u16/f32, rank 2 and 3): the fast kernel (all
+    its paths: runtime-shape regions, clipped boxes, batched/inline fp64
+    re-decisions, per-lane/aggregated deltas) equals the exact fp64 kernel
+    bit for bit at every iteration."""
+    import torch
+    cfg, dims, ch, dtype, grid, m, iters = case
+    n = int(np.prod(dims))
+    tdt = {np.uint8: torch.uint8, np.uint16: torch.int16, np.float32: torch.float32}[dtype]
+    # blocky piecewise-constant channels + noise (host numpy, seeded per case)
+    rng = np.random.default_rng(abs(hash((dims, ch, grid))) % (1 << 32))
+    hi = {np.uint8: 255.0, np.uint16: 65535.0, np.float32: 1.0}[dtype]
+    coarse = [max(1, d // 9) for d in dims]
+    base = rng.uniform(0, hi, size=tuple(reversed(coarse)) + (ch,))
+    idx = np.ix_(*[np.minimum(np.arange(d) // max(1, d // c), c - 1)
+                   for d, c in zip(reversed(dims), reversed(coarse))])
+    vol = base[idx] + rng.normal(0, 0.06 * hi, size=tuple(reversed(dims)) + (ch,))
+    vol = np.clip(vol, 0, hi)
+    host = (np.rint(vol) if dtype != np.float32 else vol).astype(dtype).reshape(-1)
+    img = torch.from_numpy(host.view(np.int16) if dtype == np.uint16 else host).cuda()
+    assert img.dtype == tdt and img.numel() == n * ch
+    torch.cuda.synchronize()
+    p = sslic.SlicParams(grid=list(grid), weight_m=m, max_iterations=iters)
+    fast = sslic.Engine(dims, ch, dtype, img.data_ptr(), p)
+    exact = sslic.Engine(dims, ch, dtype, img.data_ptr(), p)
+    exact.set_exact(True)
+    la = torch.empty(n, dtype=torch.int32, device="cuda")
+    lb = torch.empty(n, dtype=torch.int32, device="cuda")
+    for e in (fast, exact):
+        e.init()
+        e.commit()
+    for it in range(iters):
+        fast.assign()
+        exact.assign()
+        assert fast.undefined_count() == exact.undefined_count()
+        fast.update()
+        exact.update()
+        fast.labels_to(la.data_ptr())
+        exact.labels_to(lb.data_ptr())
+        torch.cuda.synchronize()
+        assert int((la != lb).sum().item()) == 0, f"iteration {it}: labels differ"
+        assert np.array_equal(fast.centers(), exact.centers()), f"iteration {it}: centres"
