@@ -258,3 +258,46 @@ def test_mask_label_contour_matches_oracle(sslic, oracle_lib):
         assert np.array_equal(np.asarray(ours.data, np.float64), ref)
     with pytest.raises(s.InvalidArgument):
         s.mask_label_contour(s.NDImage((2, 2), 1, np.zeros(4)), np.zeros(6, np.uint32), (3, 2))
+
+
+def _pipeline_fuzz(n=24, seed=18060874):
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(n):
+        rank = int(rng.integers(2, 4))
+        ch = int(rng.integers(1, 5))
+        dtype = [np.uint8, np.uint16][int(rng.integers(0, 2))]
+        dims = tuple(int(x) for x in rng.integers(24, 160 if rank == 2 else 48, size=rank))
+        grid = tuple(int(rng.integers(3, min(d, 16) + 1)) for d in dims)
+        m = float(rng.choice([2.0, 10.0, 30.0]))
+        iters = int(rng.integers(2, 6))
+        out.append((dims, ch, dtype, grid, m, iters, int(rng.integers(0, 1 << 30))))
+    return out
+
+
+@pytest.mark.parametrize("case", _pipeline_fuzz(), ids=lambda c: f"r{len(c[0])}c{c[1]}-"
+                         f"{np.dtype(c[2]).name}-{'x'.join(map(str, c[0]))}")
+def test_segment_matches_oracle_fuzz(sslic, oracle_lib, case):
+    """The whole product pipeline (sslic_segment: upload, init + perturb, the
+    iterations, connectivity) against the CPU oracle on seeded random
+    volumes: labels after connectivity and centres bit for bit, residuals at
+    rtol 1e-12."""
+    s = sslic
+    dims, ch, dtype, grid, m, iters, seed = case
+    rng = np.random.default_rng(seed)
+    hi = 255 if dtype == np.uint8 else 65535
+    n = int(np.prod(dims))
+    coarse = [max(1, d // 6) for d in dims]
+    base = rng.integers(0, hi + 1, size=tuple(reversed(coarse)) + (ch,))
+    idx = np.ix_(*[np.minimum(np.arange(d) // max(1, d // c), c - 1)
+                   for d, c in zip(reversed(dims), reversed(coarse))])
+    vol = base[idx] + rng.normal(0, 0.05 * hi, size=tuple(reversed(dims)) + (ch,))
+    data = np.clip(np.rint(vol), 0, hi).astype(dtype).reshape(-1)
+    p = s.SlicParams(grid=list(grid), weight_m=m, max_iterations=iters)
+    res, _ = s.segment(s.NDImage(dims, ch, data), p, device=0)
+    lab, cen, rs = oracle_lib.run_slic(data.astype(np.float64), dims, ch, list(grid), m,
+                                       max_iterations=iters)
+    assert np.array_equal(res.centers.data.reshape(-1), cen.reshape(-1)), "centres"
+    np.testing.assert_allclose(res.residuals, rs, rtol=RES_RTOL)
+    cc = oracle_lib.enforce_connectivity(dims, lab, cen, ch, list(grid))
+    assert np.array_equal(res.labels, cc), f"{int((res.labels != cc).sum())} labels differ"
