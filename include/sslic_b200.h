@@ -191,6 +191,15 @@ int64_t sslic_engine_launch_count(sslic_engine* e);
 /* Device time (ms, CUDA events on the engine stream) of the i-th assign
  * kernel launch since creation; *n_out = launches recorded. Synchronizes. */
 int sslic_engine_assign_ms(sslic_engine* e, int i, float* ms_out, int* n_out);
+/* Value range of the engine's data: max |value| over its planes for float
+ * images (the dtype maximum for u8/u16). Multi-GPU: set every rank's engine
+ * to the MAX over ranks (after create, before init) so that the fixed-point
+ * per-cluster sums that are allreduced share one scale and the fp32 filter
+ * margins cover centres built from every rank's voxels -- the z-slab split
+ * of the reference's exact accumulate_region / reduce_and_update
+ * (slic.hpp:315-372). */
+int sslic_engine_value_range(sslic_engine* e, double* absmax_out);
+int sslic_engine_set_value_range(sslic_engine* e, double absmax);
 /* Force the exact fp64 assignment kernel (1) or allow the fast fp32-filter
  * kernel where supported (0, default). Both produce identical labels. */
 int sslic_engine_set_exact(sslic_engine* e, int exact);

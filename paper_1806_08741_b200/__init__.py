@@ -131,6 +131,8 @@ def lib():
         "sslic_engine_create": (C.c_int, [ip, pp, C.c_int, C.c_int64, C.c_int64, C.c_int64,
                                           C.c_int64, vp, C.POINTER(vp)]),
         "sslic_engine_destroy": (C.c_int, [vp]),
+        "sslic_engine_value_range": (C.c_int, [vp, C.POINTER(C.c_double)]),
+        "sslic_engine_set_value_range": (C.c_int, [vp, C.c_double]),
         "sslic_engine_init": (C.c_int, [vp]),
         "sslic_engine_centers_buffer": (C.c_int, [vp, C.POINTER(vp), i64p]),
         "sslic_engine_commit_centers": (C.c_int, [vp]),
@@ -713,6 +715,17 @@ class Engine:
                         device=f"cuda:{self.device}")
         self.labels_to(t.data_ptr())
         return t
+
+    def value_range(self) -> float:
+        """max |value| over this engine's planes (float dtypes; the dtype
+        maximum for u8/u16), see sslic_engine_value_range."""
+        v = C.c_double()
+        _check(lib().sslic_engine_value_range(self.h, C.byref(v)))
+        return float(v.value)
+
+    def set_value_range(self, absmax: float):
+        """Multi-GPU: every rank sets the MAX over ranks (before init)."""
+        _check(lib().sslic_engine_set_value_range(self.h, C.c_double(absmax)))
 
     def set_exact(self, exact: bool = True):
         _check(lib().sslic_engine_set_exact(self.h, int(exact)))

@@ -1265,6 +1265,21 @@ int sslic_engine_assign_ms(sslic_engine* e, int i, float* ms_out, int* n_out) {
   });
 }
 
+int sslic_engine_value_range(sslic_engine* e, double* absmax_out) {
+  return guarded([&] {
+    if (!absmax_out) throw Error(SSLIC_EINVAL, "null output");
+    *absmax_out = e->e->value_range();
+    return SSLIC_OK;
+  });
+}
+
+int sslic_engine_set_value_range(sslic_engine* e, double absmax) {
+  return guarded([&] {
+    e->e->set_value_range(absmax);
+    return SSLIC_OK;
+  });
+}
+
 int sslic_engine_set_exact(sslic_engine* e, int exact) {
   return guarded([&] {
     const bool fast_ok = e->e->fast_supported();

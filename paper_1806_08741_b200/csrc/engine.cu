@@ -102,30 +102,7 @@ Engine::Engine(const sslic_image& img, const sslic_params& p, int device, int64_
     launch_check("fill dists");
   }
   compute_shift();
-  if (g_.dtype == SSLIC_U8) vmax_ = 255.0;
-  if (g_.dtype == SSLIC_U16) vmax_ = 65535.0;
-  {
-    // absolute fp32 margin for the hi/lo centre split (DESIGN.md error bound)
-    const double e = vmax_ * std::ldexp(1.0, -48);
-    const double M = fast_margin(g_.channels);
-    double am = 8.0 * e * e / M + e * e + 1e-37;
-    if (g_.dtype == SSLIC_F64) {
-      // rounding of the f32 working copy (kernels_fast_main.cuh, fast margin)
-      const double ep = vmax_ * std::ldexp(1.0, -24);
-      const double eps0 = (g_.channels + 14) * std::ldexp(1.0, -24);
-      am += g_.channels * (1.0 / eps0 + 1.0) * ep * ep;
-      pix_err_ = ep;
-    }
-    abs_margin_ = (float)am;
-    // key scale 2^-k: the largest possible fp32 distance of a covered
-    // candidate, C (2 vmax + 1)^2 + m^2 rank 4, must map below 2^-67
-    // (kernels_fast.cuh "Keys"). Exact power-of-two scaling.
-    const double dmax = g_.channels * (2.0 * vmax_ + 1.0) * (2.0 * vmax_ + 1.0) +
-                        g_.m_sq * g_.rank * 4.0 + 1.0;
-    const int k = (int)std::ceil((std::log2(dmax) + 67.0) / 2.0);
-    key_scale_ = (float)std::ldexp(1.0, -k);
-    if (!(k < 120)) fast_ok_scale_ = false;  // absurd ranges: keep the exact path
-  }
+  derive_value_params();
   path_ = fast_path_supported(g_) && !dist_mode_ && fast_ok_scale_ ? AssignPath::kFast
                                                                     : AssignPath::kExact;
   if (path_ == AssignPath::kFast)
@@ -186,6 +163,51 @@ void Engine::compute_shift() {
   if (m > 0.0) std::frexp(m, &e);  // m < 2^e
   shift_ = 40 - e;                  // |v| * 2^shift < 2^40
   vmax_ = m;
+}
+
+// Parameters derived from the value range: the fixed-point shift of float
+// intensities, the fp32 filter's absolute margin and key scale.
+void Engine::derive_value_params() {
+  if (g_.dtype == SSLIC_U8) vmax_ = 255.0;
+  if (g_.dtype == SSLIC_U16) vmax_ = 65535.0;
+  {
+    // absolute fp32 margin for the hi/lo centre split (DESIGN.md error bound)
+    const double e = vmax_ * std::ldexp(1.0, -48);
+    const double M = fast_margin(g_.channels);
+    double am = 8.0 * e * e / M + e * e + 1e-37;
+    if (g_.dtype == SSLIC_F64) {
+      // rounding of the f32 working copy (kernels_fast_main.cuh, fast margin)
+      const double ep = vmax_ * std::ldexp(1.0, -24);
+      const double eps0 = (g_.channels + 14) * std::ldexp(1.0, -24);
+      am += g_.channels * (1.0 / eps0 + 1.0) * ep * ep;
+      pix_err_ = ep;
+    }
+    abs_margin_ = (float)am;
+    // key scale 2^-k: the largest possible fp32 distance of a covered
+    // candidate, C (2 vmax + 1)^2 + m^2 rank 4, must map below 2^-67
+    // (kernels_fast.cuh "Keys"). Exact power-of-two scaling.
+    const double dmax = g_.channels * (2.0 * vmax_ + 1.0) * (2.0 * vmax_ + 1.0) +
+                        g_.m_sq * g_.rank * 4.0 + 1.0;
+    const int k = (int)std::ceil((std::log2(dmax) + 67.0) / 2.0);
+    key_scale_ = (float)std::ldexp(1.0, -k);
+    if (!(k < 120)) fast_ok_scale_ = false;  // absurd ranges: keep the exact path
+  }
+}
+
+double Engine::value_range() const { return vmax_; }
+
+// Multi-GPU: every rank must use the same value range (the fixed-point
+// shift of the summed deltas, and the filter margins of centres built from
+// every rank's voxels), i.e. the MAX over ranks of value_range().
+void Engine::set_value_range(double m) {
+  if (g_.dtype == SSLIC_U8 || g_.dtype == SSLIC_U16) return;  // fixed: dtype max, shift 0
+  if (!(m >= 0.0)) throw Error(SSLIC_EINVAL, "engine: value range must be >= 0");
+  int e = 0;
+  if (m > 0.0) std::frexp(m, &e);  // m < 2^e
+  shift_ = 40 - e;
+  vmax_ = m;
+  derive_value_params();
+  if (!fast_ok_scale_) path_ = AssignPath::kExact;
 }
 
 double* Engine::current_centers() const {

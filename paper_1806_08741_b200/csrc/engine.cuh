@@ -70,6 +70,10 @@ class Engine {
   float assign_ms(int i);
   int assign_calls() const { return n_assign_; }
   void set_value_shift(int s) { shift_ = s; }
+  // max |value| over this engine's data (float dtypes; the dtype max for
+  // u8/u16) and its override with the MAX over ranks (multi-GPU)
+  double value_range() const;
+  void set_value_range(double absmax);
   int value_shift() const { return shift_; }
   void set_path(AssignPath p) { path_ = p; }
   // The fast fp32-filter kernel applies to this geometry/dtype/mode.
@@ -93,6 +97,7 @@ class Engine {
   FastParams fast_params();
   void launch_exact_kernel(bool accumulate, int64_t nv, const double* hist);
   void compute_shift();
+  void derive_value_params();
 
   Geom g_{};
   const void* img_ = nullptr;

@@ -18,7 +18,7 @@ CUDA engine over NCCL on B200s and an oracle-backed engine over gloo on CPU
 """
 from __future__ import annotations
 
-from typing import Callable, List, Tuple
+from typing import Optional, Callable, List, Tuple
 
 
 def slab_bounds(last: int, world: int, rank: int, align: int = 1) -> Tuple[int, int]:
@@ -43,18 +43,36 @@ def all_slabs(last: int, world: int, align: int = 1) -> List[Tuple[int, int]]:
     return [slab_bounds(last, world, r, align) for r in range(world)]
 
 
+def _dist_max(v: float) -> float:
+    """MAX of a scalar over the torch.distributed group (NCCL: on the
+    current CUDA device; gloo: on the CPU)."""
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 class ShardedLoop:
     """run_slic's loop (slic.hpp:397-412) over one slab per rank."""
 
-    def __init__(self, engine, allreduce: Callable, world: int):
+    def __init__(self, engine, allreduce: Callable, world: int,
+                 allreduce_max: Optional[Callable[[float], float]] = None):
         self.engine = engine
         self.allreduce = allreduce
         self.world = world
+        self.allreduce_max = allreduce_max or _dist_max
 
     def init(self):
         """init + perturb: every rank fills the clusters whose initial cell
         centre lies in its slab and zeros elsewhere; the SUM allreduce then
-        assembles the full table exactly (one non-zero term per entry)."""
+        assembles the full table exactly (one non-zero term per entry).
+        First, every rank adopts the MAX over ranks of the engines' value
+        ranges: the fixed-point scale of the allreduced float sums must be
+        one scale (sslic_engine_set_value_range)."""
+        if self.world > 1 and hasattr(self.engine, "value_range"):
+            self.engine.set_value_range(self.allreduce_max(self.engine.value_range()))
         self.engine.init()
         if self.world > 1:
             self.allreduce(self.engine.centers_tensor())

@@ -236,6 +236,10 @@ def test_slab_engines_sum_to_single_engine(sslic, world):
         for t in tensors:
             t.copy_(total)
 
+    # (ShardedLoop.init: every rank adopts the MAX of the value ranges)
+    vmax = max(e.value_range() for e in engines)
+    for e in engines:
+        e.set_value_range(vmax)
     for e in engines:
         e.init()
     allreduce([e.centers_tensor() for e in engines])
@@ -360,3 +364,83 @@ def test_fast_equals_exact_fuzz(sslic, case):
         torch.cuda.synchronize()
         assert int((la != lb).sum().item()) == 0, f"iteration {it}: labels differ"
         assert np.array_equal(fast.centers(), exact.centers()), f"iteration {it}: centres"
+
+
+def _slab_fuzz(n=10, seed=8741):
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(n):
+        ch = int(rng.integers(1, 5))
+        dtype = [np.uint8, np.uint16, np.float32][int(rng.integers(0, 3))]
+        dims = tuple(int(x) for x in rng.integers(20, 72, size=3))
+        grid = tuple(int(rng.integers(3, min(d, 14) + 1)) for d in dims)
+        world = int(rng.integers(2, 6))
+        align = bool(rng.integers(0, 2))
+        out.append((dims, ch, dtype, grid, float(rng.choice([5.0, 10.0, 25.0])),
+                    int(rng.integers(2, 5)), world, align, int(rng.integers(0, 1 << 30))))
+    return out
+
+
+@pytest.mark.parametrize("case", _slab_fuzz(), ids=lambda c: f"w{c[6]}{'a' if c[7] else 'u'}-"
+                         f"c{c[1]}-{np.dtype(c[2]).name}-{'x'.join(map(str, c[0]))}")
+def test_slab_engines_fuzz(sslic, case):
+    """Random volumes split into 2-5 z-slabs (aligned to S or not): the slab
+    engines with summed centre tables and delta buffers (the NCCL allreduces
+    of the multi-GPU path) equal one whole-volume engine bit for bit."""
+    import torch
+    from paper_1806_08741_b200.sharded import all_slabs, data_bounds
+    s = sslic
+    dims, ch, dtype, grid, m, iters, world, align, seed = case
+    rng = np.random.default_rng(seed)
+    hi = {np.uint8: 255.0, np.uint16: 65535.0, np.float32: 1.0}[dtype]
+    vol = rng.uniform(0, hi, size=(dims[2] // 5 + 1, dims[1] // 5 + 1, dims[0] // 5 + 1, ch))
+    vol = vol.repeat(5, 0)[:dims[2]].repeat(5, 1)[:, :dims[1]].repeat(5, 2)[:, :, :dims[0]]
+    vol = np.clip(vol + rng.normal(0, 0.05 * hi, size=vol.shape), 0, hi)
+    if dtype == np.float32:  # slabs with different value ranges (scales differ)
+        vol[-(dims[2] // 3):] *= 3.7
+    host = (np.rint(vol) if dtype != np.float32 else vol).astype(dtype).reshape(-1)
+    img = torch.from_numpy(host.view(np.int16) if dtype == np.uint16 else host).cuda()
+    p = s.SlicParams(grid=list(grid), weight_m=m, max_iterations=iters)
+    single = s.Engine(dims, ch, dtype, img.data_ptr(), p)
+    plane = int(np.prod(dims[:-1]))
+    esize = np.dtype(dtype).itemsize * ch
+    slabs = all_slabs(dims[-1], world, align=grid[-1] if align else 1)
+    engines = []
+    for sl in slabs:
+        dr = data_bounds(dims[-1], sl)
+        engines.append(s.Engine(dims, ch, dtype, img.data_ptr() + dr[0] * plane * esize, p,
+                                slab=sl, data_range=dr))
+
+    def allreduce(tensors):
+        total = tensors[0].clone()
+        for t in tensors[1:]:
+            total += t
+        for t in tensors:
+            t.copy_(total)
+
+    # (ShardedLoop.init: every rank adopts the MAX of the value ranges)
+    vmax = max(e.value_range() for e in engines)
+    for e in engines:
+        e.set_value_range(vmax)
+    for e in engines:
+        e.init()
+    allreduce([e.centers_tensor() for e in engines])
+    for e in engines:
+        e.commit()
+    single.init()
+    single.commit()
+    for _ in range(iters):
+        for e in engines:
+            e.assign()
+        allreduce([e.partials_tensor() for e in engines])
+        for e in engines:
+            e.update()
+        single.assign()
+        single.update()
+    torch.cuda.synchronize()
+    full = torch.cat([e.labels_tensor() for e in engines]).cpu().numpy().view(np.uint32)
+    ref = torch.empty(int(np.prod(dims)), dtype=torch.int32, device="cuda")
+    single.labels_to(ref.data_ptr())
+    assert np.array_equal(full, ref.cpu().numpy().view(np.uint32))
+    for e in engines:
+        assert np.array_equal(e.centers(), single.centers())

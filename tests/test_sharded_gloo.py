@@ -47,6 +47,13 @@ class OracleSlabEngine:
     def centers_tensor(self):
         return self.centers
 
+    def value_range(self):
+        plane = self.plane * self.ch
+        return float(np.abs(self.data[self.slab[0] * plane: self.slab[1] * plane]).max())
+
+    def set_value_range(self, v):
+        self.synced_range = v
+
     def commit(self):
         pass
 
@@ -123,6 +130,8 @@ def _worker(rank, world, port, q):
                           dims[-1], plane, align=grid[-1])
         mine = eng.labels[slab[0] * plane: slab[1] * plane].copy()
         parts = [None] * world
+        # every rank adopted the MAX of the ranks' value ranges (gloo MAX)
+        assert eng.synced_range == float(np.abs(data).max())
         dist.all_gather_object(parts, (slab, mine, eng.centers.numpy().copy(), cc))
         if rank == 0:
             labels = np.concatenate([p[1] for p in sorted(parts, key=lambda p: p[0][0])])
