@@ -112,10 +112,11 @@ def test_engine_labels_tensor_and_gather_single_rank(sslic):
     assert np.array_equal(cc, s.enforce_connectivity(full, dims, table, p))
 
 
-@pytest.mark.parametrize("dims,iters", [
-    ((256, 256, 256), 8), ((256, 256, 256), 4), ((256, 256, 264), 8), ((257, 256, 257), 6)],
-    ids=["change-list", "list-overflow", "partial-region-row", "no-pipeline"])
-def test_run_slic_overlapped_download_matches(sslic, dims, iters):
+@pytest.mark.parametrize("dims,iters,rgb", [
+    ((256, 256, 256), 8, False), ((256, 256, 256), 4, False), ((256, 256, 264), 8, False),
+    ((257, 256, 257), 6, False), ((256, 256, 256), 5, True)],
+    ids=["change-list", "list-overflow", "partial-region-row", "no-pipeline", "rgb-u8-S32"])
+def test_run_slic_overlapped_download_matches(sslic, dims, iters, rgb):
     """sslic_run_slic into a pinned host label map of >= 2^24 voxels
     * uploads the image in z chunks, overlapped with the chunk-wise centre
       perturbation and iteration 0's assign (Engine::pipeline_ok; not for a
@@ -129,12 +130,13 @@ def test_run_slic_overlapped_download_matches(sslic, dims, iters):
     import ctypes as C
     import torch
     s = sslic
-    cfg, ch, dtype, grid, m = (3, 1, np.uint16, (16, 16, 16), 10.0)
+    cfg, ch, dtype, grid, m = ((5, 3, np.uint8, (32, 32, 32), 10.0) if rgb
+                               else (3, 1, np.uint16, (16, 16, 16), 10.0))
     n = int(np.prod(dims))
-    dev = torch.empty(n * ch, dtype=torch.int16, device="cuda")
+    dev = torch.empty(n * ch, dtype=torch.uint8 if rgb else torch.int16, device="cuda")
     s.synth_generate(cfg, dims, dtype, ch, 77, 0, dims[-1], dev.data_ptr())
     torch.cuda.synchronize()
-    host = dev.cpu().numpy().view(np.uint16)
+    host = dev.cpu().numpy().view(dtype)
     L = s.lib()
     img = s.NDImage(dims, ch, host)
     p = s.SlicParams(grid=list(grid), weight_m=m, max_iterations=iters)
