@@ -446,3 +446,69 @@ def test_slab_engines_fuzz(sslic, case):
     assert np.array_equal(full, ref.cpu().numpy().view(np.uint32))
     for e in engines:
         assert np.array_equal(e.centers(), single.centers())
+
+
+def _pipeline_geoms(n=4, seed=31337):
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < n:
+        dims = tuple(int(x) for x in rng.integers(200, 330, size=3))
+        if int(np.prod(dims)) < (1 << 24):
+            continue
+        grid = tuple(int(rng.integers(3, 26)) for _ in dims)
+        ch = int(rng.integers(1, 4))
+        dtype = [np.uint8, np.uint16][int(rng.integers(0, 2))]
+        out.append((dims, grid, ch, dtype, float(rng.choice([5.0, 10.0, 20.0])),
+                    int(rng.integers(4, 9)), int(rng.integers(0, 1 << 30))))
+    return out
+
+
+@pytest.mark.parametrize("case", _pipeline_geoms(), ids=lambda c: f"{'x'.join(map(str, c[0]))}-"
+                         f"S{'x'.join(map(str, c[1]))}-c{c[2]}-{np.dtype(c[3]).name}")
+def test_run_slic_pipelined_random_geometry(sslic, case):
+    """sslic_run_slic with a pinned label map (pipelined z-chunk upload when
+    Engine::pipeline_ok, overlapped download) on random >= 2^24-voxel
+    geometries (S not dividing the dims, 1-3 channels) equals the same call
+    into pageable memory bit for bit."""
+    import ctypes as C
+    import torch
+    s = sslic
+    dims, grid, ch, dtype, m, iters, seed = case
+    rng = np.random.default_rng(seed)
+    hi = 255 if dtype == np.uint8 else 65535
+    n = int(np.prod(dims))
+    coarse = [max(1, d // 12) for d in dims]
+    base = rng.integers(0, hi + 1, size=tuple(reversed(coarse)) + (ch,))
+    idx = np.ix_(*[np.minimum(np.arange(d) // max(1, d // c), c - 1)
+                   for d, c in zip(reversed(dims), reversed(coarse))])
+    vol = base[idx] + rng.normal(0, 0.04 * hi, size=tuple(reversed(dims)) + (ch,))
+    host = np.clip(np.rint(vol), 0, hi).astype(dtype).reshape(-1)
+    pinned_img = torch.from_numpy(host.view(np.int16) if dtype == np.uint16 else host)
+    pinned_img = pinned_img.pin_memory()
+    L = s.lib()
+    p = s.SlicParams(grid=list(grid), weight_m=m, max_iterations=iters)
+    k = s.cluster_count(dims, grid)
+
+    def call(data_ptr, labels_ptr):
+        d = s._Image()
+        d.rank = 3
+        for a in range(4):
+            d.dims[a] = dims[a] if a < 3 else 1
+        d.channels = ch
+        d.dtype = s._DT[np.dtype(dtype)]
+        d.data = data_ptr
+        cen = np.empty(k * (ch + 3))
+        res = np.empty(iters)
+        done = C.c_int()
+        s._check(L.sslic_run_slic(C.byref(d), C.byref(p._c()), 0,
+                                  C.cast(C.c_void_p(labels_ptr), C.POINTER(C.c_uint32)),
+                                  cen.ctypes.data_as(C.POINTER(C.c_double)),
+                                  res.ctypes.data_as(C.POINTER(C.c_double)), C.byref(done)))
+        return cen, res
+
+    pinned = torch.empty(n, dtype=torch.int32, pin_memory=True)
+    c1, r1 = call(pinned_img.data_ptr(), pinned.data_ptr())
+    pageable = np.empty(n, np.uint32)
+    c2, r2 = call(host.ctypes.data, pageable.ctypes.data)
+    assert np.array_equal(pinned.numpy().view(np.uint32), pageable)
+    assert np.array_equal(c1, c2) and np.array_equal(r1, r2)
