@@ -214,9 +214,11 @@ __global__ void k_patch_labels_host(int64_t n, const uint32_t* before, const uin
 // writes into the caller's map). Each block walks 4096-label tiles and
 // reserves its tile's entries with one atomic; entries past `cap` are
 // counted but not written (the caller then copies the whole map).
+// (amask != ~0: `after` holds engine label words, decoded like
+// LabelCodec::label -- the final map needs no separate unpack pass)
 __global__ void k_change_list(int64_t n, const uint32_t* before, const uint32_t* after,
                               unsigned long long* count, int64_t cap, uint2* out,
-                              uint32_t idx0 = 0) {
+                              uint32_t idx0 = 0, uint32_t amask = 0xffffffffu) {
   constexpr int kPer = 16;
   __shared__ unsigned long long base;
   __shared__ int warp_tot[8];
@@ -230,7 +232,8 @@ __global__ void k_change_list(int64_t n, const uint32_t* before, const uint32_t*
       const int64_t i = tile + j * 256 + tid;
       val[j] = 0;
       if (i < n) {
-        const uint32_t a = after[i];
+        const uint32_t w = after[i];
+        const uint32_t a = w == 0xffffffffu ? w : (w & amask);
         val[j] = a;
         if (a != before[i]) chg |= 1u << j;
       }
@@ -482,10 +485,9 @@ int run_loop_overlapped(Engine& e, Stream& st, uint32_t* labels_out, int64_t n,
     e.update();
     em.mark(st.s, "it" + std::to_string(it));
   }
-  DeviceBuf fin(n * sizeof(uint32_t), st.s);
-  e.unpack_labels(fin.as<uint32_t>());
-  em.mark(st.s, "unpack");
-  if (!listed) {  // >= 2^32 voxels: snapshot, then the changed labels via the mapped map
+  DeviceBuf fin(n * sizeof(uint32_t), st.s);  // unpacked only where needed
+  if (!listed) {
+    e.unpack_labels(fin.as<uint32_t>());  // >= 2^32 voxels: snapshot, then the changed labels via the mapped map
     OwnedEvent copied_ev;
     const cudaEvent_t copied = copied_ev.e;
     SSLIC_CUDA_CHECK(cudaMemcpyAsync(labels_out, snapbuf.p, n * sizeof(uint32_t),
@@ -514,8 +516,9 @@ int run_loop_overlapped(Engine& e, Stream& st, uint32_t* labels_out, int64_t n,
   SSLIC_CUDA_CHECK(cudaMemsetAsync(cntb.p, 0, K * sizeof(unsigned long long), st.s));
   for (int c = 0; c < K; ++c) {
     k_change_list<<<148 * 2, 256, 0, st.s>>>(
-        c0[c + 1] - c0[c], snapbuf.as<uint32_t>() + c0[c], fin.as<uint32_t>() + c0[c],
-        cntb.as<unsigned long long>() + c, cap[c], dlist.as<uint2>() + off[c], (uint32_t)c0[c]);
+        c0[c + 1] - c0[c], snapbuf.as<uint32_t>() + c0[c], e.label_words() + c0[c],
+        cntb.as<unsigned long long>() + c, cap[c], dlist.as<uint2>() + off[c], (uint32_t)c0[c],
+        e.codec().label_mask);
     SSLIC_CUDA_CHECK(cudaGetLastError());
   }
   MappedStage& ms = mapped_stage();
@@ -584,6 +587,10 @@ int run_loop_overlapped(Engine& e, Stream& st, uint32_t* labels_out, int64_t n,
   bool any_whole = false;
   for (int c = 0; c < K; ++c)
     if (whole[c]) {  // too many changes in this piece: its final labels, whole
+      if (!any_whole) {
+        e.unpack_labels(fin.as<uint32_t>());
+        st.sync();
+      }
       any_whole = true;
       SSLIC_CUDA_CHECK(cudaMemcpyAsync(labels_out + c0[c], fin.as<uint32_t>() + c0[c],
                                        (c0[c + 1] - c0[c]) * sizeof(uint32_t),
