@@ -227,15 +227,15 @@ class Oracle:
                                  int(min_size), int(k_start))
         return lab, mk, int(nxt)
 
-    def enforce_connectivity(self, dims, labels, centers, channels, grid):
+    def enforce_connectivity(self, dims, labels, centers, channels, grid, return_next=False):
         dims, grid = _dims(dims), _dims(grid)
         lab = np.ascontiguousarray(labels, dtype=np.uint32).reshape(-1)
         c = np.ascontiguousarray(centers, dtype=np.float64)
         out = np.empty_like(lab)
-        self.lib.orc_enforce_connectivity(len(dims), _p(dims, _i64p), _p(lab, _u32p),
-                                          _p(c, _f64p), channels, c.shape[0], _p(grid, _i64p),
-                                          _p(out, _u32p))
-        return out
+        nxt = self.lib.orc_enforce_connectivity(len(dims), _p(dims, _i64p), _p(lab, _u32p),
+                                                _p(c, _f64p), channels, c.shape[0],
+                                                _p(grid, _i64p), _p(out, _u32p))
+        return (out, int(nxt)) if return_next else out
 
 
 class Reference:

@@ -549,9 +549,10 @@ def reduce_and_update(table: ClusterTable, partials, device: int = 0):
 
 
 def enforce_connectivity(labels: np.ndarray, dims, table: ClusterTable, params: SlicParams,
-                         workers: int = 1, device: int = 0) -> np.ndarray:
+                         workers: int = 1, device: int = 0, return_next: bool = False):
     """enforce_connectivity (connectivity.hpp:265-273): returns a relabelled
-    copy of the flat label map."""
+    copy of the flat label map (and, with return_next, the next unused label
+    that sweep_relabel returns, connectivity.hpp:182)."""
     lab = np.ascontiguousarray(labels, np.uint32).reshape(-1)
     dd = np.asarray(dims, np.int64)
     g = np.asarray(params.grid, np.int64)
@@ -562,7 +563,7 @@ def enforce_connectivity(labels: np.ndarray, dims, table: ClusterTable, params: 
                                             _p(c, C.c_double), table.channels, c.shape[0],
                                             _p(g, C.c_int64), device, _p(out, C.c_uint32),
                                             C.byref(nxt)))
-    return out
+    return (out, int(nxt.value)) if return_next else out
 
 
 def synth_generate(config: int, dims, dtype, channels: int, seed: int, z_begin: int,
