@@ -7,13 +7,25 @@ A step is one SLIC iteration (fused assign+accumulate, allreduce when N>1,
 centre update) over the whole synthetic volume of the chosen BASELINE.json
 config, already resident in HBM (generated on device by the seeded
 counter-based generator). Default workload: config 3 (1024^3 uint16, S=16,
-m=10), the largest single-GPU config the metric is quoted on at 1/2/4/8 GPUs
-(configs 3-5); the others are parity cases. Inputs (2 GiB image + 4 GiB labels)
-are larger than L2, so no flush is needed between iterations.
+m=10, 10 iterations), the largest single-GPU config the metric is quoted on
+at 1/2/4/8 GPUs (configs 3-5); the others are parity cases.
+
+Iteration window: the steps are the CONFIGURED iterations of whole runs. Step
+j is iteration j mod I of run j div I (I = the config's iteration count); each
+run starts from a fresh init + perturbation (outside the timed spans), so
+K = 20 times iterations 0..9 exactly twice. The warm-up steps are a separate
+untimed run. Inputs (2 GiB image + 4 GiB labels for config 3) exceed L2; the
+L2-resident configs 1-2 flush L2 with a 512 MB write between steps.
 
 Under torchrun (N>1) each rank owns a contiguous z-slab; the one exchange per
 iteration is an NCCL allreduce of the int64 per-cluster partials. Rank 0
 prints ONE JSON line.
+
+--impl reference times the UNMODIFIED reference's multi-threaded CPU loop
+(oracle/_ref: the reference headers compiled by oracle/Makefile) on the
+host cores, over the same iteration window, on a bounded sample of the same
+synthetic volume produced by the CPU twin of the device generator
+(oracle/synth_ref.c). That arm never loads the product library.
 """
 from __future__ import annotations
 
@@ -41,6 +53,16 @@ CONFIGS = {
 }
 SEED = 0x1806_08741
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+# CPU runs of the reference. The reference arm runs the whole config volume
+# (config 5's 17.4 G voxels need ~630 GB of fp64 host state, so it takes a
+# 512-plane z-range); the GPU arm's cpu_baseline leg takes a bounded sample of
+# ~10-30 s. Samples are planes [z0, z1) of the same volume treated as their
+# own image: whole multiples of S from the middle, with at least as many
+# S-plane slabs (the reference's unit of parallel work, parallel.hpp:31-50)
+# as host threads where the time allows.
+REF_SAMPLE = {5: (3328, 3840)}
+BASE_SAMPLE = {3: (256, 768), 5: (3456, 3712)}
+METRIC = "voxels/sec per SLIC iteration (assign+update)"
 
 
 def fp32_peak_tflops(sm_count: int, mhz: float) -> float:
@@ -117,32 +139,97 @@ def flops_per_voxel(E, ch, rank):
     return E * (3 * ch + 4 * rank + 2) + (ch + rank)
 
 
-def cpu_sample(cfg_id, dims, ch, dtype):
-    """Bounded CPU sample of the same workload: the first planes of the same
-    synthetic volume, treated as their own image."""
-    if len(dims) == 2:
-        return dims, 2
-    planes = {3: 32, 4: 32, 5: 32}[cfg_id]  # >= S (the reference rejects S > dims)
-    return (dims[0], dims[1], planes), 1
+def host_cores():
+    """(logical, physical) host cores; physical = distinct (package, core id)
+    pairs of /proc/cpuinfo (the acceptance.cpp:44-58 method)."""
+    logical = os.cpu_count() or 1
+    pairs, phys, core = set(), None, None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("physical id"):
+                    phys = line.split(":")[1].strip()
+                elif line.startswith("core id"):
+                    core = line.split(":")[1].strip()
+                elif not line.strip():
+                    if core is not None:
+                        pairs.add((phys, core))
+                    phys = core = None
+    except OSError:
+        pass
+    return logical, (len(pairs) or logical)
 
 
-def run_reference_cpu(cfg_id, steps, warmup, data_host, sdims, ch, grid, m):
-    """Times the UNMODIFIED reference's multi-threaded CPU iteration loop
-    (oracle/_ref, reference headers) on the bounded sample."""
+def cpu_sample(cfg_id, dims, table):
+    """A CPU sample of the config volume: (sample dims, z0, z1)."""
+    if cfg_id in table:
+        z0, z1 = table[cfg_id]
+        return (dims[0], dims[1], z1 - z0), z0, z1
+    return tuple(dims), 0, (dims[-1] if len(dims) == 3 else 1)
+
+
+def window(steps, iters):
+    """Iteration indices of `steps` consecutive steps cycling whole runs."""
+    return [j % iters for j in range(steps)]
+
+
+def reference_window_rate(cfg_id, steps, warmup, workers, table):
+    """The unmodified reference (oracle/_ref) over the configured-iteration
+    window on the bounded sample: one warm-up run of `warmup` iterations,
+    then whole runs whose first `steps` iterations (cycling) are timed.
+    Returns (voxel-iter/s, sample description)."""
     import oracle
+    dims, ch, dtype, grid, m, iters = CONFIGS[cfg_id]
+    sdims, z0, z1 = cpu_sample(cfg_id, dims, table)
+    t0 = time.perf_counter()
+    data = oracle.Oracle().synth_generate(cfg_id, dims, dtype, ch, SEED, z0, z1)
+    gen_s = time.perf_counter() - t0
+    d = data.astype(np.float64)
     ref = oracle.Reference()
-    cores = os.cpu_count() or 1
-    d = data_host.astype(np.float64)
-    _, per_iter = ref.time_iterations(d, sdims, ch, grid, m, warmup + steps, cores)
-    t = sum(per_iter[warmup:])
+    if warmup > 0:
+        ref.time_iterations(d, sdims, ch, grid, m, min(warmup, iters), workers)
+    per_iter = []
+    left = steps
+    while left > 0:
+        n = min(iters, left)
+        _, t = ref.time_iterations(d, sdims, ch, grid, m, n, workers)
+        per_iter += t
+        left -= n
     nvox = int(np.prod(sdims))
-    return nvox * steps / t, cores
+    rate = nvox * steps / sum(per_iter)
+    where = (f"planes [{z0},{z1}) of the config volume ({'x'.join(map(str, sdims))}, "
+             f"{nvox} voxels) as their own image" if cfg_id in table
+             else f"the whole config volume ({nvox} voxels)")
+    desc = (f"{where}; iterations {window(steps, iters)[:iters]} of whole runs "
+            f"({steps} timed after {warmup} warm-up), reference headers -O3 "
+            f"-ffp-contract=off, {workers} threads; CPU generator {gen_s:.1f} s (untimed)")
+    return rate, desc, per_iter
+
+
+def run_reference_arm(args, config):
+    logical, physical = host_cores()
+    rate, desc, per_iter = reference_window_rate(args.config, args.steps, args.warmup, logical,
+                                                 REF_SAMPLE)
+    dims = CONFIGS[args.config][0]
+    sdims, _, _ = cpu_sample(args.config, dims, REF_SAMPLE)
+    line = {"metric": METRIC, "value": rate, "unit": "voxel-iter/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": int(np.prod(sdims)) / rate * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded; CPU twin of the device generator)",
+            "impl": "reference", "config": config,
+            "cpu_baseline": {"value": rate, "unit": "voxel-iter/s", "cores": logical,
+                             "physical_cores": physical, "kind": "reference", "sample": desc},
+            "e2e": {"value": rate, "unit": "voxel-iter/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "reference_ms_per_iteration": [t * 1e3 for t in per_iter]}
+    print(json.dumps(line))
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=7)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=3, choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -157,47 +244,25 @@ def main():
     world, rank, local = dist_setup()
     dims, ch, dtype, grid, m, cfg_iters = CONFIGS[args.config]
     nvox = int(np.prod(dims))
-    metric = "voxels/sec per SLIC iteration (assign+update)"
     config = {"workload": f"config{args.config}", "dims": list(dims), "channels": ch,
               "dtype": np.dtype(dtype).name, "grid": list(grid), "m": m,
-              "parallelism": f"zslab{world}"}
+              "iterations": cfg_iters, "parallelism": f"zslab{world}"}
     # working set per step: image + label words (+ tables); B200 L2 = 126 MB
     fits_l2 = nvox * (ch * np.dtype(dtype).itemsize + 4) < 126e6
     config["l2"] = ("fits in L2: 512 MB flush write between timed steps (outside the timed "
                     "spans)" if fits_l2 else "inputs larger than L2 (no flush needed)")
+    config["window"] = (f"configured iterations 0..{cfg_iters - 1} of whole runs, cycled; "
+                        "init + perturbation outside the timed spans")
+
+    if args.impl == "reference":
+        # the reference's CPU path on the host cores; rank 0 only, no GPU, and
+        # nothing from the product package is imported
+        if rank == 0:
+            run_reference_arm(args, config)
+        return
 
     import torch
     torch.cuda.set_device(local)
-
-    if args.impl == "reference":
-        if rank != 0:
-            return
-        # the reference's CPU path on the host cores: bounded sample per step
-        import paper_1806_08741_b200 as s
-        sdims, _ = cpu_sample(args.config, dims, ch, dtype)
-        n_s = int(np.prod(sdims))
-        buf = torch.empty(n_s * ch, dtype={np.uint8: torch.uint8, np.uint16: torch.int16,
-                                          np.float32: torch.float32}[dtype], device="cuda")
-        s.synth_generate(args.config, dims, dtype, ch, SEED, 0, sdims[-1] if len(dims) == 3
-                         else 1, buf.data_ptr())
-        torch.cuda.synchronize()
-        host = buf.cpu().numpy().view(dtype)
-        v, cores = run_reference_cpu(args.config, args.steps, args.warmup, host, sdims, ch,
-                                     grid, m)
-        line = {"metric": metric, "value": v, "unit": "voxel-iter/s", "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": n_s / v * 1e3,
-                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-                "dtype": "f64", "data": "synthetic", "impl": "reference",
-                "config": dict(config, sample=list(sdims)),
-                "cpu_baseline": {"value": v, "unit": "voxel-iter/s", "cores": cores,
-                                 "kind": "reference",
-                                 "sample": f"first {sdims[-1]} planes ({n_s} voxels) of the "
-                                           f"config volume, {args.steps} timed iterations"},
-                "e2e": {"value": v, "unit": "voxel-iter/s", "h2d_bytes_per_step": 0,
-                        "d2h_bytes_per_step": 0}}
-        print(json.dumps(line))
-        return
-
     if world > 1:
         import torch.distributed as tdist
         if os.environ.get("SSLIC_BENCH_FUNCTIONAL_CHECK") == "1":
@@ -223,8 +288,7 @@ def main():
     else:
         s.synth_generate(args.config, dims, dtype, ch, SEED, 0, 1, img.data_ptr(),
                          stream.cuda_stream)
-    total_iters = args.warmup + args.steps + 1
-    params = s.SlicParams(grid=list(grid), weight_m=m, max_iterations=max(total_iters, 1))
+    params = s.SlicParams(grid=list(grid), weight_m=m, max_iterations=cfg_iters)
     eng = s.Engine(dims, ch, dtype, img.data_ptr(), params, slab=slab, data_range=drange,
                    device=local, stream=stream.cuda_stream)
     if args.path == "exact":
@@ -235,9 +299,27 @@ def main():
         tdist.all_reduce(t)
 
     loop = ShardedLoop(eng, allreduce, world)
-    loop.init()
-    for _ in range(args.warmup):
+
+    def fresh_run():
+        eng.reset()
+        loop.init()
+
+    # warm-up: an untimed run of W iterations (cycling when W > I)
+    for j in range(args.warmup):
+        if j % cfg_iters == 0:
+            fresh_run()
         loop.iterate()
+
+    graphs = world == 1 and not args.no_graph
+    config["launch"] = "CUDA graph per timed span" if graphs else "direct launches"
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda") if fits_l2 else None
+    # timed spans: one per run (inputs > L2) or one per step (L2-resident)
+    runs = []
+    j = 0
+    while j < args.steps:
+        n = min(cfg_iters, args.steps - j)
+        runs.append(n)
+        j += n
     clocks = Clocks(local)
     clocks.start()
     if world > 1:
@@ -245,103 +327,104 @@ def main():
         tdist.barrier()
     torch.cuda.synchronize()
     launches0 = eng.launch_count()
-    a0 = eng.assign_calls()
-    # Inputs larger than L2 (configs 3-5): one event pair around the K steps.
-    # Inputs that fit in L2 (configs 1-2): each step timed by its own events
-    # with a 512 MB L2-flushing write between steps, outside the timed spans.
-    # On one GPU the steps run as CUDA graphs (capture outside the timed
-    # span, one launch inside it), which removes the per-kernel launch gaps
-    # that dominate the small configs; with NCCL between steps (N > 1) they
-    # are launched directly.
-    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda") if fits_l2 else None
-    graphs = world == 1 and not args.no_graph
-    config["launch"] = "CUDA graph per timed span" if graphs else "direct launches"
-    if flush is None:
-        if graphs:
-            ms = eng.iterate_graph(args.steps)
-        else:
-            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            ev0.record(stream)
-            for _ in range(args.steps):
-                loop.iterate()
-            ev1.record(stream)
-            torch.cuda.synchronize()
-            ms = ev0.elapsed_time(ev1)
-    else:
-        ms = 0.0
-        evs = []
-        for _ in range(args.steps):
-            flush.fill_(1)
+    ms = 0.0
+    assign_idx = []  # (assign launch index, iteration index)
+    for n in runs:
+        fresh_run()  # untimed
+        spans = [n] if flush is None else [1] * n
+        it = 0
+        for span in spans:
+            if flush is not None:
+                flush.fill_(1)
+            a0 = eng.assign_calls()
             if graphs:
-                ms += eng.iterate_graph(1)
-                continue
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            loop.iterate()
-            e1.record(stream)
-            evs.append((e0, e1))
-        torch.cuda.synchronize()
-        ms += sum(e0.elapsed_time(e1) for e0, e1 in evs)
-        del flush
+                ms += eng.iterate_graph(span)
+            else:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for _ in range(span):
+                    loop.iterate()
+                e1.record(stream)
+                e1.synchronize()
+                ms += e0.elapsed_time(e1)
+            assign_idx += [(a0 + i, it + i) for i in range(span)]
+            it += span
+    torch.cuda.synchronize()
     if world > 1:
         tdist.barrier()
     clk = clocks.stop()
     launches = eng.launch_count() - launches0
-    assign_ms = [eng.assign_ms(i) for i in range(a0, a0 + args.steps)]
-    # one extra (untimed) iteration with evaluation statistics for the roofline's E
+    del flush
+    assign_ms = [eng.assign_ms(i) for i, _ in assign_idx]
+
+    # untimed statistics run: evaluations and window volume per iteration
+    E_it, evals_it, amb_it, chg_it = [], [], [], []
+    fresh_run()
     eng.set_stats(True)
-    loop.iterate()
-    evals, window = eng.eval_stats()
-    ambiguous, overflow, changed = eng.fast_stats()
+    for i in range(cfg_iters):
+        loop.iterate()
+        ev, win = eng.eval_stats()
+        amb, _ovf, chg = eng.fast_stats()
+        E_it.append(win / nvox if world == 1 else win)
+        evals_it.append(ev)
+        amb_it.append(amb)
+        chg_it.append(chg)
     eng.set_stats(False)
     undefined = eng.undefined_count()
     if world > 1:
-        t = torch.tensor([ms, evals, window, float(undefined)], dtype=torch.float64,
+        t = torch.tensor([ms] + assign_ms, dtype=torch.float64, device="cuda")
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        ms, assign_ms = float(t[0].item()), t[1:].tolist()
+        w = torch.tensor(E_it + evals_it + [float(undefined)], dtype=torch.float64,
                          device="cuda")
-        mx = t[:1].clone()
-        tdist.all_reduce(mx, op=tdist.ReduceOp.MAX)
-        tdist.all_reduce(t[1:])
-        ms = float(mx.item())
-        evals, window, undefined = (float(x) for x in t[1:].tolist())
-        am = torch.tensor(assign_ms, dtype=torch.float64, device="cuda")
-        tdist.all_reduce(am, op=tdist.ReduceOp.MAX)
-        assign_ms = am.tolist()
+        tdist.all_reduce(w)
+        vals = w.tolist()
+        E_it = [v / nvox for v in vals[:cfg_iters]]
+        evals_it = vals[cfg_iters:2 * cfg_iters]
+        undefined = vals[-1]
     value = nvox * args.steps / (ms / 1e3)
 
-    # roofline of the dominant kernel (fused assign+accumulate), per launch
-    E = window / nvox
-    fpv = flops_per_voxel(E, ch, len(dims))
-    bpv = bytes_per_voxel(ch, dtype)
-    slab_vox = (slab[1] - slab[0]) * plane
-    amean = statistics.mean(assign_ms)
-    achieved_tf = slab_vox * fpv / (amean / 1e3) / 1e12
-    achieved_gbs = slab_vox * bpv / (amean / 1e3) / 1e9
+    # roofline of the dominant kernel (fused assign+accumulate), per launch:
+    # algorithmic flops F(E_i) of the iteration each launch ran
     peaks = json.load(open(PEAKS)) if os.path.exists(PEAKS) else {}
     sm_count = torch.cuda.get_device_properties(local).multi_processor_count
     max_mhz = float(peaks.get("sm_max_mhz", 1965.0))
     p32 = fp32_peak_tflops(sm_count, max_mhz)
-    hbm = float(peaks.get("hbm_gbs", 6650.0))
-    t_roof = max(slab_vox * bpv / (hbm * 1e9), slab_vox * fpv / (p32 * 1e12))
-    bound = "fp32" if slab_vox * fpv / (p32 * 1e12) >= slab_vox * bpv / (hbm * 1e9) else "hbm"
+    hbm = float(peaks.get("hbm_gbs", 6550.0))
+    bpv = bytes_per_voxel(ch, dtype)
+    slab_vox = (slab[1] - slab[0]) * plane
+    flops = [slab_vox * flops_per_voxel(E_it[it], ch, len(dims)) for _, it in assign_idx]
+    kernel_s = sum(assign_ms) / 1e3
+    t_roof = sum(max(f / (p32 * 1e12), slab_vox * bpv / (hbm * 1e9)) for f in flops)
+    fp32_bound = sum(f / (p32 * 1e12) for f in flops) >= len(flops) * slab_vox * bpv / (hbm * 1e9)
+    achieved_tf = sum(flops) / kernel_s / 1e12
+    achieved_gbs = slab_vox * bpv * len(flops) / kernel_s / 1e9
     traffic = None
     tf = os.path.join(ROOT, "profiles", "assign_traffic.json")
     if os.path.exists(tf):
         traffic = json.load(open(tf)).get(f"config{args.config}")
+    E_mean = statistics.mean(E_it[it] for _, it in assign_idx)
     roofline = {
-        "bound": bound,
-        "achieved": achieved_tf if bound == "fp32" else achieved_gbs,
-        "peak": p32 if bound == "fp32" else hbm,
-        "unit": "TFLOP/s" if bound == "fp32" else "GB/s",
-        "frac": (t_roof / (amean / 1e3)),
+        "bound": "fp32" if fp32_bound else "hbm",
+        "achieved": achieved_tf if fp32_bound else achieved_gbs,
+        "peak": p32 if fp32_bound else hbm,
+        "unit": "TFLOP/s" if fp32_bound else "GB/s",
+        "frac": t_roof / kernel_s,
         "traffic": traffic,
         "kernel": "assign (fused assign+accumulate)",
-        "kernel_ms": amean,
-        "kernel_share_of_step": amean * args.steps / ms,
-        "algorithmic": {"E_window_evals_per_voxel": E, "flops_per_voxel": fpv,
-                        "bytes_per_voxel": bpv, "evals_performed_per_voxel": evals / nvox,
-                        "fp64_redecided_voxel_frac": ambiguous / nvox,
-                        "crowded_ctas": overflow,
-                        "label_changed_voxel_frac_last_iter": changed / nvox},
+        "kernel_ms": kernel_s * 1e3 / len(flops),
+        "kernel_ms_per_iteration": [statistics.mean(a for a, (_, it) in zip(assign_ms, assign_idx)
+                                                    if it == i) for i in range(min(cfg_iters,
+                                                                                    args.steps))],
+        "kernel_share_of_step": kernel_s * 1e3 / ms,
+        "algorithmic": {"E_window_evals_per_voxel_mean": E_mean,
+                        "E_per_iteration": E_it,
+                        "flops_per_voxel_mean": flops_per_voxel(E_mean, ch, len(dims)),
+                        "bytes_per_voxel": bpv,
+                        "evals_performed_per_voxel": [e / nvox for e in evals_it],
+                        "fp64_redecided_voxel_frac": [a / nvox for a in amb_it],
+                        "label_changed_voxel_frac": [c / nvox for c in chg_it]},
         "hbm_gbs": achieved_gbs, "hbm_peak_gbs": hbm, "hbm_frac": achieved_gbs / hbm,
         "peak_source": f"FP32 = {sm_count} SMs x 128 x 2 x {max_mhz:.0f} MHz "
                        f"(no measured FP32 peak); HBM = MEASURED_PEAKS.json hbm_gbs",
@@ -359,14 +442,14 @@ def main():
         host.copy_(img)
         slab_vox_e = (slab[1] - slab[0]) * plane
         labels_h = torch.empty(slab_vox_e, dtype=torch.int32, pin_memory=True)
+        eng.close()
         del eng
         torch.cuda.synchronize()
         tdist.barrier()
         t0 = time.perf_counter()
         img2 = torch.empty_like(img)
         img2.copy_(host, non_blocking=True)
-        p2 = s.SlicParams(grid=list(grid), weight_m=m, max_iterations=cfg_iters)
-        eng2 = s.Engine(dims, ch, dtype, img2.data_ptr(), p2, slab=slab, data_range=drange,
+        eng2 = s.Engine(dims, ch, dtype, img2.data_ptr(), params, slab=slab, data_range=drange,
                         device=local, stream=stream.cuda_stream)
         loop2 = ShardedLoop(eng2, allreduce, world)
         loop2.init()
@@ -390,6 +473,7 @@ def main():
         host = torch.empty(img.numel(), dtype=tdt, pin_memory=True)
         host.copy_(img)
         labels_h = torch.empty(nvox, dtype=torch.int32, pin_memory=True)
+        eng.close()
         del eng
         torch.cuda.synchronize()
         import ctypes as C
@@ -413,7 +497,7 @@ def main():
                                     cen.ctypes.data_as(C.POINTER(C.c_double)),
                                     res.ctypes.data_as(C.POINTER(C.c_double)), C.byref(done))
         # one untimed call (lazy module loading, allocator growth), then the
-        # mean of `reps` timed calls; each call is a whole run (H2D, init,
+        # median of `reps` timed calls; each call is a whole run (H2D, init,
         # every iteration, D2H of labels/centres/residuals)
         s._check(call())
         reps = 3 if nvox > (1 << 28) else 9
@@ -429,28 +513,26 @@ def main():
                "call": "sslic_run_slic (host buffers, pinned)", "iterations": done.value,
                "seconds_per_call": sec, "timed_calls": reps, "warmup_calls": 1,
                "statistic": "median over timed calls",
-               "seconds_min_max": [min(per_call), max(per_call)]}
+               "seconds_min_max": [min(per_call), max(per_call)],
+               "note": "a step here is one whole call (all configured iterations)"}
 
     cpu = None
     if not args.no_cpu and world == 1 and rank == 0:
         try:
-            sdims, reps = cpu_sample(args.config, dims, ch, dtype)
-            n_s = int(np.prod(sdims))
-            hs = (img[: n_s * ch] if len(dims) == 3 else img).cpu().numpy().view(dtype)
-            v, cores = run_reference_cpu(args.config, reps, 1, hs, sdims, ch, grid, m)
-            cpu = {"value": v, "unit": "voxel-iter/s", "cores": cores, "kind": "reference",
-                   "sample": f"first {sdims[-1] if len(dims) == 3 else dims[-1]} planes "
-                             f"({n_s} voxels) of the same synthetic volume, {reps} timed "
-                             f"iteration(s) after 1 warm-up, reference headers -O3, "
-                             f"{cores} threads"}
+            logical, physical = host_cores()
+            rate, desc, _ = reference_window_rate(args.config, cfg_iters, 0, logical,
+                                                  BASE_SAMPLE)
+            cpu = {"value": rate, "unit": "voxel-iter/s", "cores": logical,
+                   "physical_cores": physical, "kind": "reference", "sample": desc}
         except Exception as exc:  # the baseline is reported, not required
             cpu = {"value": None, "error": str(exc)[:200]}
 
     if rank == 0:
-        line = {"metric": metric, "value": value, "unit": "voxel-iter/s", "n_gpus": world,
+        line = {"metric": METRIC, "value": value, "unit": "voxel-iter/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-                "dtype": "f64" if args.path == "exact" else "f32 filter + f64 exact", "data": "synthetic (seeded device generator)",
+                "dtype": "f64" if args.path == "exact" else "f32 filter + f64 exact",
+                "data": "synthetic (seeded device generator)",
                 "config": config, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clk, "undefined_labels": undefined}
         print(json.dumps(line))

@@ -161,6 +161,10 @@ int sslic_engine_destroy(sslic_engine* e);
  * lies in this slab (zeros elsewhere). With several slabs, sum the tables
  * across ranks (exact: one non-zero term per entry) then commit. */
 int sslic_engine_init(sslic_engine* e);
+/* Back to iteration 0 (every label undefined, zero sums): the same engine
+ * then runs another whole run from sslic_engine_init (bench: timed runs
+ * over the configured iteration window). */
+int sslic_engine_reset(sslic_engine* e);
 int sslic_engine_centers_buffer(sslic_engine* e, double** dev_ptr, int64_t* count);
 int sslic_engine_commit_centers(sslic_engine* e);
 

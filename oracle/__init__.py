@@ -84,7 +84,29 @@ class Oracle:
         lib.orc_enforce_connectivity.restype = C.c_uint32
         lib.orc_enforce_connectivity.argtypes = [C.c_int, _i64p, _u32p, _f64p, C.c_int,
                                                  C.c_int64, _i64p, _u32p]
+        lib.orc_synth_generate.restype = C.c_int
+        lib.orc_synth_generate.argtypes = [C.c_int, C.c_int, _i64p, C.c_int, C.c_uint64,
+                                           C.c_int64, C.c_int64, C.c_void_p, C.c_int]
         self.lib = lib
+
+    def synth_generate(self, config, dims, dtype, channels, seed, z_begin=0, z_end=None,
+                       threads=None):
+        """Planes [z_begin, z_end) of a seeded config volume (the device
+        generator's bytes), as a flat numpy array of the native dtype."""
+        d = _dims(dims)
+        if len(dims) == 2:
+            z_begin, z_end = 0, 1
+        elif z_end is None:
+            z_end = int(dims[-1])
+        plane = int(np.prod(dims[:2])) if len(dims) == 3 else int(np.prod(dims))
+        out = np.empty(plane * (z_end - z_begin) * channels, dtype=dtype)
+        st = self.lib.orc_synth_generate(int(config), len(d), _p(d, _i64p), int(channels),
+                                         int(seed), int(z_begin), int(z_end),
+                                         out.ctypes.data_as(C.c_void_p),
+                                         int(threads or os.cpu_count() or 1))
+        if st != 0:
+            raise ValueError(f"synth_generate: bad shape for config {config}")
+        return out
 
     # -- helpers -----------------------------------------------------------
     @staticmethod

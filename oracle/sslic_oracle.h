@@ -99,6 +99,11 @@ uint32_t orc_enforce_connectivity(int rank, const int64_t* dims, const uint32_t*
                                   const double* centers, int channels, int64_t k,
                                   const int64_t* grid, uint32_t* labels_out);
 
+/* Seeded synthetic config volume (planes [z_begin, z_end)), the same bytes
+ * as the device generator (synth_ref.c; bench reference arm / cpu_baseline). */
+int orc_synth_generate(int config, int rank, const int64_t* dims, int channels, uint64_t seed,
+                       int64_t z_begin, int64_t z_end, void* out, int threads);
+
 #ifdef __cplusplus
 }
 #endif

@@ -134,6 +134,7 @@ def lib():
         "sslic_engine_value_range": (C.c_int, [vp, C.POINTER(C.c_double)]),
         "sslic_engine_set_value_range": (C.c_int, [vp, C.c_double]),
         "sslic_engine_init": (C.c_int, [vp]),
+        "sslic_engine_reset": (C.c_int, [vp]),
         "sslic_engine_centers_buffer": (C.c_int, [vp, C.POINTER(vp), i64p]),
         "sslic_engine_commit_centers": (C.c_int, [vp]),
         "sslic_engine_assign": (C.c_int, [vp]),
@@ -629,6 +630,10 @@ class Engine:
             self.close()
         except Exception:
             pass
+
+    def reset(self):
+        """Back to iteration 0 for another whole run (labels undefined)."""
+        _check(lib().sslic_engine_reset(self.h))
 
     def init(self):
         _check(lib().sslic_engine_init(self.h))

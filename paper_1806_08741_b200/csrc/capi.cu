@@ -1133,6 +1133,14 @@ int sslic_engine_destroy(sslic_engine* e) {
   });
 }
 
+int sslic_engine_reset(sslic_engine* e) {
+  return guarded([&] {
+    SSLIC_CUDA_CHECK(cudaSetDevice(e->e->device()));
+    e->e->reset();
+    return SSLIC_OK;
+  });
+}
+
 int sslic_engine_init(sslic_engine* e) {
   return guarded([&] {
     e->e->init(true);

@@ -215,6 +215,23 @@ double* Engine::current_centers() const {
   return centers_ + (size_t)slot * g_.k * g_.stride;
 }
 
+void Engine::reset() {
+  cudaStream_t s = stream_;
+  const int64_t nv = slab_voxels();
+  iter_ = 0;
+  SSLIC_CUDA_CHECK(cudaMemsetAsync(labels_, 0xff, nv * sizeof(uint32_t), s));
+  SSLIC_CUDA_CHECK(cudaMemsetAsync(sums_, 0, partials_count() * sizeof(unsigned long long), s));
+  SSLIC_CUDA_CHECK(cudaMemsetAsync(acc_, 0, partials_count() * sizeof(unsigned long long), s));
+  acc_zero_ = true;
+  SSLIC_CUDA_CHECK(cudaMemsetAsync(counters_, 0, 8 * sizeof(unsigned long long), s));
+  SSLIC_CUDA_CHECK(cudaMemsetAsync(update_done_, 0, 2 * sizeof(unsigned), s));
+  if (chg_) SSLIC_CUDA_CHECK(cudaMemsetAsync(chg_, 0, g_.k * sizeof(int), s));
+  if (dist_mode_) {
+    k_fill_f64<<<blocks_for(nv, 256), 256, 0, s>>>(dists_, nv, __builtin_huge_val());
+    launch_check("fill dists");
+  }
+}
+
 void Engine::init(bool perturb) {
   k_init_perturb<<<blocks_for(g_.k, 128), 128, 0, stream_>>>(g_, img_, current_centers(),
                                                              perturb ? 1 : 0);

@@ -22,6 +22,9 @@ class Engine {
   Engine(const Engine&) = delete;
   Engine& operator=(const Engine&) = delete;
 
+  // Back to the state after construction (iteration 0, every label
+  // undefined, zero sums), so one engine runs several whole runs.
+  void reset();
   // K1 on the owned clusters (zeros elsewhere).
   void init(bool perturb);
   // Load a caller-given centre table (host) as the current table.

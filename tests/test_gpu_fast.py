@@ -512,3 +512,33 @@ def test_run_slic_pipelined_random_geometry(sslic, case):
     c2, r2 = call(host.ctypes.data, pageable.ctypes.data)
     assert np.array_equal(pinned.numpy().view(np.uint32), pageable)
     assert np.array_equal(c1, c2) and np.array_equal(r1, r2)
+
+
+@pytest.mark.parametrize("exact", [False, True])
+def test_engine_reset_reruns_identically(sslic, exact):
+    """Engine.reset (the bench's whole-run cycling) returns the engine to
+    iteration 0: a second run after reset equals the first bit for bit,
+    fast and exact paths, including a run cut short before the reset."""
+    import torch
+    s = sslic
+    dims, ch, dtype, grid, m, iters = (96, 80, 48), 1, np.uint16, (16, 16, 16), 10.0, 6
+    img, fast, ex = _engines(s, 3, dims, ch, dtype, grid, m, iters, torch)
+    e = ex if exact else fast
+    n = int(np.prod(dims))
+    la = torch.empty(n, dtype=torch.int32, device="cuda")
+
+    def run(k):
+        e.init()
+        e.commit()
+        for _ in range(k):
+            e.assign()
+            e.update()
+        e.labels_to(la.data_ptr())
+        return la.cpu().numpy().copy(), e.centers().copy(), e.residuals().copy()
+
+    l1, c1, r1 = run(iters)
+    e.reset()
+    run(2)
+    e.reset()
+    l2, c2, r2 = run(iters)
+    assert np.array_equal(l1, l2) and np.array_equal(c1, c2) and np.array_equal(r1, r2)
