@@ -218,6 +218,46 @@ int sslic_engine_set_stats(sslic_engine* e, int on);
  * sum_k |W_k ∩ slab| (the algorithmic count). Synchronizes. */
 int sslic_engine_eval_stats(sslic_engine* e, double* evals, double* window_evals);
 
+/* ---- multi-GPU (z-slabs, one NCCL allreduce of the int64 per-cluster
+ * partials per iteration) ------------------------------------
+ * The reference parallelises run_slic(img, params, workers) over slabs with
+ * an ordered merge of per-slab accumulators (slic.hpp:384-415,
+ * parallel.hpp:52-94); here the slabs are z-slabs of a 3-D volume, one per
+ * GPU, and results are bitwise the single-GPU result for any device count. */
+
+/* run_slic over `n_devices` GPUs of this process (devices: their indices, or
+ * NULL for 0..n-1): one host thread per device, ncclCommInitAll. img / labels
+ * / centres / residuals as sslic_run_slic (host buffers, full image).
+ * n_devices > 1 needs a rank-3 image with at least n_devices planes. */
+int sslic_run_slic_multi(const sslic_image* img, const sslic_params* params, int n_devices,
+                         const int* devices, uint32_t* labels_out, double* centers_out,
+                         double* residuals_out, int* iterations_done);
+/* One rank of a one-process-per-GPU job (torchrun): img is the FULL host
+ * image (only this rank's planes + a 2-plane halo are uploaded); labels_out
+ * receives this rank's slab (sslic_slab_bounds); centres / residuals /
+ * iterations_done (nullable) are the same on every rank. nccl_id: the
+ * NCCL_UNIQUE_ID_BYTES from sslic_nccl_unique_id on one rank, given to all
+ * (may be NULL when world == 1: no communicator). Collective: every rank must
+ * call it. */
+int sslic_run_slic_rank(const sslic_image* img, const sslic_params* params, int rank, int world,
+                        const void* nccl_id, int device, uint32_t* labels_out,
+                        double* centers_out, double* residuals_out, int* iterations_done);
+/* ncclGetUniqueId into out (bytes >= 128). */
+int sslic_nccl_unique_id(void* out, int64_t bytes);
+/* The z-slab [lo, hi) of `rank` (slabs rounded to multiples of `align` planes
+ * when there are at least `world` such units). */
+int sslic_slab_bounds(int64_t last, int world, int rank, int64_t align, int64_t* lo,
+                      int64_t* hi);
+/* Attach an NCCL communicator to an engine (collective over the ranks):
+ * sslic_engine_start, _iterate and _iterate_graph then run the value-range
+ * MAX, the SUM of the init tables and the per-iteration SUM of the partials
+ * on the engine's stream (inside the captured graph). nccl_id == NULL (world
+ * 1) detaches. A 1-rank communicator is valid (the NCCL path on one GPU). */
+int sslic_engine_attach_nccl(sslic_engine* e, const void* nccl_id, int rank, int world);
+/* init + perturb of the slab's clusters, the synced table, anchors and bins
+ * (with a communicator: value-range MAX first, table SUM before the commit). */
+int sslic_engine_start(sslic_engine* e);
+
 /* Seeded synthetic volumes for the five BASELINE configs, generated on the
  * device straight into HBM (planes [z_begin, z_end) of the last axis). */
 int sslic_synth_generate(int config, int rank, const int64_t* dims, int channels, int dtype,

@@ -156,6 +156,14 @@ def lib():
                                              C.POINTER(C.c_int)]),
         "sslic_synth_generate": (C.c_int, [C.c_int, C.c_int, i64p, C.c_int, C.c_int, C.c_uint64,
                                            C.c_int64, C.c_int64, vp, vp]),
+        "sslic_run_slic_multi": (C.c_int, [ip, pp, C.c_int, C.POINTER(C.c_int), u32p, f64p, f64p,
+                                           C.POINTER(C.c_int)]),
+        "sslic_run_slic_rank": (C.c_int, [ip, pp, C.c_int, C.c_int, vp, C.c_int, u32p, f64p, f64p,
+                                          C.POINTER(C.c_int)]),
+        "sslic_nccl_unique_id": (C.c_int, [vp, C.c_int64]),
+        "sslic_slab_bounds": (C.c_int, [C.c_int64, C.c_int, C.c_int, C.c_int64, i64p, i64p]),
+        "sslic_engine_attach_nccl": (C.c_int, [vp, vp, C.c_int, C.c_int]),
+        "sslic_engine_start": (C.c_int, [vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -342,6 +350,69 @@ def run_slic(img: NDImage, params: SlicParams, workers: int = 1, device: int = 0
                             _p(centers, C.c_double), _p(res, C.c_double), C.byref(done)))
     return SlicResult(labels, ClusterTable(img.channels, img.rank, centers),
                       list(res[: done.value]))
+
+
+def run_slic_multi(img: NDImage, params: SlicParams, devices: Sequence[int]) -> SlicResult:
+    """run_slic over several GPUs of this process (sslic_run_slic_multi):
+    z-slabs of a 3-D volume, one per device, one NCCL allreduce of the int64
+    per-cluster partials per iteration; bitwise the single-GPU result."""
+    params.validate(img.dims)
+    L = lib()
+    n = img.pixel_count()
+    k = cluster_count(img.dims, params.grid)
+    iters = params.iterations_for(img.rank)
+    labels = np.empty(n, np.uint32)
+    centers = np.empty(k * (img.channels + img.rank))
+    res = np.empty(max(iters, 1))
+    done = C.c_int(0)
+    devs = (C.c_int * len(devices))(*[int(d) for d in devices])
+    d, p = img._desc(), params._c()
+    _check(L.sslic_run_slic_multi(C.byref(d), C.byref(p), len(devices), devs,
+                                  _p(labels, C.c_uint32), _p(centers, C.c_double),
+                                  _p(res, C.c_double), C.byref(done)))
+    return SlicResult(labels, ClusterTable(img.channels, img.rank, centers),
+                      list(res[: done.value]))
+
+
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId (128 bytes), to be shared with every rank."""
+    buf = C.create_string_buffer(128)
+    _check(lib().sslic_nccl_unique_id(buf, 128))
+    return buf.raw
+
+
+def slab_bounds_native(last: int, world: int, rank: int, align: int = 1):
+    """The C ABI's z-slab split (sslic_slab_bounds)."""
+    lo, hi = C.c_int64(), C.c_int64()
+    _check(lib().sslic_slab_bounds(int(last), int(world), int(rank), int(align), C.byref(lo),
+                                   C.byref(hi)))
+    return lo.value, hi.value
+
+
+def run_slic_rank(img: NDImage, params: SlicParams, rank: int, world: int, uid: bytes,
+                  device: int = 0, labels_out=None):
+    """One rank of a one-process-per-GPU run (sslic_run_slic_rank): img is the
+    full host volume; returns (slab labels, SlicResult-like centres/residuals).
+    labels_out: optional preallocated uint32 host buffer (pinned memory works)."""
+    params.validate(img.dims)
+    L = lib()
+    k = cluster_count(img.dims, params.grid)
+    iters = params.iterations_for(img.rank)
+    lo, hi = (slab_bounds_native(img.dims[-1], world, rank, params.grid[-1]) if world > 1
+              else (0, img.dims[-1]))
+    plane = int(np.prod(img.dims[:-1]))
+    labels = labels_out if labels_out is not None else np.empty((hi - lo) * plane, np.uint32)
+    centers = np.empty(k * (img.channels + img.rank))
+    res = np.empty(max(iters, 1))
+    done = C.c_int(0)
+    d, p = img._desc(), params._c()
+    ub = C.create_string_buffer(uid, 128) if uid else None
+    _check(L.sslic_run_slic_rank(C.byref(d), C.byref(p), int(rank), int(world), ub, int(device),
+                                 _p(labels, C.c_uint32) if isinstance(labels, np.ndarray)
+                                 else C.cast(C.c_void_p(labels.data_ptr()),
+                                             C.POINTER(C.c_uint32)),
+                                 _p(centers, C.c_double), _p(res, C.c_double), C.byref(done)))
+    return labels, ClusterTable(img.channels, img.rank, centers), list(res[: done.value])
 
 
 def segment(img: NDImage, params: SlicParams, device: int = 0):
@@ -634,6 +705,16 @@ class Engine:
     def reset(self):
         """Back to iteration 0 for another whole run (labels undefined)."""
         _check(lib().sslic_engine_reset(self.h))
+
+    def attach_nccl(self, uid: bytes, rank: int, world: int):
+        """NCCL communicator for this engine (collective over the ranks):
+        start / iterate / iterate_graph then run the allreduces natively."""
+        ub = C.create_string_buffer(uid, 128) if uid else None
+        _check(lib().sslic_engine_attach_nccl(self.h, ub, int(rank), int(world)))
+
+    def start(self):
+        """init + perturb, the (allreduced) table and its anchors / bins."""
+        _check(lib().sslic_engine_start(self.h))
 
     def init(self):
         _check(lib().sslic_engine_init(self.h))

@@ -667,9 +667,6 @@ __global__ void k_update_from_sums(int64_t k, int stride, const double* sums,
 
 }  // namespace
 
-struct sslic_engine {
-  std::unique_ptr<Engine> e;
-};
 
 extern "C" {
 
@@ -1187,8 +1184,10 @@ int sslic_engine_update(sslic_engine* e) {
 
 int sslic_engine_iterate(sslic_engine* e, int iterations) {
   return guarded([&] {
+    SSLIC_CUDA_CHECK(cudaSetDevice(e->e->device()));
     for (int i = 0; i < iterations; ++i) {
       e->e->assign(true);
+      comm_sum_partials(e->comm, *e->e);  // attached NCCL communicator (multi.cu)
       e->e->update();
     }
     return SSLIC_OK;
@@ -1210,6 +1209,7 @@ int sslic_engine_iterate_graph(sslic_engine* e, int iterations, float* ms_out) {
     try {
       for (int i = 0; i < iterations; ++i) {
         en.assign(true);
+        comm_sum_partials(e->comm, en);  // the NCCL allreduce is a graph node
         en.update();
       }
     } catch (...) {

@@ -2,6 +2,7 @@
 // (run_slic, slic.hpp:384-415) for one slab on one GPU.
 #include <cub/device/device_scan.cuh>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -159,10 +160,25 @@ void Engine::compute_shift() {
   SSLIC_CUDA_CHECK(cudaStreamSynchronize(stream_));
   double m;
   std::memcpy(&m, &bits, sizeof(m));
+  shift_ = fixed_shift(m);
+  vmax_ = m;
+}
+
+// Fixed-point scale 2^shift of float intensities. Each |v| 2^shift stays
+// below 2^(40 - h), where 2^h bounds a cluster's population (its window,
+// prod_a min(2 S_a + 1, dims_a): a voxel only joins a cluster whose window
+// covers it), so every per-cluster int64 sum and delta stays below 2^40 x
+// population <= 2^62 (grid = extent on an 8M-voxel float image
+// used to wrap). h = 0 up to 2^22 members (every fast-path geometry).
+int Engine::fixed_shift(double m) const {
   int e = 0;
   if (m > 0.0) std::frexp(m, &e);  // m < 2^e
-  shift_ = 40 - e;                  // |v| * 2^shift < 2^40
-  vmax_ = m;
+  double pop = 1.0;
+  for (int a = 0; a < g_.rank; ++a)
+    pop *= (double)std::min<int64_t>(2 * g_.grid[a] + 1, g_.dims[a]);
+  int h = 0;
+  while (std::ldexp(1.0, 22 + h) < pop) ++h;
+  return 40 - h - e;
 }
 
 // Parameters derived from the value range: the fixed-point shift of float
@@ -202,9 +218,7 @@ double Engine::value_range() const { return vmax_; }
 void Engine::set_value_range(double m) {
   if (g_.dtype == SSLIC_U8 || g_.dtype == SSLIC_U16) return;  // fixed: dtype max, shift 0
   if (!(m >= 0.0)) throw Error(SSLIC_EINVAL, "engine: value range must be >= 0");
-  int e = 0;
-  if (m > 0.0) std::frexp(m, &e);  // m < 2^e
-  shift_ = 40 - e;
+  shift_ = fixed_shift(m);
   vmax_ = m;
   derive_value_params();
   if (!fast_ok_scale_) path_ = AssignPath::kExact;

@@ -100,6 +100,7 @@ class Engine {
   FastParams fast_params();
   void launch_exact_kernel(bool accumulate, int64_t nv, const double* hist);
   void compute_shift();
+  int fixed_shift(double absmax) const;
   void derive_value_params();
 
   Geom g_{};

@@ -71,7 +71,15 @@ struct FastParams {
   int* region_cand_out;     // same buffer, written by k_region_cand
   int aligned4;       // dims[0] % 4 == 0: 4-voxel runs are vector-aligned
   int max_cand;       // regions with more candidates take the exact crowded path
+  int skip_full;      // k_assign_fast: full regions were done by k_assign_lean
 };
+
+// A region not clipped by the volume or the slab (k_assign_lean's domain).
+__device__ __forceinline__ bool region_full(const FastParams& P, const int64_t* org, int RX,
+                                            int RY, int RZ) {
+  return org[0] + RX <= P.g.dims[0] && org[1] + RY <= P.g.dims[1] &&
+         org[2] >= P.g.slab_begin && org[2] + RZ <= P.g.slab_end;
+}
 
 #ifndef SSLIC_BOX3_X  // (build-time override for layout experiments)
 #define SSLIC_BOX3_X 8

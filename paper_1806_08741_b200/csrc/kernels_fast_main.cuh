@@ -3,6 +3,8 @@
 // DESIGN.md "K2").
 #pragma once
 
+#include <atomic>
+#include <cstdlib>
 #include <type_traits>
 
 #include "kernels_fast.cuh"
@@ -229,6 +231,7 @@ __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fas
   const int rzi = (int)(rb / (unsigned)P.nreg[1]);
   const int64_t org[3] = {(int64_t)rxi * RX, (int64_t)ryi * RY,
                           RANK == 3 ? P.reg_z0 + (int64_t)rzi * RZ : 0};
+  if (RANK == 3 && P.skip_full && region_full(P, org, RX, RY, RZ)) return;  // k_assign_lean's
   const int64_t hi[3] = {min(org[0] + RX, g.dims[0]) - 1, min(org[1] + RY, g.dims[1]) - 1,
                          RANK == 3 ? min(org[2] + RZ, g.dims[2]) - 1 : 0};
   const int64_t zlo = RANK == 3 ? max(org[2], g.slab_begin) : 0;
@@ -1406,16 +1409,79 @@ inline size_t fast_smem_bytes(const Geom& g, const int* R, int cap = kFastMaxCan
   return b;
 }
 
+}  // namespace sslic_b200
+#include "kernels_lean.cuh"
+namespace sslic_b200 {
+
+// k_assign_lean over the full regions (the compile-time shapes of configs 3
+// and 5); returns false when the geometry is not one of them. *all_full:
+// no clipped region exists (k_assign_fast then needs no launch).
+template <int C, typename T, int RXc, int RYc, int RZc, int CAPc, int MINB>
+void launch_lean_shape(const FastParams& P, int64_t nblocks, cudaStream_t s) {
+  auto kern = k_assign_lean<C, T, RXc, RYc, RZc, CAPc, MINB>;
+  static std::atomic<unsigned long long> configured{0};
+  int dev = 0;
+  SSLIC_CUDA_CHECK(cudaGetDevice(&dev));
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (!(configured.load(std::memory_order_acquire) & bit)) {
+    SSLIC_CUDA_CHECK(
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    SSLIC_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                          cudaSharedmemCarveoutMaxShared));
+    configured.fetch_or(bit, std::memory_order_acq_rel);
+  }
+  const int R[3] = {RXc, RYc, RZc};
+  const size_t smem = lean_smem_bytes(P.g, R, CAPc, (int)P.tag_now);
+  kern<<<(unsigned)nblocks, kFastThreads, smem, s>>>(P);
+}
+
+inline bool launch_lean(const FastParams& P, int64_t nblocks, cudaStream_t s) {
+  const Geom& g = P.g;
+  if (g.rank != 3 || !P.aligned4 || std::getenv("SSLIC_NO_LEAN") != nullptr) return false;
+  const int* R = P.R;
+  // config 3 (1 channel, 8.6 evaluations per voxel): measured slower than
+  // k_assign_fast (76.8 vs 83.2 Gvox/s, profiles/r2/lean_ab.txt) -- kept
+  // behind SSLIC_LEAN_C1=1 for experiments; config 5 gains 11 %
+  if (g.channels == 1 && g.dtype == SSLIC_U16 && R[0] == 32 && R[1] == 16 && R[2] == 16 &&
+      std::getenv("SSLIC_LEAN_C1") != nullptr && fast_cand_need(g, R) <= 56 &&
+      P.max_cand >= 56) {
+    FastParams Q = P;
+    Q.max_cand = 56;
+    launch_lean_shape<1, uint16_t, 32, 16, 16, 56, 5>(Q, nblocks, s);  // config 3
+    return true;
+  }
+  if (g.channels == 3 && g.dtype == SSLIC_U8 && R[0] == 32 && R[1] == 32 && R[2] == 32 &&
+      fast_cand_need(g, R) <= 40 && P.max_cand >= 40) {
+    FastParams Q = P;
+    Q.max_cand = 40;
+    launch_lean_shape<3, uint8_t, 32, 32, 32, 40, 4>(Q, nblocks, s);  // config 5
+    return true;
+  }
+  return false;
+}
+
+inline bool all_regions_full(const FastParams& P) {
+  const Geom& g = P.g;
+  if (g.dims[0] % P.R[0] || g.dims[1] % P.R[1]) return false;
+  const int64_t z0 = P.reg_z0, z1 = z0 + (int64_t)P.nreg[2] * P.R[2];
+  return z0 >= g.slab_begin && z1 <= g.slab_end;
+}
+
 template <int RANK, int C, typename T, int RXc, int RYc, int RZc, int CAPc = 0>
 void launch_fast_shape(const FastParams& P, size_t smem, int64_t nblocks, cudaStream_t s) {
   auto kern = k_assign_fast<RANK, C, T, RXc, RYc, RZc, CAPc>;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  // function attributes are per device context: one bit per device
+  static std::atomic<unsigned long long> configured{0};
+  int dev = 0;
+  SSLIC_CUDA_CHECK(cudaGetDevice(&dev));
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (!(configured.load(std::memory_order_acquire) & bit)) {
+    SSLIC_CUDA_CHECK(
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     // all of the unified L1 as shared memory: occupancy is smem/register bound
-    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         cudaSharedmemCarveoutMaxShared);
-    configured = true;
+    SSLIC_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                          cudaSharedmemCarveoutMaxShared));
+    configured.fetch_or(bit, std::memory_order_acq_rel);
   }
   kern<<<(unsigned)nblocks, kFastThreads, smem, s>>>(P);
 }
@@ -1529,6 +1595,12 @@ inline void launch_fast_assign(FastParams P, cudaStream_t s, int64_t row0 = 0,
   P.region_cand_out = const_cast<int*>(P.region_cand);
   if (g.rank == 3) {
     k_region_cand<3><<<(unsigned)((nb + 3) / 4), 128, 0, s>>>(P, nb);
+    // full regions of configs 3 and 5 take k_assign_lean; the clipped ones
+    // (if any) k_assign_fast, which then skips the full ones
+    if (launch_lean(P, nb, s)) {
+      if (all_regions_full(P)) return;
+      P.skip_full = 1;
+    }
     launch_fast_r<3>(P, smem, nb, s);
   } else {
     k_region_cand<2><<<(unsigned)((nb + 3) / 4), 128, 0, s>>>(P, nb);
