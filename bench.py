@@ -18,8 +18,12 @@ untimed run. Inputs (2 GiB image + 4 GiB labels for config 3) exceed L2; the
 L2-resident configs 1-2 flush L2 with a 512 MB write between steps.
 
 Under torchrun (N>1) each rank owns a contiguous z-slab; the one exchange per
-iteration is an NCCL allreduce of the int64 per-cluster partials. Rank 0
-prints ONE JSON line.
+iteration is an NCCL allreduce of the int64 per-cluster partials, issued by
+the library on the engine's own communicator (sslic_engine_attach_nccl) and
+captured with the kernels in each timed span's CUDA graph; torch.distributed
+only carries the NCCL unique id, the barriers and the max-over-ranks timing.
+e2e at N>1 is sslic_run_slic_rank per rank on pinned host planes. Rank 0
+prints ONE JSON line. --nccl runs those N>1 code paths at N=1.
 
 --impl reference times the UNMODIFIED reference's multi-threaded CPU loop
 (oracle/_ref: the reference headers compiled by oracle/Makefile) on the
@@ -124,10 +128,6 @@ def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    # functional check of the N>1 code path on a one-GPU box (gloo, every
-    # rank on device 0); never used for reported numbers
-    if os.environ.get("SSLIC_BENCH_FUNCTIONAL_CHECK") == "1":
-        local = 0
     return world, rank, local
 
 
@@ -236,7 +236,10 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--path", default="auto", choices=["auto", "exact"])
-    ap.add_argument("--no-graph", action="store_true", help="launch steps directly (N=1)")
+    ap.add_argument("--no-graph", action="store_true", help="launch steps directly")
+    ap.add_argument("--nccl", action="store_true",
+                    help="run the N>1 code paths (engine NCCL communicator, run_slic_rank e2e) "
+                         "even at N=1 (functional check on one GPU)")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
@@ -265,12 +268,9 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as tdist
-        if os.environ.get("SSLIC_BENCH_FUNCTIONAL_CHECK") == "1":
-            tdist.init_process_group("gloo")
-        else:
-            tdist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        tdist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     import paper_1806_08741_b200 as s
-    from paper_1806_08741_b200.sharded import ShardedLoop, data_bounds, slab_bounds
+    from paper_1806_08741_b200.sharded import data_bounds, slab_bounds
 
     last = dims[-1]
     slab = slab_bounds(last, world, rank, align=grid[-1]) if len(dims) == 3 else (0, last)
@@ -293,24 +293,30 @@ def main():
                    device=local, stream=stream.cuda_stream)
     if args.path == "exact":
         eng.set_exact(True)
-
-    def allreduce(t):
-        import torch.distributed as tdist
-        tdist.all_reduce(t)
-
-    loop = ShardedLoop(eng, allreduce, world)
+    uid = None
+    multi = world > 1 or args.nccl
+    if multi:
+        # the engine's own NCCL communicator: the value-range MAX, the init
+        # table SUM and the per-iteration SUM of the int64 partials run on the
+        # engine stream (inside the captured graph); torch.distributed only
+        # carries the unique id and the barriers
+        obj = [s.nccl_unique_id() if rank == 0 else None]
+        if world > 1:
+            tdist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+        eng.attach_nccl(uid, rank, world)
 
     def fresh_run():
         eng.reset()
-        loop.init()
+        eng.start()
 
     # warm-up: an untimed run of W iterations (cycling when W > I)
     for j in range(args.warmup):
         if j % cfg_iters == 0:
             fresh_run()
-        loop.iterate()
+        eng.iterate(1)
 
-    graphs = world == 1 and not args.no_graph
+    graphs = not args.no_graph
     config["launch"] = "CUDA graph per timed span" if graphs else "direct launches"
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda") if fits_l2 else None
     # timed spans: one per run (inputs > L2) or one per step (L2-resident)
@@ -343,8 +349,7 @@ def main():
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
-                for _ in range(span):
-                    loop.iterate()
+                eng.iterate(span)
                 e1.record(stream)
                 e1.synchronize()
                 ms += e0.elapsed_time(e1)
@@ -363,7 +368,7 @@ def main():
     fresh_run()
     eng.set_stats(True)
     for i in range(cfg_iters):
-        loop.iterate()
+        eng.iterate(1)
         ev, win = eng.eval_stats()
         amb, _ovf, chg = eng.fast_stats()
         E_it.append(win / nvox if world == 1 else win)
@@ -432,12 +437,13 @@ def main():
 
     # end-to-end through the reference-facing C ABI with HOST buffers
     e2e = None
-    if not args.no_e2e and world > 1:
-        # N GPUs: the public multi-GPU API end to end on every rank — H2D of
-        # the rank's slab (+ halo) from pinned host memory, engine setup,
-        # init + all iterations with the NCCL allreduce, D2H of the slab's
-        # labels; wall time between barriers, max over ranks.
-        import torch.distributed as tdist
+    if not args.no_e2e and multi:
+        # N GPUs: the public multi-GPU entry point end to end on every rank
+        # (sslic_run_slic_rank): H2D of the rank's planes (slab + halo) from
+        # pinned host memory, engine setup, a fresh NCCL communicator, init +
+        # every iteration with the allreduce, D2H of the slab's labels and the
+        # centres; one warm-up call, then one timed call between barriers,
+        # max over ranks.
         host = torch.empty(img.numel(), dtype=tdt, pin_memory=True)
         host.copy_(img)
         slab_vox_e = (slab[1] - slab[0]) * plane
@@ -445,31 +451,31 @@ def main():
         eng.close()
         del eng
         torch.cuda.synchronize()
-        tdist.barrier()
+        hp = (dims, host.data_ptr(), drange[0], ch, dtype)
+
+        def call():
+            o = [s.nccl_unique_id() if rank == 0 else None]
+            if world > 1:
+                tdist.broadcast_object_list(o, src=0)
+            return s.run_slic_rank(None, params, rank, world, o[0], device=local,
+                                   labels_out=labels_h, host_planes=hp)
+        call()
+        if world > 1:
+            tdist.barrier()
         t0 = time.perf_counter()
-        img2 = torch.empty_like(img)
-        img2.copy_(host, non_blocking=True)
-        eng2 = s.Engine(dims, ch, dtype, img2.data_ptr(), params, slab=slab, data_range=drange,
-                        device=local, stream=stream.cuda_stream)
-        loop2 = ShardedLoop(eng2, allreduce, world)
-        loop2.init()
-        for _ in range(cfg_iters):
-            loop2.iterate()
-        lab_d = torch.empty(slab_vox_e, dtype=torch.int32, device="cuda")
-        eng2.labels_to(lab_d.data_ptr())
-        labels_h.copy_(lab_d)
-        torch.cuda.synchronize()
+        _, cen_e, _ = call()
         dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
-        tdist.all_reduce(dt, op=tdist.ReduceOp.MAX)
+        if world > 1:
+            tdist.all_reduce(dt, op=tdist.ReduceOp.MAX)
         sec = float(dt.item())
         e2e = {"value": nvox * cfg_iters / sec, "unit": "voxel-iter/s",
                "h2d_bytes_per_step": img.numel() * img.element_size(),
-               "d2h_bytes_per_step": slab_vox_e * 4,
-               "call": "Engine + ShardedLoop per rank (host buffers, pinned), NCCL allreduce",
+               "d2h_bytes_per_step": slab_vox_e * 4 + cen_e.data.nbytes,
+               "call": "sslic_run_slic_rank per rank (pinned host planes, own NCCL "
+                       "communicator created inside the call)",
                "iterations": cfg_iters, "seconds_per_call": sec, "timed_calls": 1,
-               "note": "bytes are per rank"}
-        eng2.close()
-    if not args.no_e2e and world == 1:
+               "warmup_calls": 1, "note": "bytes are per rank"}
+    if not args.no_e2e and not multi:
         host = torch.empty(img.numel(), dtype=tdt, pin_memory=True)
         host.copy_(img)
         labels_h = torch.empty(nvox, dtype=torch.int32, pin_memory=True)

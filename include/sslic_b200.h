@@ -232,16 +232,21 @@ int sslic_engine_eval_stats(sslic_engine* e, double* evals, double* window_evals
 int sslic_run_slic_multi(const sslic_image* img, const sslic_params* params, int n_devices,
                          const int* devices, uint32_t* labels_out, double* centers_out,
                          double* residuals_out, int* iterations_done);
-/* One rank of a one-process-per-GPU job (torchrun): img is the FULL host
- * image (only this rank's planes + a 2-plane halo are uploaded); labels_out
+/* One rank of a one-process-per-GPU job (torchrun): img->dims are the FULL
+ * image; img->data points at plane `data_first_plane` of it (0: the whole
+ * host image) and must hold this rank's slab plus a 2-plane halo (only those
+ * planes are uploaded, sslic_slab_bounds gives the slab); labels_out
  * receives this rank's slab (sslic_slab_bounds); centres / residuals /
  * iterations_done (nullable) are the same on every rank. nccl_id: the
  * NCCL_UNIQUE_ID_BYTES from sslic_nccl_unique_id on one rank, given to all
  * (may be NULL when world == 1: no communicator). Collective: every rank must
  * call it. */
 int sslic_run_slic_rank(const sslic_image* img, const sslic_params* params, int rank, int world,
-                        const void* nccl_id, int device, uint32_t* labels_out,
-                        double* centers_out, double* residuals_out, int* iterations_done);
+                        const void* nccl_id, int device, int64_t data_first_plane,
+                        uint32_t* labels_out, double* centers_out, double* residuals_out,
+                        int* iterations_done);
+/* Number of visible CUDA devices (0 when none). */
+int sslic_device_count(void);
 /* ncclGetUniqueId into out (bytes >= 128). */
 int sslic_nccl_unique_id(void* out, int64_t bytes);
 /* The z-slab [lo, hi) of `rank` (slabs rounded to multiples of `align` planes

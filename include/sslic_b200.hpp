@@ -7,7 +7,10 @@
 // path to the B200 path is a namespace change:
 //
 //   sslic::SlicResult r = sslic::run_slic(img, params, workers);        // CPU
-//   sslic::SlicResult r = sslic::b200::run_slic(img, params);           // B200
+//   sslic::SlicResult r = sslic::b200::run_slic(img, params, workers);  // B200(s)
+//
+// (`workers` keeps its reference meaning and caps the GPU count; see
+// run_slic below. run_slic_on_device picks one device explicitly.)
 //
 // Errors are rethrown as the reference's exception classes
 // (std::invalid_argument / std::logic_error / std::out_of_range), CUDA
@@ -99,8 +102,8 @@ inline sslic_params params_of(const SlicParams& p) {
 
 }  // namespace detail
 
-/// run_slic (slic.hpp:384-415) on a B200. `device` replaces `workers`.
-inline SlicResult run_slic(const NDImage& img, const SlicParams& params, int device = 0) {
+/// run_slic (slic.hpp:384-415) on ONE given device.
+inline SlicResult run_slic_on_device(const NDImage& img, const SlicParams& params, int device) {
   params.validate(img.dims());  // same exceptions as the reference, before any copy
   detail::NativeImage nimg = detail::narrow(img);
   const sslic_params p = detail::params_of(params);
@@ -114,6 +117,39 @@ inline SlicResult run_slic(const NDImage& img, const SlicParams& params, int dev
   int done = 0;
   detail::check(sslic_run_slic(&nimg.desc, &p, device, labels.data().data(),
                                table.data().data(), residuals.data(), &done));
+  residuals.resize(done);
+  return SlicResult{std::move(labels), std::move(table), std::move(residuals)};
+}
+
+/// run_slic (slic.hpp:384-415) on B200s, same signature as the reference.
+/// `workers` keeps its meaning -- the degree of parallelism, >= 1
+/// (slic.hpp:386, same std::invalid_argument) -- and caps how many GPUs share
+/// the work: a 3-D volume of at least 2^26 voxels is split into
+/// min(workers, visible devices, planes) z-slabs, one per GPU, with one NCCL
+/// allreduce of the per-cluster partials per iteration
+/// (sslic_run_slic_multi); anything smaller runs on device 0. The result is
+/// bitwise the same for any count, as the reference's is for any worker
+/// count (parallel.hpp:1-8).
+inline SlicResult run_slic(const NDImage& img, const SlicParams& params, int workers = 1) {
+  params.validate(img.dims());
+  if (workers < 1) throw std::invalid_argument("run_slic: workers must be >= 1");
+  int n_dev = std::min(workers, sslic_device_count());
+  const int64_t n = static_cast<int64_t>(img.pixel_count());
+  if (img.rank() != 3 || n < (int64_t(1) << 26)) n_dev = 1;
+  if (n_dev > 1) n_dev = static_cast<int>(std::min<int64_t>(n_dev, img.dims()[2]));
+  if (n_dev <= 1) return run_slic_on_device(img, params, 0);
+  detail::NativeImage nimg = detail::narrow(img);
+  const sslic_params p = detail::params_of(params);
+  const int iters = params.iterations_for(img.rank());
+  std::vector<int64_t> dims(img.dims().begin(), img.dims().end());
+  std::vector<int64_t> grid(params.grid.begin(), params.grid.end());
+  ClusterTable table(img.channels(), img.rank(),
+                     sslic_cluster_count(img.rank(), dims.data(), grid.data()));
+  LabelMap labels(img.dims());
+  std::vector<double> residuals(iters > 0 ? iters : 1);
+  int done = 0;
+  detail::check(sslic_run_slic_multi(&nimg.desc, &p, n_dev, nullptr, labels.data().data(),
+                                     table.data().data(), residuals.data(), &done));
   residuals.resize(done);
   return SlicResult{std::move(labels), std::move(table), std::move(residuals)};
 }

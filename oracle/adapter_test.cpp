@@ -29,7 +29,7 @@ int main() {
     params.grid = oracle::random_grid(rng, img.dims());
     params.weight_m = oracle::random_weight(rng);
     const sslic::SlicResult cpu = sslic::run_slic(img, params, 2);
-    const sslic::SlicResult gpu = sslic::b200::run_slic(img, params);
+    const sslic::SlicResult gpu = sslic::b200::run_slic(img, params, 2);  // namespace switch only
     const sslic::LabelMap cc_cpu = sslic::enforce_connectivity(cpu.labels, cpu.centers, params, 2);
     const sslic::LabelMap cc_gpu = sslic::b200::enforce_connectivity(gpu.labels, gpu.centers, params);
     const bool ok = cpu.labels == gpu.labels && cpu.centers == gpu.centers && cc_cpu == cc_gpu &&
@@ -92,6 +92,13 @@ int main() {
     sslic::SlicParams bad;
     bad.grid = sslic::GridSize{9, 8};
     sslic::b200::run_slic(sslic::NDImage::zeros(sslic::Shape{8, 8}, 1), bad);
+    ++failures;
+  } catch (const std::invalid_argument&) {
+  }
+  try {  // workers keeps its meaning: >= 1 (slic.hpp:386)
+    sslic::SlicParams ok;
+    ok.grid = sslic::GridSize{4, 4};
+    sslic::b200::run_slic(sslic::NDImage::zeros(sslic::Shape{8, 8}, 1), ok, 0);
     ++failures;
   } catch (const std::invalid_argument&) {
   }

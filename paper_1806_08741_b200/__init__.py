@@ -158,8 +158,9 @@ def lib():
                                            C.c_int64, C.c_int64, vp, vp]),
         "sslic_run_slic_multi": (C.c_int, [ip, pp, C.c_int, C.POINTER(C.c_int), u32p, f64p, f64p,
                                            C.POINTER(C.c_int)]),
-        "sslic_run_slic_rank": (C.c_int, [ip, pp, C.c_int, C.c_int, vp, C.c_int, u32p, f64p, f64p,
-                                          C.POINTER(C.c_int)]),
+        "sslic_run_slic_rank": (C.c_int, [ip, pp, C.c_int, C.c_int, vp, C.c_int, C.c_int64, u32p,
+                                          f64p, f64p, C.POINTER(C.c_int)]),
+        "sslic_device_count": (C.c_int, []),
         "sslic_nccl_unique_id": (C.c_int, [vp, C.c_int64]),
         "sslic_slab_bounds": (C.c_int, [C.c_int64, C.c_int, C.c_int, C.c_int64, i64p, i64p]),
         "sslic_engine_attach_nccl": (C.c_int, [vp, vp, C.c_int, C.c_int]),
@@ -390,29 +391,42 @@ def slab_bounds_native(last: int, world: int, rank: int, align: int = 1):
 
 
 def run_slic_rank(img: NDImage, params: SlicParams, rank: int, world: int, uid: bytes,
-                  device: int = 0, labels_out=None):
-    """One rank of a one-process-per-GPU run (sslic_run_slic_rank): img is the
-    full host volume; returns (slab labels, SlicResult-like centres/residuals).
-    labels_out: optional preallocated uint32 host buffer (pinned memory works)."""
-    params.validate(img.dims)
+                  device: int = 0, labels_out=None, host_planes=None):
+    """One rank of a one-process-per-GPU run (sslic_run_slic_rank). img: the
+    full volume, or (host_planes=(dims, data_ptr, first_plane)) a raw host
+    buffer holding planes [first_plane, ...) of it, e.g. pinned memory with
+    just this rank's slab and halo. Returns (slab labels, centres, residuals);
+    labels_out: optional preallocated uint32 buffer (numpy or pinned torch)."""
     L = lib()
-    k = cluster_count(img.dims, params.grid)
-    iters = params.iterations_for(img.rank)
-    lo, hi = (slab_bounds_native(img.dims[-1], world, rank, params.grid[-1]) if world > 1
-              else (0, img.dims[-1]))
-    plane = int(np.prod(img.dims[:-1]))
+    if host_planes is None:
+        params.validate(img.dims)
+        desc, first, dims, ch = img._desc(), 0, img.dims, img.channels
+    else:
+        dims, data_ptr, first, ch, dtype = host_planes
+        desc = _Image()
+        desc.rank = len(dims)
+        for a in range(4):
+            desc.dims[a] = dims[a] if a < len(dims) else 1
+        desc.channels = ch
+        desc.dtype = _DT[np.dtype(dtype)]
+        desc.data = data_ptr
+    k = cluster_count(dims, params.grid)
+    iters = params.iterations_for(len(dims))
+    lo, hi = (slab_bounds_native(dims[-1], world, rank, params.grid[-1]) if world > 1
+              else (0, dims[-1]))
+    plane = int(np.prod(dims[:-1]))
     labels = labels_out if labels_out is not None else np.empty((hi - lo) * plane, np.uint32)
-    centers = np.empty(k * (img.channels + img.rank))
+    centers = np.empty(k * (ch + len(dims)))
     res = np.empty(max(iters, 1))
     done = C.c_int(0)
-    d, p = img._desc(), params._c()
+    p = params._c()
     ub = C.create_string_buffer(uid, 128) if uid else None
-    _check(L.sslic_run_slic_rank(C.byref(d), C.byref(p), int(rank), int(world), ub, int(device),
-                                 _p(labels, C.c_uint32) if isinstance(labels, np.ndarray)
-                                 else C.cast(C.c_void_p(labels.data_ptr()),
-                                             C.POINTER(C.c_uint32)),
-                                 _p(centers, C.c_double), _p(res, C.c_double), C.byref(done)))
-    return labels, ClusterTable(img.channels, img.rank, centers), list(res[: done.value])
+    lp = (_p(labels, C.c_uint32) if isinstance(labels, np.ndarray)
+          else C.cast(C.c_void_p(labels.data_ptr()), C.POINTER(C.c_uint32)))
+    _check(L.sslic_run_slic_rank(C.byref(desc), C.byref(p), int(rank), int(world), ub,
+                                 int(device), int(first), lp, _p(centers, C.c_double),
+                                 _p(res, C.c_double), C.byref(done)))
+    return labels, ClusterTable(ch, len(dims), centers), list(res[: done.value])
 
 
 def segment(img: NDImage, params: SlicParams, device: int = 0):

@@ -240,7 +240,31 @@ static __global__ void k_bin_sort(int64_t ncells, const int* cell_start, int* it
   const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (c >= ncells) return;
   const int b = cell_start[c], e = cell_start[c + 1];
-  for (int i = b + 1; i < e; ++i) {
+  if (e - b > 32) {  // crowded cell (degenerate tables): heapsort, O(n log n) worst case
+    int* a = items + b;
+    const int n = e - b;
+    auto sift = [&](int root, int end) {
+      for (;;) {
+        int child = 2 * root + 1;
+        if (child >= end) return;
+        if (child + 1 < end && a[child + 1] > a[child]) ++child;
+        if (a[root] >= a[child]) return;
+        const int t = a[root];
+        a[root] = a[child];
+        a[child] = t;
+        root = child;
+      }
+    };
+    for (int i = n / 2 - 1; i >= 0; --i) sift(i, n);
+    for (int end = n - 1; end > 0; --end) {
+      const int t = a[0];
+      a[0] = a[end];
+      a[end] = t;
+      sift(0, end);
+    }
+    return;
+  }
+  for (int i = b + 1; i < e; ++i) {  // typical cells hold one or two clusters
     const int v = items[i];
     int j = i - 1;
     while (j >= b && items[j] > v) {
@@ -608,7 +632,31 @@ static __global__ void k_bin_sort_reset(int64_t ncells, const int* cell_start, i
   if (c == ncells) return;
   cursor[c] = 0;
   const int b = cell_start[c], e = cell_start[c + 1];
-  for (int i = b + 1; i < e; ++i) {
+  if (e - b > 32) {  // crowded cell (degenerate tables): heapsort, O(n log n) worst case
+    int* a = items + b;
+    const int n = e - b;
+    auto sift = [&](int root, int end) {
+      for (;;) {
+        int child = 2 * root + 1;
+        if (child >= end) return;
+        if (child + 1 < end && a[child + 1] > a[child]) ++child;
+        if (a[root] >= a[child]) return;
+        const int t = a[root];
+        a[root] = a[child];
+        a[child] = t;
+        root = child;
+      }
+    };
+    for (int i = n / 2 - 1; i >= 0; --i) sift(i, n);
+    for (int end = n - 1; end > 0; --end) {
+      const int t = a[0];
+      a[0] = a[end];
+      a[end] = t;
+      sift(0, end);
+    }
+    return;
+  }
+  for (int i = b + 1; i < e; ++i) {  // typical cells hold one or two clusters
     const int v = items[i];
     int j = i - 1;
     while (j >= b && items[j] > v) {

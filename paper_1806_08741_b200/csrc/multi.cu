@@ -167,7 +167,7 @@ void check_rank_args(const sslic_image* img, int world) {
 // labels_out: this rank's slab (host). centers/residuals/done: nullable.
 void run_rank(const sslic_image* img, const sslic_params* p, int rank, int world, RankComm* comm,
               int device, uint32_t* labels_out, double* centers_out, double* residuals_out,
-              int* done_out) {
+              int* done_out, int64_t data_first_plane = 0) {
   RankStream st(device);
   const int last_axis = img->rank - 1;
   const int64_t last = img->dims[last_axis];
@@ -177,8 +177,10 @@ void run_rank(const sslic_image* img, const sslic_params* p, int rank, int world
   int64_t plane = 1;
   for (int a = 0; a < last_axis; ++a) plane *= img->dims[a];
   const size_t plane_bytes = (size_t)plane * img->channels * dsize(img->dtype);
+  if (d0 < data_first_plane)
+    throw Error(SSLIC_EINVAL, "run_slic_rank: host planes must cover the slab plus its halo");
   DevMem dimg((size_t)(d1 - d0) * plane_bytes, st.s);
-  SSLIC_CUDA_CHECK(cudaMemcpyAsync(dimg.p, static_cast<const char*>(img->data) + d0 * plane_bytes,
+  SSLIC_CUDA_CHECK(cudaMemcpyAsync(dimg.p, static_cast<const char*>(img->data) + (d0 - data_first_plane) * plane_bytes,
                                    (size_t)(d1 - d0) * plane_bytes, cudaMemcpyHostToDevice, st.s));
   if (img->dtype == SSLIC_F32 || img->dtype == SSLIC_F64) {  // NDImage checks (image.hpp:238-249)
     DevMem cnt(sizeof(unsigned long long), st.s);
@@ -231,6 +233,15 @@ void run_rank(const sslic_image* img, const sslic_params* p, int rank, int world
 }  // namespace sslic_b200
 
 extern "C" {
+
+int sslic_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
 
 int sslic_nccl_unique_id(void* out, int64_t bytes) {
   return guarded([&] {
@@ -315,8 +326,9 @@ int sslic_run_slic_multi(const sslic_image* img, const sslic_params* params, int
 }
 
 int sslic_run_slic_rank(const sslic_image* img, const sslic_params* params, int rank, int world,
-                        const void* nccl_id, int device, uint32_t* labels_out,
-                        double* centers_out, double* residuals_out, int* iterations_done) {
+                        const void* nccl_id, int device, int64_t data_first_plane,
+                        uint32_t* labels_out, double* centers_out, double* residuals_out,
+                        int* iterations_done) {
   return guarded([&] {
     if (!img || !params || !labels_out) throw Error(SSLIC_EINVAL, "run_slic_rank: null argument");
     if (rank < 0 || rank >= world) throw Error(SSLIC_EINVAL, "run_slic_rank: bad rank");
@@ -331,8 +343,9 @@ int sslic_run_slic_rank(const sslic_image* img, const sslic_params* params, int 
       SSLIC_NCCL_CHECK(ncclCommInitRank(&comm, world, id, rank));
       own.c = make_comm(comm, rank, world);
     }
+    if (data_first_plane < 0) throw Error(SSLIC_EINVAL, "run_slic_rank: negative first plane");
     run_rank(img, params, rank, world, own.c, device, labels_out, centers_out, residuals_out,
-             iterations_done);
+             iterations_done, data_first_plane);
     return SSLIC_OK;
   });
 }

@@ -7,6 +7,33 @@ rep = sys.argv[1]
 def run(args):
     return subprocess.run(["ncu", "-i", rep] + args, capture_output=True, text=True).stdout
 
+raw = list(csv.reader(io.StringIO(run(["--page", "raw", "--csv"]))))
+if len(raw) > 2:
+    h, v = raw[0], raw[2]
+    print("kernel:", v[h.index("Kernel Name")] if "Kernel Name" in h else "?")
+    for w in ["gpu__time_duration.sum", "smsp__inst_executed.sum", "launch__registers_per_thread",
+              "launch__occupancy_limit_registers", "launch__occupancy_limit_shared_mem",
+              "launch__shared_mem_per_block_dynamic",
+              "sm__warps_active.avg.pct_of_peak_sustained_active",
+              "smsp__issue_active.avg.pct_of_peak_sustained_active",
+              "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+              "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+              "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+              "dram__bytes_read.sum", "dram__bytes_write.sum"]:
+        if w in h:
+            print(f"  {w:58s} {v[h.index(w)]} {raw[1][h.index(w)]}")
+    print("stall reasons (warp-cycles per issued instruction):")
+    st = []
+    for i, name in enumerate(h):
+        if name.startswith("smsp__average_warps_issue_stalled_") and name.endswith(
+                "_per_issue_active.ratio"):
+            try:
+                st.append((float(v[i]), name[len("smsp__average_warps_issue_stalled_"):
+                                             -len("_per_issue_active.ratio")]))
+            except ValueError:
+                pass
+    for val, name in sorted(st, reverse=True)[:10]:
+        print(f"  {name:28s} {val:.3f}")
 det = run(["--page", "details", "--csv"])
 keys = ["Duration", "Executed Ipc Active", "Issue Slots Busy", "Warp Cycles Per Issued Instruction",
         "No Eligible", "Registers Per Thread", "Achieved Occupancy", "DRAM Throughput",
