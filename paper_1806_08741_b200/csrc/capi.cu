@@ -749,27 +749,29 @@ int sslic_segment(const sslic_image* img, const sslic_params* params, int device
     validate_image(img);
     validate_params(params, img);
     Stream st(device);
+    PhaseTimer pt("segment");
     auto dimg = upload_image(img, st);
     const sslic_image v = device_view(img, dimg->p);
     const int64_t last = img->dims[img->rank - 1];
     Engine e(v, *params, device, 0, last, 0, last, st.s);
     const int done = run_loop(e, params, st);
+    pt.mark(st, "upload + iterations");
     const int64_t n = pixel_count(*img);
-    DeviceBuf lab(n * sizeof(uint32_t), st.s);
-    e.unpack_labels(lab.as<uint32_t>());
+    // Memory-lean tail (config 5: 17.4 G voxels): the image is no longer
+    // read, the label words are unpacked in place and relabelled in place,
+    // so the connectivity pass needs only the node ids on top of the map.
+    dimg.reset();
+    uint32_t* lab = e.label_words();
+    e.unpack_labels(lab);
     uint32_t next = (uint32_t)e.geom().k;
     if (params->enforce_connectivity) {
-      DeviceBuf out(n * sizeof(uint32_t), st.s);
-      next = enforce_connectivity_device(e.geom(), lab.as<uint32_t>(), e.current_centers(),
-                                         out.as<uint32_t>(), st.s);
-      SSLIC_CUDA_CHECK(cudaMemcpyAsync(labels_out, out.p, n * sizeof(uint32_t),
-                                       cudaMemcpyDeviceToHost, st.s));
-      st.sync();
-    } else {
-      SSLIC_CUDA_CHECK(cudaMemcpyAsync(labels_out, lab.p, n * sizeof(uint32_t),
-                                       cudaMemcpyDeviceToHost, st.s));
-      st.sync();
+      next = enforce_connectivity_device(e.geom(), lab, e.current_centers(), lab, st.s);
+      pt.mark(st, "connectivity");
     }
+    SSLIC_CUDA_CHECK(cudaMemcpyAsync(labels_out, lab, n * sizeof(uint32_t),
+                                     cudaMemcpyDeviceToHost, st.s));
+    st.sync();
+    pt.mark(st, "labels D2H");
     e.copy_centers_to_host(centers_out);
     if (residuals_out) e.residuals_to_host(residuals_out, done);
     if (iterations_done) *iterations_done = done;
@@ -1083,15 +1085,15 @@ int sslic_enforce_connectivity(int rank, const int64_t* dims, const uint32_t* la
     g.slab_begin = g.data_begin = 0;
     g.slab_end = g.data_end = g.dims[rank - 1];
     const int64_t n = acc;
-    DeviceBuf din(n * sizeof(uint32_t), st.s), dout(n * sizeof(uint32_t), st.s),
-        dc(k * g.stride * sizeof(double), st.s);
+    // relabelled in place on the device (4 bytes per voxel + the node ids)
+    DeviceBuf din(n * sizeof(uint32_t), st.s), dc(k * g.stride * sizeof(double), st.s);
     SSLIC_CUDA_CHECK(cudaMemcpyAsync(din.p, labels_in, n * sizeof(uint32_t),
                                      cudaMemcpyHostToDevice, st.s));
     SSLIC_CUDA_CHECK(cudaMemcpyAsync(dc.p, centers, k * g.stride * sizeof(double),
                                      cudaMemcpyHostToDevice, st.s));
     const uint32_t next = enforce_connectivity_device(g, din.as<uint32_t>(), dc.as<double>(),
-                                                      dout.as<uint32_t>(), st.s);
-    SSLIC_CUDA_CHECK(cudaMemcpyAsync(labels_out, dout.p, n * sizeof(uint32_t),
+                                                      din.as<uint32_t>(), st.s);
+    SSLIC_CUDA_CHECK(cudaMemcpyAsync(labels_out, din.p, n * sizeof(uint32_t),
                                      cudaMemcpyDeviceToHost, st.s));
     st.sync();
     if (next_label_out) *next_label_out = next;

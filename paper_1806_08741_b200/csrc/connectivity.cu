@@ -1,9 +1,14 @@
 // Connectivity enforcement (connectivity.hpp:125-273), entirely on the device.
 //
-// 1. Face-connected component labelling of the label map: lock-free
-//    union-find (atomicMin hooking; a component's root is its smallest flat
-//    offset), then the components are numbered densely in root order, so a
-//    node id orders components exactly like the raster sweep reaches them.
+// 1. Face-connected component labelling of the label map, slab by slab along
+//    the last axis (32-bit local offsets per slab): lock-free union-find
+//    (atomicMin hooking; a component's root is its smallest flat offset),
+//    then the components are numbered densely in root order, so a node id
+//    orders components exactly like the raster sweep reaches them. Volumes of
+//    2^32 voxels or more take several slabs: their components are stitched
+//    across the slab faces by a union-find over node ids (a set's smallest
+//    node id is its smallest root offset) and renumbered densely, which gives
+//    the same ids a whole-volume labelling would (SURVEY §2 "C2").
 // 2. finalize_cluster_components (connectivity.hpp:125-173): one thread per
 //    cluster (seed search, "final if size > floor(prod S / 4)").
 // 3. sweep_relabel (connectivity.hpp:182-261) as a fixpoint over the
@@ -27,11 +32,19 @@
 //    until no pending pixel remains, then the fixpoint takes over. Label maps
 //    holding ids >= k (never produced by run_slic) are swept entirely by that
 //    device thread, because fresh ids could then collide with input labels.
+//
+// Voxel offsets are `Off` (uint32_t below 2^32 voxels, uint64_t above);
+// component (node) ids are 32-bit. Per voxel the pass needs the label map and
+// one node id (8 bytes); labels_out may alias labels_in.
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
 
+#include <algorithm>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <memory>
+#include <vector>
 
 #include "connectivity.cuh"
 
@@ -48,27 +61,35 @@ constexpr uint8_t kProc = 4;    // decided by the sequential prefix
 constexpr uint8_t kFixed = 8;   // final label fixed by the prefix (flab)
 constexpr uint8_t kAbs = 16;    // absorbed by the extension fill of its label
 
+// Geometry: the last axis is the slab axis; the in-plane extent is < 2^32.
+template <class Off>
 struct CG {
   int rank;
-  uint32_t dims[kMaxRank];
-  uint32_t strides[kMaxRank];
-  uint32_t n;
+  Off dims[kMaxRank];
+  Off strides[kMaxRank];
+  Off n;
+  Off plane;  // product of the in-plane extents (1 for rank 1)
 };
 
-__device__ __forceinline__ void decode(const CG& g, uint32_t p, uint32_t* c) {
+template <class Off>
+__device__ __forceinline__ void decode(const CG<Off>& g, Off p, Off* c) {
+  const Off z = p / g.plane;
+  uint32_t i = (uint32_t)(p - z * g.plane);
 #pragma unroll
-  for (int a = 0; a < kMaxRank; ++a) {
-    if (a < g.rank) {
-      c[a] = p % g.dims[a];
-      p /= g.dims[a];
+  for (int a = 0; a < kMaxRank - 1; ++a) {
+    if (a < g.rank - 1) {
+      const uint32_t d = (uint32_t)g.dims[a];
+      c[a] = i % d;
+      i /= d;
     }
   }
+  c[g.rank - 1] = z;
 }
 
 // Calls f(q) for every face neighbour q of p.
-template <class F>
-__device__ __forceinline__ void for_neighbours(const CG& g, uint32_t p, F&& f) {
-  uint32_t c[kMaxRank];
+template <class Off, class F>
+__device__ __forceinline__ void for_neighbours(const CG<Off>& g, Off p, F&& f) {
+  Off c[kMaxRank];
   decode(g, p, c);
 #pragma unroll
   for (int a = 0; a < kMaxRank; ++a) {
@@ -104,17 +125,22 @@ __device__ __forceinline__ void unite(uint32_t* parent, uint32_t a, uint32_t b) 
   }
 }
 
-#define GRID_STRIDE(i, n)                                                     \
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (n); \
-       i += (int64_t)gridDim.x * blockDim.x)
+// grid-stride loop over [0, n) with a 64-bit counter (a 32-bit one would wrap
+// past 2^32 near n); the body sees `i` as a T (the inner one-trip loop keeps
+// `continue` meaning "next element")
+#define GRID_STRIDE(T, i, n)                                                           \
+  for (uint64_t i##_g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;               \
+       i##_g < (uint64_t)(n); i##_g += (uint64_t)gridDim.x * blockDim.x)               \
+    for (T i = (T)i##_g, i##_once = 1; i##_once; i##_once = 0)
 
+// ---- slab CCL (32-bit local offsets) ------------------------------------------
 __global__ void k_cc_init(uint32_t* parent, uint32_t n) {
-  GRID_STRIDE(i, n) parent[i] = (uint32_t)i;
+  GRID_STRIDE(uint32_t, i, n) parent[i] = i;
 }
 
-__global__ void k_cc_union(CG g, const uint32_t* labels, uint32_t* parent) {
-  GRID_STRIDE(i, g.n) {
-    const uint32_t p = (uint32_t)i, l = labels[p];
+__global__ void k_cc_union(CG<uint32_t> g, const uint32_t* labels, uint32_t* parent) {
+  GRID_STRIDE(uint32_t, p, g.n) {
+    const uint32_t l = labels[p];
     uint32_t c[kMaxRank];
     decode(g, p, c);
 #pragma unroll
@@ -126,31 +152,74 @@ __global__ void k_cc_union(CG g, const uint32_t* labels, uint32_t* parent) {
 
 // parent -> root; idx[p] = 1 for roots (scanned into dense node ids)
 __global__ void k_cc_flatten(uint32_t* parent, uint32_t* idx, uint32_t n) {
-  GRID_STRIDE(i, n) {
-    const uint32_t r = find_root(parent, (uint32_t)i);
+  GRID_STRIDE(uint32_t, i, n) {
+    const uint32_t r = find_root(parent, i);
     parent[i] = r;
-    idx[i] = r == (uint32_t)i;
+    idx[i] = r == i;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) idx[n] = 0;
 }
 
-// parent[p] (root offset) -> node id, in place; node_off/size/label per node
+// parent[p] (local root) -> global node id (base + dense local id), in place;
+// node_off (global flat offset of the root), nlab and size per node
+// component sizes are 32-bit; a component of 2^32 voxels or more sets *ovf
+__device__ __forceinline__ void add_size(uint32_t* size, uint32_t id, uint32_t v, unsigned* ovf) {
+  const uint32_t old = atomicAdd(size + id, v);
+  if (old + v < old) *ovf = 1;
+}
+
+template <class Off>
 __global__ void k_node_ids(uint32_t* nid, const uint32_t* idx, const uint32_t* labels,
-                           uint32_t* node_off, uint32_t* size, uint32_t* nlab, uint32_t n) {
-  GRID_STRIDE(i, n) {
+                           Off* node_off, uint32_t* size, uint32_t* nlab, uint32_t n,
+                           uint32_t base, Off off0, unsigned* ovf) {
+  GRID_STRIDE(uint32_t, i, n) {
     const uint32_t r = nid[i];
-    const uint32_t id = idx[r];
+    const uint32_t id = base + idx[r];
     nid[i] = id;
-    if (r == (uint32_t)i) {
-      node_off[id] = r;
+    if (r == i) {
+      node_off[id] = off0 + (Off)r;
       nlab[id] = labels[r];
     }
     const unsigned same = __match_any_sync(__activemask(), id);
-    if ((threadIdx.x & 31) == (unsigned)(__ffs(same) - 1)) atomicAdd(size + id, __popc(same));
+    if ((threadIdx.x & 31) == (unsigned)(__ffs(same) - 1)) add_size(size, id, __popc(same), ovf);
   }
 }
 
+// ---- stitching across slab faces (node-level union-find) ---------------------
+template <class Off>
+__global__ void k_face_union(const uint32_t* labels, const uint32_t* nid, Off below, Off above,
+                             uint32_t plane, uint32_t* parent) {
+  GRID_STRIDE(uint32_t, i, plane) {
+    const Off p = below + i, q = above + i;
+    if (labels[p] == labels[q]) unite(parent, nid[p], nid[q]);
+  }
+}
+
+__global__ void k_node_flatten(uint32_t* parent, uint32_t* flag, uint8_t* root, uint32_t m) {
+  GRID_STRIDE(uint32_t, i, m) {
+    const uint32_t r = find_root(parent, i);
+    parent[i] = r;
+    flag[i] = r == i;
+    root[i] = r == i;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) flag[m] = 0;
+}
+
+// a merged set's size goes to its root entry (non-roots are only read)
+__global__ void k_size_to_root(uint32_t m, const uint32_t* parent, uint32_t* size, unsigned* ovf) {
+  GRID_STRIDE(uint32_t, i, m) {
+    const uint32_t r = parent[i];
+    if (r != i) add_size(size, r, size[i], ovf);
+  }
+}
+
+template <class Off>
+__global__ void k_nid_remap(uint32_t* nid, const uint32_t* parent, const uint32_t* fid, Off n) {
+  GRID_STRIDE(Off, i, n) nid[i] = fid[parent[nid[i]]];
+}
+
 // finalize_cluster_components (connectivity.hpp:125-173), one thread per k.
+template <class Off>
 __global__ void k_finalize(Geom g, const uint32_t* labels, const double* centers,
                            const uint32_t* nid, const uint32_t* size, int64_t min_size,
                            uint8_t* flags, uint32_t* fcomp) {
@@ -201,48 +270,55 @@ __global__ void k_finalize(Geom g, const uint32_t* labels, const double* centers
   }
 }
 
-__global__ void k_max_label(const uint32_t* labels, uint32_t n, unsigned* out) {
+template <class Off>
+__global__ void k_max_label(const uint32_t* labels, Off n, unsigned* out) {
   uint32_t m = 0;
-  GRID_STRIDE(i, n) m = max(m, labels[i]);
+  GRID_STRIDE(Off, i, n) m = max(m, labels[i]);
   m = __reduce_max_sync(0xffffffffu, m);
   if ((threadIdx.x & 31) == 0) atomicMax(out, m);
 }
 
 // Largest neighbour offset below the component's root (the merge target of
 // a small component: every pixel before the root is final when the sweep
-// reaches it), and for the component at offset 0 the smallest finalized
-// neighbour offset (best_after, connectivity.hpp:231-233).
-__global__ void k_best_before(CG g, const uint32_t* nid, const uint32_t* node_off,
-                              const uint8_t* flags, uint32_t* bb, uint32_t* ba0) {
-  GRID_STRIDE(i, g.n) {
-    const uint32_t p = (uint32_t)i, d = nid[p];
-    uint32_t best = 0, after = kNone;
+// reaches it), kept as the distance back from the root (< the plane stride,
+// so 32 bits; 0xffffffff: none) and minimised; for the component at offset
+// 0 the smallest finalized neighbour offset (best_after, connectivity.hpp:
+// 231-233).
+template <class Off>
+__global__ void k_best_before(CG<Off> g, const uint32_t* nid, const Off* node_off,
+                              const uint8_t* flags, uint32_t* back, unsigned long long* ba0) {
+  GRID_STRIDE(Off, p, g.n) {
+    const uint32_t d = nid[p];
+    uint32_t best = kNone;
+    unsigned long long after = ~0ull;
     if (!(flags[d] & kFin)) {
-      const uint32_t r = node_off[d];
-      for_neighbours(g, p, [&](uint32_t q) {
-        if (q < r) best = max(best, q + 1);
-        if (d == 0 && nid[q] != d && (flags[nid[q]] & kFin)) after = min(after, q);
+      const Off r = node_off[d];
+      for_neighbours(g, p, [&](Off q) {
+        if (q < r) best = min(best, (uint32_t)(r - q));
+        if (d == 0 && nid[q] != d && (flags[nid[q]] & kFin)) after = min(after, (unsigned long long)q);
       });
     }
-    if (best) atomicMax(bb + d, best);
-    if (after != kNone) atomicMin(ba0, after);
+    if (best != kNone) atomicMin(back + d, best);
+    if (after != ~0ull) atomicMin(ba0, after);
   }
 }
 
 // Static pointers and flags per node.
+template <class Off>
 __global__ void k_pointers(uint32_t m, int64_t min_size, const uint32_t* nid,
-                           const uint32_t* size, const uint32_t* bb, const uint32_t* ba0,
-                           uint8_t* flags, uint32_t* ptr, unsigned* pending) {
-  GRID_STRIDE(i, m) {
+                           const uint32_t* size, const uint32_t* back,
+                           const Off* node_off, const unsigned long long* ba0, uint8_t* flags,
+                           uint32_t* ptr, unsigned* pending) {
+  GRID_STRIDE(uint32_t, i, m) {
     uint8_t f = flags[i];
-    uint32_t p = (uint32_t)i;
+    uint32_t p = i;
     if (!(f & kFin)) {
       if ((int64_t)size[i] > min_size || m == 1) {
         f |= kFresh;
-      } else if (bb[i]) {
-        p = nid[bb[i] - 1];
-      } else if (*ba0 != kNone) {  // i == 0: merge ahead (best_after)
-        p = nid[*ba0];
+      } else if (back[i] != kNone) {
+        p = nid[node_off[i] - (Off)back[i]];
+      } else if (*ba0 != ~0ull) {  // i == 0: merge ahead (best_after)
+        p = nid[(Off)*ba0];
       } else {
         *pending = 1;  // pending adoption at offset 0
       }
@@ -256,35 +332,41 @@ __global__ void k_pointers(uint32_t m, int64_t min_size, const uint32_t* nid,
 // connectivity.hpp:182-261 verbatim in behaviour, used (a) for the pending
 // cascade at the start of the raster and (b) for label maps with ids >= k.
 // cur: labels (in/out); mk: bit 0 final, bit 1 visited, bit 2 touched by an
-// event; queue: n entries. Unless `full`, stops at the first offset > 0 where
-// every touched pixel is final (no pending region left).
-__global__ void k_sweep_serial(CG g, uint32_t* cur, uint8_t* mk,
-                               uint32_t* queue, int64_t min_size, uint32_t next, int full,
-                               uint32_t* result /* [0] = stop offset, [1] = next label */) {
+// event; queue: qcap entries. Unless `full`, stops at the first offset > 0
+// where every touched pixel is final (no pending region left).
+template <class Off>
+__global__ void k_sweep_serial(CG<Off> g, uint32_t* cur, uint8_t* mk, Off* queue, Off qcap,
+                               int64_t min_size, uint32_t next, int full,
+                               unsigned long long* result /* [0] stop, [1] next, [2] overflow */) {
   if (blockIdx.x != 0 || threadIdx.x != 0) return;
   int64_t pending = 0;
-  uint32_t off = 0;
+  Off off = 0;
   while (off < g.n && (full || off == 0 || pending > 0)) {
     if (mk[off] & 1) {
       ++off;
       continue;
     }
     const uint32_t label = cur[off];
-    uint32_t len = 0;
+    Off len = 0;
     queue[len++] = off;
     mk[off] |= 2;
-    for (uint32_t head = 0; head < len; ++head) {
-      for_neighbours(g, queue[head], [&](uint32_t q) {
+    for (Off head = 0; head < len; ++head) {
+      for_neighbours(g, queue[head], [&](Off q) {
         if (!(mk[q] & 2) && cur[q] == label) {
           mk[q] |= 2;
-          queue[len++] = q;
+          if (len < qcap) queue[len] = q;
+          ++len;
         }
       });
+      if (len > qcap) {
+        result[2] = 1;
+        return;
+      }
     }
     int64_t bb = -1, ba = -1, bp = -1;
     uint32_t lb = 0, la = 0, lp = 0;
-    for (uint32_t h = 0; h < len; ++h) {
-      for_neighbours(g, queue[h], [&](uint32_t q) {
+    for (Off h = 0; h < len; ++h) {
+      for_neighbours(g, queue[h], [&](Off q) {
         const uint32_t lq = cur[q];
         if (lq == label) return;
         if (mk[q] & 1) {
@@ -316,8 +398,8 @@ __global__ void k_sweep_serial(CG g, uint32_t* cur, uint8_t* mk,
       target = next++;
     }
     // pending = touched pixels that are not final yet (bit 2 = touched)
-    for (uint32_t h = 0; h < len; ++h) {
-      const uint32_t o = queue[h];
+    for (Off h = 0; h < len; ++h) {
+      const Off o = queue[h];
       const uint8_t w = mk[o];
       const bool was = (w & 4) && !(w & 1);
       cur[o] = target;
@@ -326,23 +408,26 @@ __global__ void k_sweep_serial(CG g, uint32_t* cur, uint8_t* mk,
     }
     ++off;
   }
-  result[0] = off;
+  result[0] = (unsigned long long)off;
   result[1] = next;
 }
 
-__global__ void k_markers(const uint32_t* nid, const uint8_t* flags, uint8_t* mk, uint32_t n) {
-  GRID_STRIDE(i, n) mk[i] = flags[nid[i]] & kFin;
+template <class Off>
+__global__ void k_markers(const uint32_t* nid, const uint8_t* flags, uint8_t* mk, Off n) {
+  GRID_STRIDE(Off, i, n) mk[i] = flags[nid[i]] & kFin;
 }
 
 // Components the prefix decided: pointer into F_label (merged into its
 // region) or a fixed fresh label; a finalized component the prefix relabelled
 // retires its label from the fixpoint.
-__global__ void k_prefix_nodes(uint32_t m, const uint32_t* node_off, const uint32_t* nlab,
+template <class Off>
+__global__ void k_prefix_nodes(uint32_t m, const Off* node_off, const uint32_t* nlab,
                                const uint32_t* cur, const uint8_t* mk, uint32_t k,
                                const uint32_t* fcomp, uint8_t* flags, uint32_t* ptr,
                                uint32_t* flab, uint8_t* factive, unsigned* err) {
-  GRID_STRIDE(i, m) {
-    const uint32_t r = node_off[i], lam = cur[r];
+  GRID_STRIDE(uint32_t, i, m) {
+    const Off r = node_off[i];
+    const uint32_t lam = cur[r];
     uint8_t f = flags[i];
     if (f & kFin) {
       if (lam != nlab[i]) {
@@ -355,7 +440,7 @@ __global__ void k_prefix_nodes(uint32_t m, const uint32_t* node_off, const uint3
       if (lam >= k) {
         f |= kFixed;
         flab[i] = lam;
-        ptr[i] = (uint32_t)i;
+        ptr[i] = i;
       } else if (fcomp[lam] != kNone) {
         ptr[i] = fcomp[lam];
       } else {
@@ -370,12 +455,12 @@ __global__ void k_prefix_nodes(uint32_t m, const uint32_t* node_off, const uint3
 __global__ void k_round_ptr(uint32_t m, const uint8_t* flags, const uint32_t* ptr,
                             const uint32_t* nlab, const uint32_t* fcomp, const uint8_t* factive,
                             const uint32_t* te, uint32_t* T) {
-  GRID_STRIDE(i, m) {
+  GRID_STRIDE(uint32_t, i, m) {
     const uint8_t f = flags[i];
     uint32_t t = ptr[i];
     if (!(f & (kFin | kProc))) {
       const uint32_t l = nlab[i];
-      if (factive[l] && fcomp[l] != kNone && (te[l] == (uint32_t)i || (f & kAbs))) t = fcomp[l];
+      if (factive[l] && fcomp[l] != kNone && (te[l] == i || (f & kAbs))) t = fcomp[l];
     }
     T[i] = t;
   }
@@ -384,7 +469,7 @@ __global__ void k_round_ptr(uint32_t m, const uint8_t* flags, const uint32_t* pt
 // Pointer jumping towards the terminals (each thread chases a few hops).
 __global__ void k_jump(uint32_t m, uint32_t* T, unsigned* changed) {
   bool ch = false;
-  GRID_STRIDE(i, m) {
+  GRID_STRIDE(uint32_t, i, m) {
     uint32_t t = T[i];
 #pragma unroll 1
     for (int h = 0; h < 8; ++h) {
@@ -400,11 +485,12 @@ __global__ void k_jump(uint32_t m, uint32_t* T, unsigned* changed) {
 
 // One pass over the face edges: extension candidates (te_new) and absorbed
 // components (against the previous round's te).
-__global__ void k_edges(CG g, const uint32_t* nid, const uint8_t* flags, const uint32_t* nlab,
-                        const uint32_t* fcomp, const uint8_t* factive, const uint32_t* T,
-                        const uint32_t* te, uint32_t* te_new, uint8_t* absn) {
-  GRID_STRIDE(i, g.n) {
-    const uint32_t p = (uint32_t)i, d = nid[p];
+template <class Off>
+__global__ void k_edges(CG<Off> g, const uint32_t* nid, const uint8_t* flags,
+                        const uint32_t* nlab, const uint32_t* fcomp, const uint8_t* factive,
+                        const uint32_t* T, const uint32_t* te, uint32_t* te_new, uint8_t* absn) {
+  GRID_STRIDE(Off, p, g.n) {
+    const uint32_t d = nid[p];
     if (flags[d] & (kFin | kProc)) continue;
     const uint32_t l = nlab[d];
     if (!factive[l]) continue;
@@ -412,7 +498,7 @@ __global__ void k_edges(CG g, const uint32_t* nid, const uint8_t* flags, const u
     if (f == kNone) continue;
     const uint32_t t0 = te[l];
     bool cand = false, ab = false;
-    for_neighbours(g, p, [&](uint32_t q) {
+    for_neighbours(g, p, [&](Off q) {
       const uint32_t x = nid[q];
       if (x == d || T[x] != f) return;
       const bool proc = flags[x] & kProc;
@@ -425,7 +511,7 @@ __global__ void k_edges(CG g, const uint32_t* nid, const uint8_t* flags, const u
 }
 
 __global__ void k_swap_te(uint32_t k, uint32_t* te, uint32_t* te_new, unsigned* changed) {
-  GRID_STRIDE(i, k) {
+  GRID_STRIDE(uint32_t, i, k) {
     if (te[i] != te_new[i]) {
       te[i] = te_new[i];
       *changed = 1;
@@ -435,7 +521,7 @@ __global__ void k_swap_te(uint32_t k, uint32_t* te, uint32_t* te_new, unsigned* 
 }
 
 __global__ void k_swap_abs(uint32_t m, uint8_t* flags, uint8_t* absn, unsigned* changed) {
-  GRID_STRIDE(i, m) {
+  GRID_STRIDE(uint32_t, i, m) {
     const uint8_t f = flags[i];
     const bool a = absn[i] != 0, b = (f & kAbs) != 0;
     if (a != b) {
@@ -458,9 +544,9 @@ __device__ __forceinline__ bool is_ext(uint32_t i, uint8_t f, const uint32_t* nl
 __global__ void k_events(uint32_t m, const uint8_t* flags, const uint32_t* nlab,
                          const uint32_t* fcomp, const uint8_t* factive, const uint32_t* te,
                          uint32_t* ev) {
-  GRID_STRIDE(i, m) {
+  GRID_STRIDE(uint32_t, i, m) {
     const uint8_t f = flags[i];
-    ev[i] = is_ext((uint32_t)i, f, nlab, fcomp, factive, te) ||
+    ev[i] = is_ext(i, f, nlab, fcomp, factive, te) ||
             (!(f & (kFin | kProc)) && (f & kFresh) && !(f & kAbs));
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) ev[m] = 0;
@@ -470,22 +556,23 @@ __global__ void k_final_labels(uint32_t m, const uint8_t* flags, const uint32_t*
                                const uint32_t* fcomp, const uint8_t* factive,
                                const uint32_t* te, const uint32_t* rank, uint32_t next0,
                                uint32_t* flab) {
-  GRID_STRIDE(i, m) {
+  GRID_STRIDE(uint32_t, i, m) {
     const uint8_t f = flags[i];
     if (f & kFixed) continue;
     if (f & kFin) {
       const uint32_t l = nlab[i];
       flab[i] = (factive[l] && te[l] != kNone) ? next0 + rank[te[l]] : l;
     } else if (!(f & kProc) && (f & kFresh) && !(f & kAbs) &&
-               !is_ext((uint32_t)i, f, nlab, fcomp, factive, te)) {
+               !is_ext(i, f, nlab, fcomp, factive, te)) {
       flab[i] = next0 + rank[i];
     }
   }
 }
 
+template <class Off>
 __global__ void k_output(const uint32_t* nid, const uint32_t* T, const uint32_t* flab,
-                         uint32_t* out, uint32_t n) {
-  GRID_STRIDE(i, n) out[i] = flab[T[nid[i]]];
+                         uint32_t* out, Off n) {
+  GRID_STRIDE(Off, i, n) out[i] = flab[T[nid[i]]];
 }
 
 // Stream-ordered device allocation owned for the scope of one call.
@@ -495,8 +582,10 @@ struct Scratch {
   Scratch(size_t bytes, cudaStream_t st) : s(st) {
     SSLIC_CUDA_CHECK(cudaMallocAsync(&p, bytes ? bytes : 1, st));
   }
-  ~Scratch() {
+  ~Scratch() { release(); }
+  void release() {
     if (p) cudaFreeAsync(p, s);
+    p = nullptr;
   }
   Scratch(const Scratch&) = delete;
   Scratch& operator=(const Scratch&) = delete;
@@ -517,88 +606,204 @@ T read_scalar(const T* d, cudaStream_t s) {
   return h;
 }
 
-}  // namespace
+template <class Off>
+CG<Off> make_cg(const Geom& g, int64_t z0, int64_t z1) {
+  CG<Off> c{};
+  c.rank = g.rank;
+  int64_t plane = 1;
+  for (int a = 0; a < kMaxRank; ++a) {
+    c.dims[a] = a < g.rank ? (Off)g.dims[a] : 1;
+    c.strides[a] = a < g.rank ? (Off)g.strides[a] : 0;
+  }
+  for (int a = 0; a + 1 < g.rank; ++a) plane *= g.dims[a];
+  c.dims[g.rank - 1] = (Off)(z1 - z0);
+  c.plane = (Off)plane;
+  c.n = (Off)(plane * (z1 - z0));
+  return c;
+}
 
-uint32_t enforce_connectivity_device(const Geom& g, const uint32_t* labels_in,
-                                     const double* centers, uint32_t* labels_out,
-                                     cudaStream_t s) {
+// Planes per CCL slab: the whole image below 2^31 voxels (one slab), else
+// slabs of at most 2^30 voxels (32-bit local offsets and a 4 GB scan
+// buffer). SSLIC_CC_SLAB_PLANES forces a slab height (tests of the
+// stitching on small volumes).
+int64_t slab_planes(const Geom& g, int64_t plane, int64_t last) {
+  if (const char* e = std::getenv("SSLIC_CC_SLAB_PLANES")) {
+    const int64_t v = std::atoll(e);
+    if (v > 0) return std::min(v, last);
+  }
+  if (plane * last < ((int64_t)1 << 31)) return last;
+  const int64_t p = ((int64_t)1 << 30) / plane;
+  if (p < 1) throw Error(SSLIC_EINVAL, "enforce_connectivity: one plane holds >= 2^30 voxels");
+  return std::min(p, last);
+}
+
+template <class Off>
+uint32_t connectivity_impl(const Geom& g, const uint32_t* labels_in, const double* centers,
+                           uint32_t* labels_out, cudaStream_t s) {
   int64_t n64 = 1;
   for (int a = 0; a < g.rank; ++a) n64 *= g.dims[a];
-  if (n64 >= (int64_t)0xffffffffLL)
-    throw Error(SSLIC_EINVAL, "enforce_connectivity: volumes >= 2^32 voxels need the slab path");
-  const uint32_t n = (uint32_t)n64;
+  const Off n = (Off)n64;
   int64_t min_size = 1;
   for (int a = 0; a < g.rank; ++a) min_size *= g.grid[a];
   min_size /= 4;  // size_threshold (connectivity.hpp:34-38)
   const uint32_t k = (uint32_t)g.k;
   const bool timing = std::getenv("SSLIC_TIMING") != nullptr;
   const auto t0 = std::chrono::steady_clock::now();
+  const int last_axis = g.rank - 1;
+  const int64_t last = g.dims[last_axis];
+  int64_t plane = 1;
+  for (int a = 0; a < last_axis; ++a) plane *= g.dims[a];
+  const CG<Off> cg = make_cg<Off>(g, 0, last);
 
-  CG cg{};
-  cg.rank = g.rank;
-  cg.n = n;
-  for (int a = 0; a < kMaxRank; ++a) {
-    cg.dims[a] = a < g.rank ? (uint32_t)g.dims[a] : 1;
-    cg.strides[a] = a < g.rank ? (uint32_t)g.strides[a] : 0;
-  }
-  // small control block: [0] max label, [1] pending, [2] changed, [3] err,
-  // [4] ba0, [5..6] serial result
+  // small control block: [0] max label, [1] pending, [2] changed, [3] err
   Scratch ctl(8 * sizeof(unsigned), s);
   unsigned* c = ctl.as<unsigned>();
   SSLIC_CUDA_CHECK(cudaMemsetAsync(c, 0, 8 * sizeof(unsigned), s));
-  SSLIC_CUDA_CHECK(cudaMemsetAsync(c + 4, 0xff, sizeof(unsigned), s));
+  Scratch ull(4 * sizeof(unsigned long long), s);  // [0] best_after of node 0, [1..3] serial
+  unsigned long long* cu = ull.as<unsigned long long>();
+  SSLIC_CUDA_CHECK(cudaMemsetAsync(cu, 0, 4 * sizeof(unsigned long long), s));
+  SSLIC_CUDA_CHECK(cudaMemsetAsync(cu, 0xff, sizeof(unsigned long long), s));
+  k_max_label<Off><<<148 * 8, 256, 0, s>>>(labels_in, n, c + 0);
 
-  Scratch nid_b((size_t)n * 4, s), idx_b(((size_t)n + 1) * 4, s);
+  // ---- 1. CCL per slab, node ids in raster order ----
+  const int64_t sp = slab_planes(g, plane, last);
+  const int nslabs = (int)((last + sp - 1) / sp);
+  const int64_t slab_max = sp * plane;
+  Scratch nid_b((size_t)n64 * 4, s), idx_b(((size_t)slab_max + 1) * 4, s);
   uint32_t* nid = nid_b.as<uint32_t>();
   uint32_t* idx = idx_b.as<uint32_t>();
-  k_cc_init<<<blocks(n), 256, 0, s>>>(nid, n);
-  k_cc_union<<<blocks(n), 256, 0, s>>>(cg, labels_in, nid);
-  k_cc_flatten<<<blocks(n), 256, 0, s>>>(nid, idx, n);
   size_t tmp_bytes = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, idx, idx, (int64_t)n + 1, s);
-  Scratch tmp(tmp_bytes, s);
-  SSLIC_CUDA_CHECK(
-      cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, idx, idx, (int64_t)n + 1, s));
-  k_max_label<<<148 * 8, 256, 0, s>>>(labels_in, n, c + 0);
-  SSLIC_CUDA_CHECK(cudaGetLastError());
-  const uint32_t m = read_scalar(idx + n, s);
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, idx, idx, slab_max + 1, s);
+  std::vector<uint32_t> slab_m(nslabs);
+  auto slab_ccl = [&](int si) {  // -> nid[slab] = local roots, idx = scanned root flags
+    const int64_t z0 = si * sp, z1 = std::min(last, z0 + sp);
+    const CG<uint32_t> sg = make_cg<uint32_t>(g, z0, z1);
+    uint32_t* par = nid + z0 * plane;
+    const uint32_t* lab = labels_in + z0 * plane;
+    k_cc_init<<<blocks(sg.n), 256, 0, s>>>(par, sg.n);
+    k_cc_union<<<blocks(sg.n), 256, 0, s>>>(sg, lab, par);
+    k_cc_flatten<<<blocks(sg.n), 256, 0, s>>>(par, idx, sg.n);
+    return sg.n;
+  };
+  uint64_t m_total = 0;
+  {
+    Scratch tmp(tmp_bytes, s);
+    for (int si = 0; si < nslabs; ++si) {
+      const uint32_t ns = slab_ccl(si);
+      SSLIC_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, idx, idx, (int64_t)ns + 1, s));
+      slab_m[si] = read_scalar(idx + ns, s);
+      m_total += slab_m[si];
+    }
+  }
+  if (m_total >= kNone) throw Error(SSLIC_EINVAL, "enforce_connectivity: >= 2^32 components");
+  uint32_t m = (uint32_t)m_total;
   const unsigned max_label = read_scalar(c + 0, s);
-
-  // per-node arrays
-  Scratch node_off_b((size_t)m * 4, s), size_b((size_t)m * 4, s), nlab_b((size_t)m * 4, s),
-      ptr_b((size_t)m * 4, s), T_b((size_t)m * 4, s), flab_b((size_t)m * 4, s),
+  // per-node arrays (node_off / nlab / size are compacted in place after
+  // stitching; ptr / T / flags double as the stitching scratch)
+  Scratch node_off_b((size_t)m * sizeof(Off), s), nlab_b((size_t)m * 4, s),
+      size_b(((size_t)m + 1) * 4, s);
+  Scratch ptr_b((size_t)m * 4, s), T_b(((size_t)m + 1) * 4, s), flab_b((size_t)m * 4, s),
       flags_b(m, s), absn_b(m, s);
-  uint32_t *node_off = node_off_b.as<uint32_t>(), *size = size_b.as<uint32_t>(),
-           *nlab = nlab_b.as<uint32_t>(), *ptr = ptr_b.as<uint32_t>(), *T = T_b.as<uint32_t>(),
-           *flab = flab_b.as<uint32_t>();
+  SSLIC_CUDA_CHECK(cudaMemsetAsync(size_b.p, 0, (size_t)m * 4, s));
+  {
+    Scratch tmp(tmp_bytes, s);
+    uint32_t base = 0;
+    for (int si = 0; si < nslabs; ++si) {
+      const int64_t z0 = si * sp;
+      uint32_t ns;
+      if (nslabs > 1) {  // the first pass's roots were overwritten by the next slab's scan
+        ns = slab_ccl(si);
+        SSLIC_CUDA_CHECK(
+            cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, idx, idx, (int64_t)ns + 1, s));
+      } else {
+        ns = (uint32_t)(plane * last);
+      }
+      k_node_ids<Off><<<blocks(ns), 256, 0, s>>>(nid + z0 * plane, idx, labels_in + z0 * plane,
+                                                node_off_b.as<Off>(), size_b.as<uint32_t>(),
+                                                nlab_b.as<uint32_t>(), ns, base,
+                                                (Off)(z0 * plane), c + 4);
+      base += slab_m[si];
+    }
+  }
+  idx_b.release();
+  if (nslabs > 1) {
+    // stitch the slab faces: union of the node ids of face-adjacent voxels
+    // with equal labels; the smallest node id of a set holds its root offset
+    uint32_t* par = ptr_b.as<uint32_t>();
+    uint32_t* fid = T_b.as<uint32_t>();
+    uint8_t* isroot = flags_b.as<uint8_t>();
+    k_cc_init<<<blocks(m), 256, 0, s>>>(par, m);
+    for (int si = 1; si < nslabs; ++si) {
+      const int64_t zb = si * sp;
+      k_face_union<Off><<<blocks(plane), 256, 0, s>>>(labels_in, nid, (Off)((zb - 1) * plane),
+                                                      (Off)(zb * plane), (uint32_t)plane, par);
+    }
+    k_node_flatten<<<blocks(m), 256, 0, s>>>(par, fid, isroot, m);
+    {
+      size_t tb = 0;
+      cub::DeviceScan::ExclusiveSum(nullptr, tb, fid, fid, (int64_t)m + 1, s);
+      Scratch tmp(tb, s);
+      SSLIC_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, fid, fid, (int64_t)m + 1, s));
+    }
+    const uint32_t mf = read_scalar(fid + m, s);
+    k_nid_remap<Off><<<blocks(n64), 256, 0, s>>>(nid, par, fid, n);
+    k_size_to_root<<<blocks(m), 256, 0, s>>>(m, par, size_b.as<uint32_t>(), c + 4);
+    // keep the root entries, in place, in node order (= final id order)
+    {
+      Scratch nsel_b(sizeof(long long), s);
+      long long* nsel = nsel_b.as<long long>();
+      size_t tb = 0, t2 = 0, t3 = 0;
+      cub::DeviceSelect::Flagged(nullptr, tb, node_off_b.as<Off>(), isroot, nsel, (int64_t)m, s);
+      cub::DeviceSelect::Flagged(nullptr, t2, nlab_b.as<uint32_t>(), isroot, nsel, (int64_t)m, s);
+      cub::DeviceSelect::Flagged(nullptr, t3, size_b.as<uint32_t>(), isroot, nsel, (int64_t)m, s);
+      Scratch tmp(std::max(tb, std::max(t2, t3)), s);
+      size_t tbb = std::max(tb, std::max(t2, t3));
+      SSLIC_CUDA_CHECK(cub::DeviceSelect::Flagged(tmp.p, tbb, node_off_b.as<Off>(), isroot, nsel,
+                                                  (int64_t)m, s));
+      tbb = std::max(tb, std::max(t2, t3));
+      SSLIC_CUDA_CHECK(cub::DeviceSelect::Flagged(tmp.p, tbb, nlab_b.as<uint32_t>(), isroot,
+                                                  nsel, (int64_t)m, s));
+      tbb = std::max(tb, std::max(t2, t3));
+      SSLIC_CUDA_CHECK(cub::DeviceSelect::Flagged(tmp.p, tbb, size_b.as<uint32_t>(), isroot,
+                                                  nsel, (int64_t)m, s));
+    }
+    SSLIC_CUDA_CHECK(cudaGetLastError());
+    m = mf;
+  }
+  if (read_scalar(c + 4, s) != 0)
+    throw Error(SSLIC_EINVAL, "enforce_connectivity: a component holds >= 2^32 voxels");
+  const Off* node_off = node_off_b.as<Off>();
+  const uint32_t* nlab = nlab_b.as<uint32_t>();
+  uint32_t* size = size_b.as<uint32_t>();
+
+  // ---- 2. finalize; 3. static pointers ----
+  uint32_t *ptr = ptr_b.as<uint32_t>(), *T = T_b.as<uint32_t>(), *flab = flab_b.as<uint32_t>();
   uint8_t *flags = flags_b.as<uint8_t>(), *absn = absn_b.as<uint8_t>();
   const size_t kk = k ? k : 1;
   Scratch fcomp_b(kk * 4, s), te_b(kk * 4, s), te_new_b(kk * 4, s), factive_b(kk, s);
   uint32_t *fcomp = fcomp_b.as<uint32_t>(), *te = te_b.as<uint32_t>(),
            *te_new = te_new_b.as<uint32_t>();
   uint8_t* factive = factive_b.as<uint8_t>();
-  SSLIC_CUDA_CHECK(cudaMemsetAsync(size, 0, (size_t)m * 4, s));
   SSLIC_CUDA_CHECK(cudaMemsetAsync(flags, 0, m, s));
   SSLIC_CUDA_CHECK(cudaMemsetAsync(absn, 0, m, s));
-  SSLIC_CUDA_CHECK(cudaMemsetAsync(flab, 0, (size_t)m * 4, s));
   SSLIC_CUDA_CHECK(cudaMemsetAsync(fcomp, 0xff, kk * 4, s));
   SSLIC_CUDA_CHECK(cudaMemsetAsync(te, 0xff, kk * 4, s));
   SSLIC_CUDA_CHECK(cudaMemsetAsync(te_new, 0xff, kk * 4, s));
   SSLIC_CUDA_CHECK(cudaMemsetAsync(factive, 1, kk, s));
-  k_node_ids<<<blocks(n), 256, 0, s>>>(nid, idx, labels_in, node_off, size, nlab, n);
   if (g.k > 0)
-    k_finalize<<<(unsigned)((g.k + 127) / 128), 128, 0, s>>>(g, labels_in, centers, nid, size,
-                                                             min_size, flags, fcomp);
+    k_finalize<Off><<<(unsigned)((g.k + 127) / 128), 128, 0, s>>>(g, labels_in, centers, nid, size,
+                                                                   min_size, flags, fcomp);
   SSLIC_CUDA_CHECK(cudaGetLastError());
   const bool full_serial = m > 0 && (uint64_t)max_label >= (uint64_t)k;
 
   uint32_t next = k;
   bool done = false;
   if (!full_serial) {
-    // bb -> ptr (flab doubles as bb storage until the end)
-    k_best_before<<<blocks(n), 256, 0, s>>>(cg, nid, node_off, flags, flab, c + 4);
-    k_pointers<<<blocks(m), 256, 0, s>>>(m, min_size, nid, size, flab, c + 4, flags, ptr,
-                                         c + 1);
+    // distance back to the merge target -> ptr (flab doubles as its storage)
+    SSLIC_CUDA_CHECK(cudaMemsetAsync(flab, 0xff, (size_t)m * 4, s));
+    k_best_before<Off><<<blocks(n64), 256, 0, s>>>(cg, nid, node_off, flags, flab, cu + 0);
+    k_pointers<Off><<<blocks(m), 256, 0, s>>>(m, min_size, nid, size, flab, node_off, cu + 0,
+                                              flags, ptr, c + 1);
     SSLIC_CUDA_CHECK(cudaMemsetAsync(flab, 0, (size_t)m * 4, s));
     SSLIC_CUDA_CHECK(cudaGetLastError());
   }
@@ -606,23 +811,31 @@ uint32_t enforce_connectivity_device(const Geom& g, const uint32_t* labels_in,
   if (serial) {
     // exact sequential sweep on one device thread: the whole map (ids >= k)
     // or the pending cascade at the start of the raster
-    SSLIC_CUDA_CHECK(cudaMemcpyAsync(labels_out, labels_in, (size_t)n * 4,
-                                     cudaMemcpyDeviceToDevice, s));
-    Scratch mk_b(n, s);
+    if (full_serial && sizeof(Off) > 4)
+      throw Error(SSLIC_EINVAL,
+                  "enforce_connectivity: label ids >= k on >= 2^32 voxels (serial sweep) "
+                  "are not supported");
+    if (labels_out != labels_in)
+      SSLIC_CUDA_CHECK(cudaMemcpyAsync(labels_out, labels_in, (size_t)n64 * 4,
+                                       cudaMemcpyDeviceToDevice, s));
+    Scratch mk_b((size_t)n64, s);
     uint8_t* mk = mk_b.as<uint8_t>();
-    k_markers<<<blocks(n), 256, 0, s>>>(nid, flags, mk, n);
-    k_sweep_serial<<<1, 1, 0, s>>>(cg, labels_out, mk, idx, min_size, k,
-                                   full_serial ? 1 : 0, c + 5);
+    const Off qcap = (Off)std::min<int64_t>(n64, (int64_t)1 << 28);
+    Scratch q_b((size_t)qcap * sizeof(Off), s);
+    k_markers<Off><<<blocks(n64), 256, 0, s>>>(nid, flags, mk, n);
+    k_sweep_serial<Off><<<1, 1, 0, s>>>(cg, labels_out, mk, q_b.as<Off>(), qcap, min_size, k,
+                                        full_serial ? 1 : 0, cu + 1);
     SSLIC_CUDA_CHECK(cudaGetLastError());
-    uint32_t res[2];
-    SSLIC_CUDA_CHECK(cudaMemcpyAsync(res, c + 5, sizeof(res), cudaMemcpyDeviceToHost, s));
+    unsigned long long res[3];
+    SSLIC_CUDA_CHECK(cudaMemcpyAsync(res, cu + 1, sizeof(res), cudaMemcpyDeviceToHost, s));
     SSLIC_CUDA_CHECK(cudaStreamSynchronize(s));
-    next = res[1];
-    if (res[0] >= n) {
+    if (res[2]) throw Error(SSLIC_ENOMEM, "enforce_connectivity: serial fill exceeds its queue");
+    next = (uint32_t)res[1];
+    if (res[0] >= (unsigned long long)n64) {
       done = true;
     } else {
-      k_prefix_nodes<<<blocks(m), 256, 0, s>>>(m, node_off, nlab, labels_out, mk, k, fcomp,
-                                               flags, ptr, flab, factive, c + 3);
+      k_prefix_nodes<Off><<<blocks(m), 256, 0, s>>>(m, node_off, nlab, labels_out, mk, k, fcomp,
+                                                    flags, ptr, flab, factive, c + 3);
       SSLIC_CUDA_CHECK(cudaGetLastError());
       if (read_scalar(c + 3, s) != 0)
         throw Error(SSLIC_ELOGIC, "enforce_connectivity: inconsistent prefix state");
@@ -640,34 +853,53 @@ uint32_t enforce_connectivity_device(const Geom& g, const uint32_t* labels_in,
         SSLIC_CUDA_CHECK(cudaGetLastError());
         if (read_scalar(c + 2, s) == 0) break;
       }
-      k_edges<<<blocks(n), 256, 0, s>>>(cg, nid, flags, nlab, fcomp, factive, T, te, te_new,
-                                        absn);
+      k_edges<Off><<<blocks(n64), 256, 0, s>>>(cg, nid, flags, nlab, fcomp, factive, T, te,
+                                               te_new, absn);
       SSLIC_CUDA_CHECK(cudaMemsetAsync(c + 2, 0, sizeof(unsigned), s));
       k_swap_te<<<blocks(kk), 256, 0, s>>>(k, te, te_new, c + 2);
       k_swap_abs<<<blocks(m), 256, 0, s>>>(m, flags, absn, c + 2);
       SSLIC_CUDA_CHECK(cudaGetLastError());
       if (read_scalar(c + 2, s) == 0) break;
     }
-    // the last round left T consistent with the converged te / absorbed sets
-    k_events<<<blocks(m), 256, 0, s>>>(m, flags, nlab, fcomp, factive, te, idx);
-    SSLIC_CUDA_CHECK(
-        cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, idx, idx, (int64_t)m + 1, s));
-    k_final_labels<<<blocks(m), 256, 0, s>>>(m, flags, nlab, fcomp, factive, te, idx, next,
-                                             flab);
-    k_output<<<blocks(n), 256, 0, s>>>(nid, T, flab, labels_out, n);
+    // the last round left T consistent with the converged te / absorbed sets;
+    // the event flags and their ranks reuse the (now dead) size array
+    uint32_t* ev = size;  // m + 1 entries
+    k_events<<<blocks(m), 256, 0, s>>>(m, flags, nlab, fcomp, factive, te, ev);
+    {
+      size_t tb = 0;
+      cub::DeviceScan::ExclusiveSum(nullptr, tb, ev, ev, (int64_t)m + 1, s);
+      Scratch tmp(tb, s);
+      SSLIC_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, ev, ev, (int64_t)m + 1, s));
+    }
+    k_final_labels<<<blocks(m), 256, 0, s>>>(m, flags, nlab, fcomp, factive, te, ev, next, flab);
+    k_output<Off><<<blocks(n64), 256, 0, s>>>(nid, T, flab, labels_out, n);
     SSLIC_CUDA_CHECK(cudaGetLastError());
-    next += read_scalar(idx + m, s);
+    next += read_scalar(ev + m, s);
   }
   if (timing) {
     SSLIC_CUDA_CHECK(cudaStreamSynchronize(s));
     const auto t1 = std::chrono::steady_clock::now();
     std::fprintf(stderr,
-                 "[sslic] connectivity: %u voxels, %u components, %s, %d rounds, %d jump "
-                 "passes, %.2f ms\n",
-                 n, m, full_serial ? "serial (ids >= k)" : (serial ? "serial prefix" : "no prefix"),
+                 "[sslic] connectivity: %lld voxels, %u components, %d CCL slab(s), %s, %d "
+                 "rounds, %d jump passes, %.2f ms\n",
+                 (long long)n64, m, nslabs,
+                 full_serial ? "serial (ids >= k)" : (serial ? "serial prefix" : "no prefix"),
                  rounds, jumps, std::chrono::duration<double, std::milli>(t1 - t0).count());
   }
   return next;
+}
+
+}  // namespace
+
+uint32_t enforce_connectivity_device(const Geom& g, const uint32_t* labels_in,
+                                     const double* centers, uint32_t* labels_out,
+                                     cudaStream_t s) {
+  int64_t n = 1;
+  for (int a = 0; a < g.rank; ++a) n *= g.dims[a];
+  // (SSLIC_CC_FORCE64=1: the 64-bit offset path on a small volume, for tests)
+  if (n < ((int64_t)1 << 32) - 1 && std::getenv("SSLIC_CC_FORCE64") == nullptr)
+    return connectivity_impl<uint32_t>(g, labels_in, centers, labels_out, s);
+  return connectivity_impl<uint64_t>(g, labels_in, centers, labels_out, s);
 }
 
 }  // namespace sslic_b200

@@ -122,3 +122,73 @@ def test_rank4_map_is_face_connected_in_w(sslic, oracle_lib):
     lab = _random_field(rng, dims, k, 2)
     out = _check(sslic, oracle_lib, dims, lab, _random_centres(rng, dims, k, 1), 1, (2, 2, 2, 2))
     assert out.size == int(np.prod(dims))
+
+
+class _env:
+    """Temporarily set environment switches the C library reads per call."""
+
+    def __init__(self, **kv):
+        self.kv = kv
+
+    def __enter__(self):
+        import os
+        self.old = {k: os.environ.get(k) for k in self.kv}
+        os.environ.update({k: str(v) for k, v in self.kv.items()})
+
+    def __exit__(self, *a):
+        import os
+        for k, v in self.old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+def _stitch_cases():
+    out = []
+    for seed in range(12):
+        rng = np.random.default_rng(3000 + seed)
+        rank = 1 + seed % 4
+        ext = {1: (200, 3000), 2: (12, 80), 3: (6, 28), 4: (4, 10)}[rank]
+        dims = tuple(int(x) for x in rng.integers(ext[0], ext[1], rank))
+        grid = tuple(int(rng.integers(1, min(d, 6) + 1)) for d in dims)
+        k = int(rng.integers(2, 40))
+        out.append((seed, dims, grid, k, int(rng.integers(1, 4))))
+    return out
+
+
+@pytest.mark.parametrize("case", _stitch_cases(), ids=lambda c: f"seed{c[0]}-rank{len(c[1])}")
+def test_slab_stitched_ccl_equals_whole_volume(sslic, oracle_lib, case):
+    """The >= 2^32-voxel path labels components slab by slab and stitches them
+    across the slab faces (connectivity.cu). Forced onto small volumes with 2,
+    3 or more slabs (SSLIC_CC_SLAB_PLANES), with 32- and 64-bit offsets
+    (SSLIC_CC_FORCE64), the output equals the whole-volume result and the
+    oracle's raster sweep bit for bit."""
+    seed, dims, grid, k, blob = case
+    rng = np.random.default_rng(seed)
+    lab = _random_field(rng, dims, k, blob)
+    cen = _random_centres(rng, dims, k, 1)
+    whole = _check(sslic, oracle_lib, dims, lab, cen, 1, grid)
+    last = dims[-1]
+    for planes in sorted({1, 2, max(1, last // 3), max(1, last // 2)}):
+        for force64 in (False, True):
+            env = {"SSLIC_CC_SLAB_PLANES": planes}
+            if force64:
+                env["SSLIC_CC_FORCE64"] = 1
+            with _env(**env):
+                got = _check(sslic, oracle_lib, dims, lab, cen, 1, grid)
+            assert np.array_equal(got, whole), (planes, force64)
+
+
+def test_slab_stitched_noisy_volume(sslic, oracle_lib):
+    """A config-3-like noisy SLIC map (most voxels outside finalized
+    components) cut into 5 slabs, 64-bit offsets: equal to the oracle."""
+    rng = np.random.default_rng(77)
+    dims, grid = (96, 80, 72), (16, 16, 16)
+    data = _noisy_volume(rng, dims, 40)
+    p = sslic.SlicParams(grid=list(grid), weight_m=10.0, max_iterations=10,
+                         enforce_connectivity=False)
+    res = sslic.run_slic(sslic.NDImage(dims, 1, data), p)
+    cen = res.centers.data.reshape(-1, 4)
+    with _env(SSLIC_CC_SLAB_PLANES=15, SSLIC_CC_FORCE64=1):
+        _check(sslic, oracle_lib, dims, res.labels, cen, 1, grid)
