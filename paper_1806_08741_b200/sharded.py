@@ -78,29 +78,34 @@ class ShardedLoop:
             self.allreduce(self.engine.centers_tensor())
         self.engine.commit()
 
-    def gather_labels(self, all_gather: Callable, last: int, plane: int, align: int = 1):
-        """The full label map, assembled on every rank: each rank contributes
-        its slab (engine.labels_tensor(), padded to the largest slab so the
-        collective sees equal sizes) and the slabs are concatenated along the
-        last axis in rank order. `all_gather(list_out, tensor)` is
-        torch.distributed.all_gather."""
+    def gather_labels(self, gather: Callable, last: int, plane: int, align: int = 1,
+                      rank: int = 0, dst: int = 0):
+        """The full label map on rank `dst` only (None elsewhere): each rank
+        sends its slab (engine.labels_tensor(), padded to the largest slab so
+        the collective sees equal sizes) and `dst` concatenates them along the
+        last axis in rank order. `gather(tensor, parts_or_None, dst)` is
+        torch.distributed.gather(tensor, gather_list, dst)."""
         import torch
         slabs = all_slabs(last, self.world, align)
         mine = self.engine.labels_tensor()
         width = max(hi - lo for lo, hi in slabs) * plane
         buf = torch.zeros(width, dtype=mine.dtype, device=mine.device)
         buf[: mine.numel()] = mine
-        parts = [torch.empty_like(buf) for _ in range(self.world)]
-        all_gather(parts, buf)
+        parts = [torch.empty_like(buf) for _ in range(self.world)] if rank == dst else None
+        gather(buf, parts, dst)
+        if rank != dst:
+            return None
         return torch.cat([parts[r][: (hi - lo) * plane] for r, (lo, hi) in enumerate(slabs)])
 
-    def segment(self, all_gather: Callable, connectivity: Callable, last: int, plane: int,
-                align: int = 1):
-        """enforce_connectivity over the sharded result: its raster sweep is a
-        sequential recurrence over the whole map (connectivity.hpp:182-261),
-        so the slabs are gathered and every rank runs `connectivity(full)`
-        (the same deterministic result everywhere)."""
-        return connectivity(self.gather_labels(all_gather, last, plane, align))
+    def segment(self, gather: Callable, connectivity: Callable, last: int, plane: int,
+                align: int = 1, rank: int = 0, dst: int = 0):
+        """enforce_connectivity over the sharded result on rank `dst`: the
+        slabs are gathered there (one copy of the map, not one per rank) and
+        `connectivity(full)` runs once -- on a B200 the device pass handles
+        2^32+ voxels with its own slab stitching (connectivity.cu), so a
+        config-5 map fits one GPU. Other ranks return None."""
+        full = self.gather_labels(gather, last, plane, align, rank, dst)
+        return None if full is None else connectivity(full)
 
     def iterate(self):
         """One iteration: fused assign+accumulate on the slab, SUM of the
