@@ -403,6 +403,7 @@ FastParams Engine::fast_params() {
     P.abs_margin = abs_margin_ * P.key_scale2;
     P.region_cand = region_cand_;
     P.max_cand = max_cand_;
+    P.vmax = (float)vmax_;
     return P;
 }
 

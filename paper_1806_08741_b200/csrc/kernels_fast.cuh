@@ -72,6 +72,7 @@ struct FastParams {
   int aligned4;       // dims[0] % 4 == 0: 4-voxel runs are vector-aligned
   int max_cand;       // regions with more candidates take the exact crowded path
   int skip_full;      // k_assign_fast: full regions were done by k_assign_lean
+  float vmax;         // value range of the image (max |v|; dtype max for u8/u16)
 };
 
 // A region not clipped by the volume or the slab (k_assign_lean's domain).
