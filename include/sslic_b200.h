@@ -90,6 +90,16 @@ int sslic_segment(const sslic_image* img, const sslic_params* params, int device
                   uint32_t* labels_out, double* centers_out, double* residuals_out,
                   int* iterations_done, uint32_t* next_label_out);
 
+/* The tools/sslic.cpp pipeline (run_slic, enforce_connectivity when
+ * params->enforce_connectivity, write_labels; tools/sslic.cpp:104-109) plus,
+ * when contour_path is not NULL, write_volume(contour_path,
+ * mask_label_contour(img, labels)) in float32 (tools/sslic.cpp:121-125,
+ * io.hpp:362-392,432-454). The label count of the labels header and the
+ * contour bitmask come out of the final relabel pass on the device (no extra
+ * pass over the map). centers_out / residuals_out as sslic_run_slic. */
+int sslic_segment_write(const sslic_image* img, const sslic_params* params, int device,
+                        const char* labels_path, const char* contour_path, double* centers_out,
+                        double* residuals_out, int* iterations_done, uint32_t* next_label_out);
 /* init_centers (slic.hpp:206-230) [+ perturb_centers (236-267) when perturb].
  * centers_out: k*(c+rank) doubles (host). */
 int sslic_init_centers(const sslic_image* img, const sslic_params* params, int perturb,

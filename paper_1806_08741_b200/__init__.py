@@ -161,6 +161,8 @@ def lib():
         "sslic_run_slic_rank": (C.c_int, [ip, pp, C.c_int, C.c_int, vp, C.c_int, C.c_int64, u32p,
                                           f64p, f64p, C.POINTER(C.c_int)]),
         "sslic_device_count": (C.c_int, []),
+        "sslic_segment_write": (C.c_int, [ip, pp, C.c_int, C.c_char_p, C.c_char_p, f64p, f64p,
+                                          C.POINTER(C.c_int), u32p]),
         "sslic_nccl_unique_id": (C.c_int, [vp, C.c_int64]),
         "sslic_slab_bounds": (C.c_int, [C.c_int64, C.c_int, C.c_int, C.c_int64, i64p, i64p]),
         "sslic_engine_attach_nccl": (C.c_int, [vp, vp, C.c_int, C.c_int]),
@@ -447,6 +449,28 @@ def segment(img: NDImage, params: SlicParams, device: int = 0):
                            C.byref(nxt)))
     return (SlicResult(labels, ClusterTable(img.channels, img.rank, centers),
                        list(res[: done.value])), int(nxt.value))
+
+
+def segment_write(img: NDImage, params: SlicParams, labels_path: str,
+                  contour_path: Optional[str] = None, device: int = 0):
+    """tools/sslic.cpp's segment pipeline writing its files (sslic_segment_write):
+    run_slic, enforce_connectivity, write_labels(labels_path) and optionally
+    write_volume(contour_path, mask_label_contour(img, labels)) as float32; the
+    label count and the contour come out of the final device pass. Returns
+    (ClusterTable, residuals, next_label)."""
+    params.validate(img.dims)
+    k = cluster_count(img.dims, params.grid)
+    iters = params.iterations_for(img.rank)
+    centers = np.empty(k * (img.channels + img.rank))
+    res = np.empty(max(iters, 1))
+    done, nxt = C.c_int(0), C.c_uint32(0)
+    d, p = img._desc(), params._c()
+    _check(lib().sslic_segment_write(C.byref(d), C.byref(p), device, os.fsencode(labels_path),
+                                     os.fsencode(contour_path) if contour_path else None,
+                                     _p(centers, C.c_double), _p(res, C.c_double),
+                                     C.byref(done), C.byref(nxt)))
+    return (ClusterTable(img.channels, img.rank, centers), list(res[: done.value]),
+            int(nxt.value))
 
 
 def init_centers(img: NDImage, params: SlicParams, device: int = 0) -> ClusterTable:

@@ -780,6 +780,60 @@ int sslic_segment(const sslic_image* img, const sslic_params* params, int device
   });
 }
 
+int sslic_segment_write(const sslic_image* img, const sslic_params* params, int device,
+                        const char* labels_path, const char* contour_path, double* centers_out,
+                        double* residuals_out, int* iterations_done, uint32_t* next_label_out) {
+  return guarded([&] {
+    validate_image(img);
+    validate_params(params, img);
+    if (!labels_path) throw Error(SSLIC_EINVAL, "segment_write: null labels path");
+    Stream st(device);
+    PhaseTimer pt("segment_write");
+    auto dimg = upload_image(img, st);
+    const sslic_image v = device_view(img, dimg->p);
+    const int64_t last = img->dims[img->rank - 1];
+    Engine e(v, *params, device, 0, last, 0, last, st.s);
+    const int done = run_loop(e, params, st);
+    pt.mark(st, "upload + iterations");
+    const int64_t n = pixel_count(*img);
+    dimg.reset();
+    uint32_t* lab = e.label_words();
+    e.unpack_labels(lab);
+    // the final pass also yields the label count and the contour bitmask
+    const int64_t words = (n + 31) / 32;
+    DeviceBuf dmax(sizeof(unsigned), st.s), dbits(contour_path ? words * 4 : 4, st.s);
+    SSLIC_CUDA_CHECK(cudaMemsetAsync(dmax.p, 0, sizeof(unsigned), st.s));
+    if (contour_path) SSLIC_CUDA_CHECK(cudaMemsetAsync(dbits.p, 0, words * 4, st.s));
+    LabelOutputs outs;
+    outs.max_label = dmax.as<unsigned>();
+    outs.boundary = contour_path ? dbits.as<uint32_t>() : nullptr;
+    uint32_t next = (uint32_t)e.geom().k;
+    if (params->enforce_connectivity)
+      next = enforce_connectivity_device(e.geom(), lab, e.current_centers(), lab, st.s, outs);
+    else
+      label_outputs_device(e.geom(), lab, outs, st.s);
+    pt.mark(st, params->enforce_connectivity ? "connectivity (fused outputs)" : "outputs");
+    std::vector<uint32_t> host((size_t)n);
+    std::vector<uint32_t> bits(contour_path ? (size_t)words : 0);
+    unsigned mx = 0;
+    SSLIC_CUDA_CHECK(
+        cudaMemcpyAsync(host.data(), lab, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, st.s));
+    if (contour_path)
+      SSLIC_CUDA_CHECK(
+          cudaMemcpyAsync(bits.data(), dbits.p, words * 4, cudaMemcpyDeviceToHost, st.s));
+    SSLIC_CUDA_CHECK(cudaMemcpyAsync(&mx, dmax.p, sizeof mx, cudaMemcpyDeviceToHost, st.s));
+    e.copy_centers_to_host(centers_out);  // (synchronizes)
+    if (residuals_out) e.residuals_to_host(residuals_out, done);
+    pt.mark(st, "D2H");
+    write_labels_counted(labels_path, img->rank, img->dims, host.data(), (uint64_t)mx + 1);
+    if (contour_path) write_contour_f32(contour_path, img, bits.data());
+    pt.mark(st, "files");
+    if (iterations_done) *iterations_done = done;
+    if (next_label_out) *next_label_out = next;
+    return SSLIC_OK;
+  });
+}
+
 int sslic_init_centers(const sslic_image* img, const sslic_params* params, int perturb,
                        int device, double* centers_out) {
   return guarded([&] {

@@ -45,6 +45,11 @@ inline void slab_bounds(int64_t last, int world, int rank, int64_t align, int64_
   *hi = std::min(units * (rank + 1) / world * align, last);
 }
 
+// Output files of the fused final pass (io.cu).
+void write_labels_counted(const char* path, int rank, const int64_t* dims,
+                          const uint32_t* labels, uint64_t count);
+void write_contour_f32(const char* path, const sslic_image* img, const uint32_t* boundary);
+
 // NCCL plumbing (multi.cu): one communicator per engine/rank. The engine's
 // collective steps -- the value-range MAX before init, the SUM of the init
 // tables, the SUM of the int64 per-cluster partials every iteration -- run

@@ -575,6 +575,56 @@ __global__ void k_output(const uint32_t* nid, const uint32_t* T, const uint32_t*
   GRID_STRIDE(Off, i, n) out[i] = flab[T[nid[i]]];
 }
 
+// k_output fused with the output files' by-products: the max label and the
+// contour bitmask, from the neighbours' OUTPUT labels (flab[T[nid[q]]], so no
+// second pass over the written map is needed).
+template <class Off>
+__global__ void k_output_fused(CG<Off> g, const uint32_t* nid, const uint32_t* T,
+                               const uint32_t* flab, uint32_t* out, unsigned* max_label,
+                               uint32_t* boundary) {
+  uint32_t mx = 0;
+  GRID_STRIDE(Off, i, g.n) {
+    const uint32_t L = flab[T[nid[i]]];
+    out[i] = L;
+    mx = max(mx, L);
+    if (boundary) {
+      bool b = false;
+      for_neighbours(g, i, [&](Off q) { b |= flab[T[nid[q]]] != L; });
+      // lanes of this warp-iteration: consecutive i from a 32-aligned base
+      const uint64_t base = (uint64_t)i - (threadIdx.x & 31);
+      const uint64_t left = (uint64_t)g.n - base;
+      const unsigned act = left >= 32 ? 0xffffffffu : ((1u << left) - 1u);
+      const unsigned bits = __ballot_sync(act, b);
+      if ((threadIdx.x & 31) == 0 && bits) boundary[i / 32] = bits;  // i is 32-aligned here
+    }
+  }
+  mx = __reduce_max_sync(0xffffffffu, mx);  // every lane leaves the loop and gets here
+  if ((threadIdx.x & 31) == 0 && max_label) atomicMax(max_label, mx);
+}
+
+// the same by-products of a final label map
+template <class Off>
+__global__ void k_label_outputs(CG<Off> g, const uint32_t* labels, unsigned* max_label,
+                                uint32_t* boundary) {
+  uint32_t mx = 0;
+  GRID_STRIDE(Off, i, g.n) {
+    const uint32_t L = labels[i];
+    mx = max(mx, L);
+    if (boundary) {
+      bool b = false;
+      for_neighbours(g, i, [&](Off q) { b |= labels[q] != L; });
+      // lanes of this warp-iteration: consecutive i from a 32-aligned base
+      const uint64_t base = (uint64_t)i - (threadIdx.x & 31);
+      const uint64_t left = (uint64_t)g.n - base;
+      const unsigned act = left >= 32 ? 0xffffffffu : ((1u << left) - 1u);
+      const unsigned bits = __ballot_sync(act, b);
+      if ((threadIdx.x & 31) == 0 && bits) boundary[i / 32] = bits;
+    }
+  }
+  mx = __reduce_max_sync(0xffffffffu, mx);  // every lane leaves the loop and gets here
+  if ((threadIdx.x & 31) == 0 && max_label) atomicMax(max_label, mx);
+}
+
 // Stream-ordered device allocation owned for the scope of one call.
 struct Scratch {
   void* p = nullptr;
@@ -639,7 +689,7 @@ int64_t slab_planes(const Geom& g, int64_t plane, int64_t last) {
 
 template <class Off>
 uint32_t connectivity_impl(const Geom& g, const uint32_t* labels_in, const double* centers,
-                           uint32_t* labels_out, cudaStream_t s) {
+                           uint32_t* labels_out, cudaStream_t s, LabelOutputs outs) {
   int64_t n64 = 1;
   for (int a = 0; a < g.rank; ++a) n64 *= g.dims[a];
   const Off n = (Off)n64;
@@ -872,9 +922,17 @@ uint32_t connectivity_impl(const Geom& g, const uint32_t* labels_in, const doubl
       SSLIC_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, ev, ev, (int64_t)m + 1, s));
     }
     k_final_labels<<<blocks(m), 256, 0, s>>>(m, flags, nlab, fcomp, factive, te, ev, next, flab);
-    k_output<Off><<<blocks(n64), 256, 0, s>>>(nid, T, flab, labels_out, n);
+    if (outs.max_label || outs.boundary)
+      k_output_fused<Off><<<blocks(n64), 256, 0, s>>>(cg, nid, T, flab, labels_out,
+                                                      outs.max_label, outs.boundary);
+    else
+      k_output<Off><<<blocks(n64), 256, 0, s>>>(nid, T, flab, labels_out, n);
     SSLIC_CUDA_CHECK(cudaGetLastError());
     next += read_scalar(ev + m, s);
+  } else if (outs.max_label || outs.boundary) {  // the serial sweep wrote the map
+    k_label_outputs<Off><<<blocks(n64), 256, 0, s>>>(cg, labels_out, outs.max_label,
+                                                     outs.boundary);
+    SSLIC_CUDA_CHECK(cudaGetLastError());
   }
   if (timing) {
     SSLIC_CUDA_CHECK(cudaStreamSynchronize(s));
@@ -893,13 +951,27 @@ uint32_t connectivity_impl(const Geom& g, const uint32_t* labels_in, const doubl
 
 uint32_t enforce_connectivity_device(const Geom& g, const uint32_t* labels_in,
                                      const double* centers, uint32_t* labels_out,
-                                     cudaStream_t s) {
+                                     cudaStream_t s, LabelOutputs outs) {
   int64_t n = 1;
   for (int a = 0; a < g.rank; ++a) n *= g.dims[a];
   // (SSLIC_CC_FORCE64=1: the 64-bit offset path on a small volume, for tests)
   if (n < ((int64_t)1 << 32) - 1 && std::getenv("SSLIC_CC_FORCE64") == nullptr)
-    return connectivity_impl<uint32_t>(g, labels_in, centers, labels_out, s);
-  return connectivity_impl<uint64_t>(g, labels_in, centers, labels_out, s);
+    return connectivity_impl<uint32_t>(g, labels_in, centers, labels_out, s, outs);
+  return connectivity_impl<uint64_t>(g, labels_in, centers, labels_out, s, outs);
+}
+
+void label_outputs_device(const Geom& g, const uint32_t* labels, LabelOutputs outs,
+                          cudaStream_t s) {
+  int64_t n = 1;
+  for (int a = 0; a < g.rank; ++a) n *= g.dims[a];
+  const int64_t last = g.dims[g.rank - 1];
+  if (n < ((int64_t)1 << 32) - 1)
+    k_label_outputs<uint32_t><<<blocks(n), 256, 0, s>>>(make_cg<uint32_t>(g, 0, last), labels,
+                                                        outs.max_label, outs.boundary);
+  else
+    k_label_outputs<uint64_t><<<blocks(n), 256, 0, s>>>(make_cg<uint64_t>(g, 0, last), labels,
+                                                        outs.max_label, outs.boundary);
+  SSLIC_CUDA_CHECK(cudaGetLastError());
 }
 
 }  // namespace sslic_b200

@@ -194,6 +194,67 @@ std::string write_volume_files(const std::string& path, int rank, const int64_t*
 }
 
 }  // namespace
+
+// write_labels (io.hpp:396-412) with the label count already known (the
+// fused final pass computes the max on the device).
+void write_labels_counted(const char* path, int rank, const int64_t* dims,
+                          const uint32_t* labels, uint64_t count) {
+  int64_t n = 1;
+  for (int a = 0; a < rank; ++a) n *= dims[a];
+  write_volume_files(path, rank, dims, 1, "uint32", labels, (size_t)n * 4,
+                     "label count: " + std::to_string((unsigned long long)count));
+}
+
+// write_volume(path, mask_label_contour(img, labels)) (io.hpp:432-454,
+// 362-392; default type float32) from the image and the contour bitmask of
+// the fused final pass: streamed in chunks, boundary voxels zeroed in every
+// channel, other values converted as static_cast<float>(double(v)).
+void write_contour_f32(const char* path, const sslic_image* img, const uint32_t* boundary) {
+  int64_t n = 1;
+  for (int a = 0; a < img->rank; ++a) n *= img->dims[a];
+  const int ch = img->channels;
+  const size_t slash = std::string(path).find_last_of('/');
+  const std::string sp(path);
+  const std::string dir = slash == std::string::npos ? "" : sp.substr(0, slash + 1);
+  std::string stem = slash == std::string::npos ? sp : sp.substr(slash + 1);
+  const size_t dot = stem.find_last_of('.');
+  if (dot != std::string::npos && dot > 0) stem = stem.substr(0, dot);
+  const std::string data_file = stem + ".raw";
+  FILE* f = std::fopen((dir + data_file).c_str(), "wb");
+  if (!f) throw Error(SSLIC_EIO_WRITE, "cannot open " + dir + data_file + " for writing");
+  constexpr int64_t kChunk = (int64_t)1 << 22;
+  std::vector<float> buf((size_t)kChunk * ch);
+  bool ok = true;
+  for (int64_t v0 = 0; v0 < n && ok; v0 += kChunk) {
+    const int64_t v1 = std::min(n, v0 + kChunk);
+    for (int64_t v = v0; v < v1; ++v) {
+      const bool b = boundary[v >> 5] >> (v & 31) & 1u;
+      for (int c = 0; c < ch; ++c) {
+        const int64_t i = v * ch + c;
+        double x;
+        switch (img->dtype) {
+          case SSLIC_U8: x = static_cast<const uint8_t*>(img->data)[i]; break;
+          case SSLIC_U16: x = static_cast<const uint16_t*>(img->data)[i]; break;
+          case SSLIC_F32: x = static_cast<const float*>(img->data)[i]; break;
+          default: x = static_cast<const double*>(img->data)[i];
+        }
+        buf[(size_t)((v - v0) * ch + c)] = b ? 0.0f : static_cast<float>(x);
+      }
+    }
+    const size_t cnt = (size_t)((v1 - v0) * ch);
+    ok = std::fwrite(buf.data(), sizeof(float), cnt, f) == cnt;
+  }
+  ok = std::fclose(f) == 0 && ok;
+  if (!ok) throw Error(SSLIC_EIO_WRITE, "short write to " + dir + data_file);
+  std::ostringstream os;
+  os << "# sslic volume\n" << "dimension: " << img->rank << '\n' << "sizes:";
+  for (int a = 0; a < img->rank; ++a) os << ' ' << img->dims[a];
+  os << '\n' << "channels: " << ch << '\n' << "type: float32\n";
+  os << "endian: little\n" << "data file: " << data_file << '\n';
+  const std::string text = os.str();
+  write_bytes(path, text.data(), text.size());
+}
+
 }  // namespace sslic_b200
 
 using namespace sslic_b200;

@@ -301,3 +301,28 @@ def test_segment_matches_oracle_fuzz(sslic, oracle_lib, case):
     np.testing.assert_allclose(res.residuals, rs, rtol=RES_RTOL)
     cc = oracle_lib.enforce_connectivity(dims, lab, cen, ch, list(grid))
     assert np.array_equal(res.labels, cc), f"{int((res.labels != cc).sum())} labels differ"
+
+
+@pytest.mark.parametrize("conn", [True, False])
+def test_segment_write_files(sslic, oracle_lib, tmp_path, conn):
+    """sslic_segment_write: the labels file equals segment()'s map with the
+    reference's "label count" header comment (write_labels, io.hpp:396-412),
+    and the contour file equals write_volume(mask_label_contour(img, labels))
+    in float32 (io.hpp:432-454, 362-392) -- both from the fused final pass."""
+    s = sslic
+    rng = np.random.default_rng(909)
+    dims = (70, 52, 33)
+    data = rng.integers(0, 255, int(np.prod(dims)) * 3).astype(np.uint8)
+    img = s.NDImage(dims, 3, data)
+    p = s.SlicParams(grid=[8, 8, 8], weight_m=10.0, max_iterations=4, enforce_connectivity=conn)
+    ref, nxt = s.segment(img, p)
+    lp, cp = str(tmp_path / "labels.hdr"), str(tmp_path / "contour.hdr")
+    cen, res, nxt2 = s.segment_write(img, p, lp, cp)
+    assert nxt2 == nxt and cen == ref.centers and res == ref.residuals
+    lab, ldims = s.read_labels(lp)
+    assert tuple(ldims) == dims and np.array_equal(lab.reshape(-1), ref.labels)
+    head = open(lp).read()
+    assert f"label count: {int(ref.labels.max()) + 1}" in head
+    vol = s.read_volume(cp)
+    want = oracle_lib.mask_label_contour(dims, 3, data.astype(np.float64), ref.labels)
+    assert np.array_equal(np.asarray(vol.data, np.float32), want.astype(np.float32))
