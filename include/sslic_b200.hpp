@@ -154,9 +154,9 @@ inline SlicResult run_slic(const NDImage& img, const SlicParams& params, int wor
   return SlicResult{std::move(labels), std::move(table), std::move(residuals)};
 }
 
-/// enforce_connectivity (connectivity.hpp:265-273) on a B200.
-inline LabelMap enforce_connectivity(const LabelMap& labels, const ClusterTable& table,
-                                     const SlicParams& params, int device = 0) {
+/// enforce_connectivity on ONE given device.
+inline LabelMap enforce_connectivity_on_device(const LabelMap& labels, const ClusterTable& table,
+                                               const SlicParams& params, int device) {
   std::vector<int64_t> dims(labels.dims().begin(), labels.dims().end());
   std::vector<int64_t> grid(params.grid.begin(), params.grid.end());
   LabelMap out(labels.dims());
@@ -167,10 +167,21 @@ inline LabelMap enforce_connectivity(const LabelMap& labels, const ClusterTable&
   return out;
 }
 
-/// perturb_centers (slic.hpp:236-267) on a B200.
-inline ClusterTable perturb_centers(const NDImage& img, ClusterTable table, int device = 0) {
+/// enforce_connectivity (connectivity.hpp:265-273) on a B200, same signature:
+/// `workers` is accepted for parity (the device pass does the work; the
+/// result does not depend on it, as the reference's does not).
+inline LabelMap enforce_connectivity(const LabelMap& labels, const ClusterTable& table,
+                                     const SlicParams& params, int workers = 1) {
+  (void)workers;
+  return enforce_connectivity_on_device(labels, table, params, 0);
+}
+
+/// perturb_centers (slic.hpp:236-267) on a B200, same signature (`workers`
+/// accepted for parity; device 0 does the work).
+inline ClusterTable perturb_centers(const NDImage& img, ClusterTable table, int workers = 1) {
+  (void)workers;
   detail::NativeImage nimg = detail::narrow(img);
-  detail::check(sslic_perturb_centers(&nimg.desc, table.data().data(), table.count(), device));
+  detail::check(sslic_perturb_centers(&nimg.desc, table.data().data(), table.count(), 0));
   return table;
 }
 

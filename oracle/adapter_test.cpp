@@ -31,7 +31,7 @@ int main() {
     const sslic::SlicResult cpu = sslic::run_slic(img, params, 2);
     const sslic::SlicResult gpu = sslic::b200::run_slic(img, params, 2);  // namespace switch only
     const sslic::LabelMap cc_cpu = sslic::enforce_connectivity(cpu.labels, cpu.centers, params, 2);
-    const sslic::LabelMap cc_gpu = sslic::b200::enforce_connectivity(gpu.labels, gpu.centers, params);
+    const sslic::LabelMap cc_gpu = sslic::b200::enforce_connectivity(gpu.labels, gpu.centers, params, 2);
     const bool ok = cpu.labels == gpu.labels && cpu.centers == gpu.centers && cc_cpu == cc_gpu &&
                     cpu.residuals.size() == gpu.residuals.size();
     if (!ok) {
