@@ -446,6 +446,8 @@ def main():
         # max over ranks.
         host = torch.empty(img.numel(), dtype=tdt, pin_memory=True)
         host.copy_(img)
+        img_numel, img_esize = img.numel(), img.element_size()
+        del img  # the call uploads its own copy
         slab_vox_e = (slab[1] - slab[0]) * plane
         labels_h = torch.empty(slab_vox_e, dtype=torch.int32, pin_memory=True)
         eng.close()
@@ -470,7 +472,7 @@ def main():
             tdist.all_reduce(dt, op=tdist.ReduceOp.MAX)
         sec = float(dt.item())
         e2e = {"value": nvox * cfg_iters / sec, "unit": "voxel-iter/s",
-               "h2d_bytes_per_step": img.numel() * img.element_size(),
+               "h2d_bytes_per_step": img_numel * img_esize,
                "d2h_bytes_per_step": slab_vox_e * 4 + cen_e.data.nbytes,
                "call": "sslic_run_slic_rank per rank (pinned host planes; the NCCL "
                        "communicator, cached per unique id, was set up by the warm-up call)",
@@ -479,10 +481,12 @@ def main():
     if not args.no_e2e and not multi:
         host = torch.empty(img.numel(), dtype=tdt, pin_memory=True)
         host.copy_(img)
+        img_numel, img_esize = img.numel(), img.element_size()
         labels_h = torch.empty(nvox, dtype=torch.int32, pin_memory=True)
         eng.close()
-        del eng
+        del eng, img  # the call uploads its own copy
         torch.cuda.synchronize()
+        torch.cuda.empty_cache()
         import ctypes as C
         L = s.lib()
         desc = s._Image()
@@ -515,7 +519,7 @@ def main():
             per_call.append(time.perf_counter() - t0)
         sec = statistics.median(per_call)
         e2e = {"value": nvox * done.value / sec, "unit": "voxel-iter/s",
-               "h2d_bytes_per_step": img.numel() * img.element_size(),
+               "h2d_bytes_per_step": img_numel * img_esize,
                "d2h_bytes_per_step": nvox * 4 + cen.nbytes + res.nbytes,
                "call": "sslic_run_slic (host buffers, pinned)", "iterations": done.value,
                "seconds_per_call": sec, "timed_calls": reps, "warmup_calls": 1,

@@ -92,6 +92,8 @@ struct DeviceBuf {
 // Keep freed device memory in the stream-ordered pool across calls (the
 // default release threshold returns it to the driver at every sync, so each
 // whole-run call would re-map gigabytes).
+}  // namespace
+namespace sslic_b200 {
 void keep_pool_memory(int device) {
   static bool done[64] = {};
   if (device < 0 || device >= 64 || done[device]) return;
@@ -103,6 +105,8 @@ void keep_pool_memory(int device) {
   cudaGetLastError();
   done[device] = true;
 }
+}  // namespace sslic_b200
+namespace {
 
 struct Stream {
   cudaStream_t s = nullptr;
@@ -698,8 +702,13 @@ int sslic_run_slic(const sslic_image* img, const sslic_params* params, int devic
     Stream st(device);
     const int64_t n = pixel_count(*img);
     const int64_t last = img->dims[img->rank - 1];
+    // the overlapped download keeps a label snapshot on the device (4 B per
+    // voxel) next to the image and the label words: only when it fits
+    size_t free_b = 0, total_b = 0;
+    SSLIC_CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
+    const double need = (double)n * (4.0 + 4.0 + img->channels * (double)dtype_size(img->dtype));
     const bool overlapped = !params->has_residual_threshold && n >= ((int64_t)1 << 24) &&
-                            host_pinned_mapped(labels_out);
+                            host_pinned_mapped(labels_out) && need < 0.9 * (double)free_b;
     // pipelined upload (u8/u16 volumes: no image-wide pre-pass before init)
     const size_t img_bytes = (size_t)n * img->channels * dtype_size(img->dtype);
     std::unique_ptr<DeviceBuf> dimg;
@@ -728,9 +737,11 @@ int sslic_run_slic(const sslic_image* img, const sslic_params* params, int devic
     } else {
       done = run_loop(e, params, st);
       pt.mark(st, "iterations");
-      DeviceBuf lab(n * sizeof(uint32_t), st.s);
-      e.unpack_labels(lab.as<uint32_t>());
-      SSLIC_CUDA_CHECK(cudaMemcpyAsync(labels_out, lab.p, n * sizeof(uint32_t),
+      // the engine is done with its words and the image: unpack in place
+      dimg.reset();
+      uint32_t* lab = e.label_words();
+      e.unpack_labels(lab);
+      SSLIC_CUDA_CHECK(cudaMemcpyAsync(labels_out, lab, n * sizeof(uint32_t),
                                        cudaMemcpyDeviceToHost, st.s));
       st.sync();
       pt.mark(st, "labels D2H");

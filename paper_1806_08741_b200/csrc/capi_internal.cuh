@@ -45,6 +45,9 @@ inline void slab_bounds(int64_t last, int world, int rank, int64_t align, int64_
   *hi = std::min(units * (rank + 1) / world * align, last);
 }
 
+// Keep freed device memory in the stream-ordered pool across calls (capi.cu).
+void keep_pool_memory(int device);
+
 // Output files of the fused final pass (io.cu).
 void write_labels_counted(const char* path, int rank, const int64_t* dims,
                           const uint32_t* labels, uint64_t count);

@@ -233,13 +233,19 @@ __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fas
   const int64_t org[3] = {(int64_t)rxi * RX, (int64_t)ryi * RY,
                           RANK == 3 ? P.reg_z0 + (int64_t)rzi * RZ : 0};
   if (RANK == 3 && P.skip_full && region_full(P, org, RX, RY, RZ)) return;  // k_assign_lean's
+  // VAR & 2: this launch takes only FULL regions (compile-time shape): every
+  // box is whole, so the clipping below folds to constants
+  constexpr bool kFull = (VAR & 2) != 0 && RANK == 3 && RXc > 0;
+  if (kFull && !region_full(P, org, RX, RY, RZ)) return;
   const int64_t hi[3] = {min(org[0] + RX, g.dims[0]) - 1, min(org[1] + RY, g.dims[1]) - 1,
                          RANK == 3 ? min(org[2] + RZ, g.dims[2]) - 1 : 0};
   const int64_t zlo = RANK == 3 ? max(org[2], g.slab_begin) : 0;
   const int64_t zhi = RANK == 3 ? min(hi[2], g.slab_end - 1) : 0;
   // region-local inclusive bounds (32-bit)
-  const int ex = (int)(hi[0] - org[0]), ey = (int)(hi[1] - org[1]);
-  const int ez_lo = (int)(zlo - org[2]), ez_hi = (int)(zhi - org[2]);
+  const int ex = kFull ? RX - 1 : (int)(hi[0] - org[0]);
+  const int ey = kFull ? RY - 1 : (int)(hi[1] - org[1]);
+  const int ez_lo = kFull ? 0 : (int)(zlo - org[2]);
+  const int ez_hi = kFull ? RZ - 1 : (int)(zhi - org[2]);
 
   // ---- box geometry and the next-box prefetch ----
   const int nbx = (RX + Box::X - 1) / Box::X, nby = (RY + Box::Y - 1) / Box::Y;
@@ -316,12 +322,12 @@ __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fas
     q.by1 = min(q.by0 + Box::Y - 1, ey);
     q.bz0c = RANK == 3 ? max(q.bz0, ez_lo) : 0;
     q.bz1 = RANK == 3 ? min(q.bz0 + Box::Z - 1, ez_hi) : 0;
-    q.nonempty = q.bx0 <= q.bx1 && q.by0 <= q.by1 && q.bz0c <= q.bz1;
+    q.nonempty = kFull || (q.bx0 <= q.bx1 && q.by0 <= q.by1 && q.bz0c <= q.bz1);
     q.lx0 = q.bx0 + 4 * xq;
     q.ly = q.by0 + yq;
     q.lz = q.bz0 + zq;
-    const bool row_ok = q.ly <= q.by1 && (RANK == 2 || (q.lz >= q.bz0c && q.lz <= q.bz1));
-    q.vec = P.aligned4 && q.nonempty && row_ok && q.lx0 + 3 <= ex && q.lx0 + 3 < RX;
+    const bool row_ok = kFull || (q.ly <= q.by1 && (RANK == 2 || (q.lz >= q.bz0c && q.lz <= q.bz1)));
+    q.vec = kFull ? true : (P.aligned4 && q.nonempty && row_ok && q.lx0 + 3 <= ex && q.lx0 + 3 < RX);
     q.rel = q.bx0 + q.by0 * s1 + q.bz0 * s2 + lane_rel;
     return q;
   };
@@ -493,10 +499,10 @@ __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fas
       continue;
     }
     const int lx0 = cur.lx0, ly = cur.ly, lz = cur.lz;
-    const bool row_ok = ly <= by1 && (RANK == 2 || (lz >= bz0c && lz <= bz1));
+    const bool row_ok = kFull || (ly <= by1 && (RANK == 2 || (lz >= bz0c && lz <= bz1)));
     bool valid[4];
 #pragma unroll
-    for (int v = 0; v < 4; ++v) valid[v] = row_ok && lx0 + v <= ex && lx0 + v < RX;
+    for (int v = 0; v < 4; ++v) valid[v] = kFull || (row_ok && lx0 + v <= ex && lx0 + v < RX);
 
     // label words + pixels (prefetched, or direct loads for clipped boxes)
     const int64_t gx0 = org[0] + lx0, gy = org[1] + ly, gz = org[2] + lz;
@@ -1502,8 +1508,18 @@ void launch_fast_t(const FastParams& P, size_t smem, int64_t nblocks, cudaStream
       // measured: evaluations identical, +2.1 % without it). Pruning is
       // exact either way; this only picks the cheaper kernel.
       const double sp = P.g.m_sq * 3.0 * 4.0, cr = (double)P.vmax / 64.0;
-      if (sp < cr * cr && std::getenv("SSLIC_KEEP_SPATIAL_LB") == nullptr)
-        return launch_fast_shape<RANK, C, T, 32, 16, 16, 0, 1>(P, smem, nblocks, s);
+      const bool no_slb = sp < cr * cr && std::getenv("SSLIC_KEEP_SPATIAL_LB") == nullptr;
+      // full regions first (clipping folded away), then the clipped ones
+      if (P.aligned4 && std::getenv("SSLIC_NO_FULL") == nullptr) {
+        if (no_slb) launch_fast_shape<RANK, C, T, 32, 16, 16, 0, 3>(P, smem, nblocks, s);
+        else launch_fast_shape<RANK, C, T, 32, 16, 16, 0, 2>(P, smem, nblocks, s);
+        if (all_regions_full(P)) return;
+        FastParams Q = P;
+        Q.skip_full = 1;
+        if (no_slb) return launch_fast_shape<RANK, C, T, 32, 16, 16, 0, 1>(Q, smem, nblocks, s);
+        return launch_fast_shape<RANK, C, T, 32, 16, 16>(Q, smem, nblocks, s);
+      }
+      if (no_slb) return launch_fast_shape<RANK, C, T, 32, 16, 16, 0, 1>(P, smem, nblocks, s);
       return launch_fast_shape<RANK, C, T, 32, 16, 16>(P, smem, nblocks, s);
     }
   }

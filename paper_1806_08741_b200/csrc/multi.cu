@@ -147,6 +147,7 @@ struct RankStream {
   cudaStream_t s = nullptr;
   explicit RankStream(int device) {
     SSLIC_CUDA_CHECK(cudaSetDevice(device));
+    keep_pool_memory(device);  // whole-run calls must not re-map gigabytes each time
     SSLIC_CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
   }
   ~RankStream() {
