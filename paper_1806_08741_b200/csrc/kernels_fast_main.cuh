@@ -1524,8 +1524,16 @@ void launch_fast_t(const FastParams& P, size_t smem, int64_t nblocks, cudaStream
     }
   }
   if constexpr (RANK == 3 && C == 4 && sizeof(T) == 4) {
-    if (R[0] == 16 && R[1] == 16 && R[2] == 8)
-      return launch_fast_shape<RANK, C, T, 16, 16, 8>(P, smem, nblocks, s);  // config 4
+    if (R[0] == 16 && R[1] == 16 && R[2] == 8) {  // config 4
+      if (P.aligned4 && std::getenv("SSLIC_NO_FULL") == nullptr) {
+        launch_fast_shape<RANK, C, T, 16, 16, 8, 0, 2>(P, smem, nblocks, s);
+        if (all_regions_full(P)) return;
+        FastParams Q = P;
+        Q.skip_full = 1;
+        return launch_fast_shape<RANK, C, T, 16, 16, 8>(Q, smem, nblocks, s);
+      }
+      return launch_fast_shape<RANK, C, T, 16, 16, 8>(P, smem, nblocks, s);
+    }
   }
   if constexpr (RANK == 3 && C == 3 && sizeof(T) == 1) {
     if (R[0] == 32 && R[1] == 32 && R[2] == 32) {  // config 5

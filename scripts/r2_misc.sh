@@ -1,5 +1,4 @@
 cd $GRAFT_REPO_ROOT
 T=${1:-misc}
-bash scripts/ab.sh ${T}_full "X=0" "SSLIC_NO_FULL=1" > gpurun_out/${T}_ab_full.txt 2>&1
-timeout 900 python bench.py --nccl --steps 10 --warmup 3 --no-cpu > gpurun_out/${T}_bench_c3_nccl.log 2>&1
-timeout 1200 python bench.py --config 5 --steps 5 --warmup 3 --no-e2e > gpurun_out/${T}_bench_c5.log 2>&1
+bash scripts/ab.sh ${T}_c4full "X=0" "SSLIC_NO_FULL=1" --config 4 > gpurun_out/${T}_ab_c4full.txt 2>&1
+timeout 1200 python -m pytest tests/test_gpu_fast.py tests/test_gpu_fullsize.py -q -x > gpurun_out/${T}_pytest.log 2>&1; echo "exit $?" >> gpurun_out/${T}_pytest.log

@@ -100,7 +100,8 @@ def test_engine_labels_tensor_and_gather_single_rank(sslic):
     for _ in range(iters):
         loop.iterate()
     plane = int(np.prod(dims[:-1]))
-    gather = lambda out, t: out[0].copy_(t)  # world size 1
+    def gather(t, parts, dst):  # torch.distributed.gather at world size 1
+        parts[0].copy_(t)
     full = loop.gather_labels(gather, dims[-1], plane).cpu().numpy().view(np.uint32)
     ref = torch.empty(int(np.prod(dims)), dtype=torch.int32, device="cuda")
     eng.labels_to(ref.data_ptr())
