@@ -28,6 +28,8 @@
 // candidate, and flushed with one global atomic per (cluster, component).
 #pragma once
 
+#include <cuda.h>  // CUtensorMap (TMA descriptors; built on the host, kernels_fast_main.cuh)
+
 #include "common.cuh"
 #include "kernels_exact.cuh"
 
@@ -73,6 +75,10 @@ struct FastParams {
   int max_cand;       // regions with more candidates take the exact crowded path
   int skip_full;      // k_assign_fast: full regions were done by k_assign_lean
   float vmax;         // value range of the image (max |v|; dtype max for u8/u16)
+  // TMA descriptors of the label words (dims0 x dims1 x slab planes, u32) and
+  // the image (dims0*C x dims1 x data planes) for 8x4x4 box loads
+  alignas(64) CUtensorMap tmap_words;
+  alignas(64) CUtensorMap tmap_img;
 };
 
 // A region not clipped by the volume or the slab (k_assign_lean's domain).
@@ -100,6 +106,7 @@ struct BoxShape<3> {
 };
 
 struct alignas(16) FastSmem {
+  unsigned long long tma_bar[kFastThreads / 32][2];  // per warp, per box buffer (TMA loads)
   int n_cand;
   int id[kFastMaxCand];
   short anc[kFastMaxCand][3];  // region-local anchors

@@ -3,6 +3,8 @@
 // DESIGN.md "K2").
 #pragma once
 
+#include <cudaTypedefs.h>
+
 #include <atomic>
 #include <cstdlib>
 #include <type_traits>
@@ -36,6 +38,40 @@ __device__ __forceinline__ void cp_async_wait_all() {
 }
 __device__ __forceinline__ void cp_async_wait_group1() {
   asm volatile("cp.async.wait_group 1;" ::: "memory");
+}
+
+// ---- TMA (cp.async.bulk.tensor) box loads with an mbarrier per buffer ----
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z,
+                                            unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
 }
 
 // sum over the warp of a pair of signed 16-bit quantities packed in 32 bits
@@ -331,9 +367,44 @@ __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fas
     q.rel = q.bx0 + q.by0 * s1 + q.bz0 * s2 + lane_rel;
     return q;
   };
+  // VAR & 16 (full regions, 3-D): the warp's next box arrives by TMA, two
+  // 3-D tensor-tile loads (label words 8x4x4 u32, pixels 8C x 4 x 4) issued by
+  // one lane into a per-warp double buffer, completion on an mbarrier per
+  // buffer; the lanes then read their 4-voxel runs from the tiles.
+  constexpr bool kTma = (VAR & 16) != 0 && kFull;
+  constexpr int kTileW = Box::X * Box::Y * Box::Z * 4;                    // bytes of words
+  constexpr int kTileP = Box::X * Box::Y * Box::Z * C * (int)sizeof(T);  // bytes of pixels
+  constexpr int kTileBuf = ((kTileW + kTileP) + 127) & ~127;
+  unsigned char* const tile_base = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(pf_words) + 127) & ~(uintptr_t)127);
+  unsigned char* const my_tiles = tile_base + (size_t)warp * 2 * kTileBuf;
+  unsigned tma_phase = 0;  // bit b: parity of buffer b's next completion
+  if constexpr (kTma) {
+    if (lane == 0) {
+      mbar_init(&sm.tma_bar[warp][0], 1);
+      mbar_init(&sm.tma_bar[warp][1], 1);
+      fence_proxy_async();
+    }
+    __syncwarp();
+  }
   // (the geometry is recomputed rather than carried: nothing extra stays live)
   auto prefetch = [&](int bn, int buf) {
     if (bn >= nbox) return;
+    if constexpr (kTma) {
+      __syncwarp();  // every lane has read this buffer's previous tiles
+      if (lane == 0) {
+        const int bx = bn % nbx, t = bn / nbx, by = t % nby, bz = t / nby;
+        const int gx = (int)org[0] + bx * Box::X, gy = (int)org[1] + by * Box::Y;
+        const int gz = (int)(org[2] + bz * Box::Z);
+        unsigned char* dst = my_tiles + buf * kTileBuf;
+        fence_proxy_async();
+        mbar_expect_tx(&sm.tma_bar[warp][buf], kTileW + kTileP);
+        tma_load_3d(dst, &P.tmap_words, gx, gy, (int)(gz - g.slab_begin), &sm.tma_bar[warp][buf]);
+        tma_load_3d(dst + kTileW, &P.tmap_img, gx * C, gy, (int)(gz - g.data_begin),
+                    &sm.tma_bar[warp][buf]);
+      }
+      return;
+    }
     const BoxG q = box_geom(bn);
     if (!q.vec) return;
     cp_async16(my_pfw + buf * 32, lab_r + q.rel);
@@ -519,7 +590,18 @@ __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fas
     uint32_t word[4];
     float p[4][C];
     const T* px = img_r + rel * C;
-    if (vec) {
+    if constexpr (kTma) {
+      mbar_wait(&sm.tma_bar[warp][buf], (tma_phase >> buf) & 1u);
+      tma_phase ^= 1u << buf;
+    }
+    const int toff = (zq * Box::Y + yq) * Box::X + 4 * xq;  // lane's run in the 8x4x4 tiles
+    if (kTma) {
+      const uint4 q = *reinterpret_cast<const uint4*>(my_tiles + buf * kTileBuf + 4 * toff);
+      word[0] = q.x;
+      word[1] = q.y;
+      word[2] = q.z;
+      word[3] = q.w;
+    } else if (vec) {
       const uint4 q = my_pfw[buf * 32];
       word[0] = q.x;
       word[1] = q.y;
@@ -529,7 +611,15 @@ __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fas
 #pragma unroll
       for (int v = 0; v < 4; ++v) word[v] = valid[v] ? lab_r[rel + v] : kUndefined;
     }
-    if constexpr (kPW > 0) {
+    if constexpr (kTma) {
+      const T* tp = reinterpret_cast<const T*>(my_tiles + buf * kTileBuf + kTileW) + toff * C;
+      T vals[4 * C];
+      memcpy(vals, tp, sizeof(vals));
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+#pragma unroll
+        for (int c = 0; c < C; ++c) p[v][c] = (float)vals[v * C + c];
+    } else if constexpr (kPW > 0) {
       if (vec) {
         uint32_t w[kPW];
 #pragma unroll
@@ -1423,6 +1513,7 @@ inline size_t fast_smem_bytes(const Geom& g, const int* R, int cap = kFastMaxCan
   const int wsize = g.dtype == SSLIC_F64 ? 4 : dtype_size(g.dtype);  // working pixel size
   b += (size_t)warps * 2 * 32 * 4 * pf_pix_words(g.channels, wsize);
   b += (size_t)warps * fast_queue_cap(g.channels) * sizeof(uint2);
+  b += 128;  // 128-byte alignment of the TMA box tiles (they reuse the prefetch area)
   return b;
 }
 
@@ -1477,6 +1568,57 @@ inline bool launch_lean(const FastParams& P, int64_t nblocks, cudaStream_t s) {
   return false;
 }
 
+// TMA descriptors for the full-region box loads (k_assign_fast VAR & 16):
+// label words of the slab (u32) and the image's data planes (channels
+// interleaved along x), 8x4x4-voxel boxes. false when TMA is unavailable.
+inline bool make_box_tmaps(FastParams& P) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    cudaDriverEntryPointQueryResult q{};
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    cudaGetLastError();
+  }
+  if (!encode) return false;
+  const Geom& g = P.g;
+  if (g.rank != 3) return false;
+  const int esz = dtype_size(g.dtype);
+  CUtensorMapDataType dt;
+  switch (g.dtype) {
+    case SSLIC_U8: dt = CU_TENSOR_MAP_DATA_TYPE_UINT8; break;
+    case SSLIC_U16: dt = CU_TENSOR_MAP_DATA_TYPE_UINT16; break;
+    case SSLIC_F32: dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT32; break;
+    default: return false;
+  }
+  const cuuint32_t box_w[3] = {(cuuint32_t)BoxShape<3>::X, (cuuint32_t)BoxShape<3>::Y,
+                               (cuuint32_t)BoxShape<3>::Z};
+  const cuuint32_t box_i[3] = {(cuuint32_t)(BoxShape<3>::X * g.channels),
+                               (cuuint32_t)BoxShape<3>::Y, (cuuint32_t)BoxShape<3>::Z};
+  const cuuint32_t one[3] = {1, 1, 1};
+  const cuuint64_t dw[3] = {(cuuint64_t)g.dims[0], (cuuint64_t)g.dims[1],
+                            (cuuint64_t)(g.slab_end - g.slab_begin)};
+  const cuuint64_t sw[2] = {(cuuint64_t)g.dims[0] * 4, (cuuint64_t)(g.dims[0] * g.dims[1]) * 4};
+  const cuuint64_t di[3] = {(cuuint64_t)(g.dims[0] * g.channels), (cuuint64_t)g.dims[1],
+                            (cuuint64_t)(g.data_end - g.data_begin)};
+  const cuuint64_t si[2] = {(cuuint64_t)(g.dims[0] * g.channels * esz),
+                            (cuuint64_t)(g.dims[0] * g.dims[1] * g.channels * esz)};
+  if (box_i[0] * esz % 16 != 0 || sw[0] % 16 || si[0] % 16) return false;
+  if (encode(&P.tmap_words, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, P.labels, dw, sw, box_w, one,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  if (encode(&P.tmap_img, dt, 3, const_cast<void*>(P.img), di, si, box_i, one,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  return true;
+}
+
 inline bool all_regions_full(const FastParams& P) {
   const Geom& g = P.g;
   if (g.dims[0] % P.R[0] || g.dims[1] % P.R[1]) return false;
@@ -1519,7 +1661,13 @@ void launch_fast_t(const FastParams& P, size_t smem, int64_t nblocks, cudaStream
       const bool no_slb = sp < cr * cr && std::getenv("SSLIC_KEEP_SPATIAL_LB") == nullptr;
       // full regions first (clipping folded away), then the clipped ones
       if (P.aligned4 && std::getenv("SSLIC_NO_FULL") == nullptr) {
-        if (no_slb) launch_fast_shape<RANK, C, T, 32, 16, 16, 0, 3>(P, smem, nblocks, s);
+        FastParams T2 = P;
+        // TMA box tiles: correct, but 7.8 % slower than the per-lane cp.async
+        // staging for 8x4x4 boxes (profiles/r2/kernel_ab.txt): opt-in
+        const bool tma = std::getenv("SSLIC_TMA") != nullptr && make_box_tmaps(T2);
+        if (no_slb && tma) launch_fast_shape<RANK, C, T, 32, 16, 16, 0, 19>(T2, smem, nblocks, s);
+        else if (no_slb) launch_fast_shape<RANK, C, T, 32, 16, 16, 0, 3>(P, smem, nblocks, s);
+        else if (tma) launch_fast_shape<RANK, C, T, 32, 16, 16, 0, 18>(T2, smem, nblocks, s);
         else launch_fast_shape<RANK, C, T, 32, 16, 16, 0, 2>(P, smem, nblocks, s);
         if (all_regions_full(P)) return;
         FastParams Q = P;
