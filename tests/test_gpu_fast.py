@@ -543,3 +543,33 @@ def test_engine_reset_reruns_identically(sslic, exact):
     e.reset()
     l2, c2, r2 = run(iters)
     assert np.array_equal(l1, l2) and np.array_equal(c1, c2) and np.array_equal(r1, r2)
+
+
+@pytest.mark.parametrize("env", ["SSLIC_TMA", "SSLIC_NO_FULL", "SSLIC_KEEP_SPATIAL_LB"])
+def test_fast_variants_equal_exact(sslic, env, monkeypatch):
+    """The kernel variants behind launch-time switches -- TMA box tiles
+    (cp.async.bulk.tensor + mbarrier), the clipped-region kernel on full
+    regions, the spatial lower bound kept -- equal the exact kernel bit for
+    bit at every iteration (config-3 shape: 32x16x16 regions, full and
+    clipped)."""
+    import torch
+    monkeypatch.setenv(env, "1")
+    cfg, dims, ch, dtype, grid, m, iters = (3, (160, 144, 128), 1, np.uint16, (16, 16, 16), 10.0,
+                                            5)
+    img, fast, exact = _engines(sslic, cfg, dims, ch, dtype, grid, m, iters, torch)
+    n = int(np.prod(dims))
+    la = torch.empty(n, dtype=torch.int32, device="cuda")
+    lb = torch.empty(n, dtype=torch.int32, device="cuda")
+    for e in (fast, exact):
+        e.init()
+        e.commit()
+    for it in range(iters):
+        fast.assign()
+        exact.assign()
+        fast.update()
+        exact.update()
+        fast.labels_to(la.data_ptr())
+        exact.labels_to(lb.data_ptr())
+        torch.cuda.synchronize()
+        assert int((la != lb).sum().item()) == 0, f"{env}: iteration {it}"
+        assert np.array_equal(fast.centers(), exact.centers()), f"{env}: iteration {it}"
