@@ -554,7 +554,7 @@ def test_fast_variants_equal_exact(sslic, env, monkeypatch):
     clipped)."""
     import torch
     monkeypatch.setenv(env, "1")
-    cfg, dims, ch, dtype, grid, m, iters = (3, (160, 144, 128), 1, np.uint16, (16, 16, 16), 10.0,
+    cfg, dims, ch, dtype, grid, m, iters = (3, (168, 144, 120), 1, np.uint16, (16, 16, 16), 10.0,
                                             5)
     img, fast, exact = _engines(sslic, cfg, dims, ch, dtype, grid, m, iters, torch)
     n = int(np.prod(dims))
