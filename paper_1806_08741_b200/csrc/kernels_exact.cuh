@@ -235,6 +235,44 @@ static __global__ void k_bin_fill(int64_t k, const int* cell_of, const int* cell
   items[cell_start[c] + pos] = (int)id;
 }
 
+// Ascending cluster ids in items[b, e): insertion sort for the usual one or
+// two clusters per cell, heapsort (O(n log n)) for crowded cells.
+__device__ __forceinline__ void sort_cell(int* items, int b, int e) {
+  if (e - b > 32) {
+    int* a = items + b;
+    const int n = e - b;
+    auto sift = [&](int root, int end) {
+      for (;;) {
+        int child = 2 * root + 1;
+        if (child >= end) return;
+        if (child + 1 < end && a[child + 1] > a[child]) ++child;
+        if (a[root] >= a[child]) return;
+        const int t = a[root];
+        a[root] = a[child];
+        a[child] = t;
+        root = child;
+      }
+    };
+    for (int i = n / 2 - 1; i >= 0; --i) sift(i, n);
+    for (int end = n - 1; end > 0; --end) {
+      const int t = a[0];
+      a[0] = a[end];
+      a[end] = t;
+      sift(0, end);
+    }
+    return;
+  }
+  for (int i = b + 1; i < e; ++i) {
+    const int v = items[i];
+    int j = i - 1;
+    while (j >= b && items[j] > v) {
+      items[j + 1] = items[j];
+      --j;
+    }
+    items[j + 1] = v;
+  }
+}
+
 // Deterministic order inside each cell (ascending cluster id).
 static __global__ void k_bin_sort(int64_t ncells, const int* cell_start, int* items) {
   const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -536,6 +574,52 @@ static __global__ void k_update(Geom g, int shift, const unsigned long long* del
   if (threadIdx.x == 0) block_partials[blockIdx.x] = red[0];
 }
 
+// One cluster of the fused update (k_update_fused, k_update_bins_small):
+// sums += deltas (deltas re-zeroed), the new centre (count > 0) or the old
+// one, chg, the hi/lo fp32 split row, the anchors; adds (new-old)^2 to *part
+// and returns the anchor cell.
+__device__ __forceinline__ int update_cluster(const Geom& g, int shift, unsigned long long* delta,
+                                              unsigned long long* sums, const double* old_c,
+                                              double* new_c, int* chg, int next_table,
+                                              float2* split_out, int split_stride, int* anchors,
+                                              int64_t id, double* part) {
+  long long* a = reinterpret_cast<long long*>(sums) + id * (g.stride + 1);
+  long long* dl = reinterpret_cast<long long*>(delta) + id * (g.stride + 1);
+  for (int i = 0; i <= g.stride; ++i) {
+    a[i] += dl[i];
+    dl[i] = 0;
+  }
+  const long long cnt = a[g.stride];
+  const double* o = old_c + id * g.stride;
+  double* n = new_c + id * g.stride;
+  bool changed = false;
+  float2* sp = split_out + id * split_stride;
+  for (int i = 0; i < g.stride; ++i) {
+    double v = o[i];
+    if (cnt != 0) {
+      const double s = i < g.channels ? ldexp((double)a[i], -shift) : (double)a[i];
+      v = __ddiv_rn(s, (double)cnt);
+      const double d = __dsub_rn(v, o[i]);
+      *part = __dadd_rn(*part, __dmul_rn(d, d));
+      changed |= __double_as_longlong(v) != __double_as_longlong(o[i]);
+    }
+    n[i] = v;
+    const float h = __double2float_rn(v);
+    sp[i] = make_float2(h, __double2float_rn(v - (double)h));
+  }
+  for (int i = g.stride; i < split_stride; ++i) sp[i] = make_float2(0.f, 0.f);
+  if (changed) chg[id] = next_table;
+  int64_t cell = 0, mul = 1;
+  for (int ax = 0; ax < g.rank; ++ax) {
+    const int64_t an = anchor_of(n[g.channels + ax]);
+    anchors[id * kMaxRank + ax] = (int)an;
+    cell += clamp_cell(an, g.grid[ax], g.cells[ax]) * mul;
+    mul *= g.cells[ax];
+  }
+  for (int ax = g.rank; ax < kMaxRank; ++ax) anchors[id * kMaxRank + ax] = 0;
+  return (int)cell;
+}
+
 // Fused update for the tag-mode loop (one launch instead of update +
 // residual + anchors + hi/lo split): sums += deltas and the deltas are
 // zeroed for the next iteration; new centre (count > 0) or unchanged; chg;
@@ -554,41 +638,9 @@ static __global__ void k_update_fused(Geom g, int shift, unsigned long long* del
   if (id == 0 && *undefined_count) *undefined_seen = 1u;  // latched for run_slic
   double part = 0.0;
   if (id < g.k) {
-    long long* a = reinterpret_cast<long long*>(sums) + id * (g.stride + 1);
-    long long* dl = reinterpret_cast<long long*>(delta) + id * (g.stride + 1);
-    for (int i = 0; i <= g.stride; ++i) {
-      a[i] += dl[i];
-      dl[i] = 0;
-    }
-    const long long cnt = a[g.stride];
-    const double* o = old_c + id * g.stride;
-    double* n = new_c + id * g.stride;
-    bool changed = false;
-    float2* sp = split_out + id * split_stride;
-    for (int i = 0; i < g.stride; ++i) {
-      double v = o[i];
-      if (cnt != 0) {
-        const double s = i < g.channels ? ldexp((double)a[i], -shift) : (double)a[i];
-        v = __ddiv_rn(s, (double)cnt);
-        const double d = __dsub_rn(v, o[i]);
-        part = __dadd_rn(part, __dmul_rn(d, d));
-        changed |= __double_as_longlong(v) != __double_as_longlong(o[i]);
-      }
-      n[i] = v;
-      const float h = __double2float_rn(v);
-      sp[i] = make_float2(h, __double2float_rn(v - (double)h));
-    }
-    for (int i = g.stride; i < split_stride; ++i) sp[i] = make_float2(0.f, 0.f);
-    if (changed) chg[id] = next_table;
-    int64_t cell = 0, mul = 1;
-    for (int ax = 0; ax < g.rank; ++ax) {
-      const int64_t an = anchor_of(n[g.channels + ax]);
-      anchors[id * kMaxRank + ax] = (int)an;
-      cell += clamp_cell(an, g.grid[ax], g.cells[ax]) * mul;
-      mul *= g.cells[ax];
-    }
-    for (int ax = g.rank; ax < kMaxRank; ++ax) anchors[id * kMaxRank + ax] = 0;
-    cell_of[id] = (int)cell;
+    const int cell = update_cluster(g, shift, delta, sums, old_c, new_c, chg, next_table,
+                                    split_out, split_stride, anchors, id, &part);
+    cell_of[id] = cell;
     atomicAdd(cell_count + cell, 1);
   }
   __shared__ double red[256];
