@@ -71,6 +71,8 @@ Engine::Engine(const sslic_image& img, const sslic_params& p, int device, int64_
   const int64_t nv = slab_voxels();
   labels_ = dalloc<uint32_t>(nv, s);
   SSLIC_CUDA_CHECK(cudaMemsetAsync(labels_, 0xff, nv * sizeof(uint32_t), s));
+  words_fresh_ = true;
+  rows_assigned_ = false;
   if (dist_mode_) {
     dists_ = dalloc<double>(nv, s);  // filled with +inf below (DistanceMap, image.hpp:323)
   } else {
@@ -234,6 +236,8 @@ void Engine::reset() {
   const int64_t nv = slab_voxels();
   iter_ = 0;
   SSLIC_CUDA_CHECK(cudaMemsetAsync(labels_, 0xff, nv * sizeof(uint32_t), s));
+  words_fresh_ = true;
+  rows_assigned_ = false;
   SSLIC_CUDA_CHECK(cudaMemsetAsync(sums_, 0, partials_count() * sizeof(unsigned long long), s));
   SSLIC_CUDA_CHECK(cudaMemsetAsync(acc_, 0, partials_count() * sizeof(unsigned long long), s));
   acc_zero_ = true;
@@ -324,7 +328,10 @@ void Engine::init_range(int64_t z0, int64_t z1) {
 
 void Engine::assign_rows(int64_t r0, int64_t r1) {
   if (r1 <= r0) return;
+  // (each region row is assigned once per iteration, so the rows of
+  // iteration 0 still hold undefined words: the first-iteration kernel applies)
   launch_fast_assign(fast_params(), stream_, r0, r1);
+  rows_assigned_ = true;
   ++launches_;
   launch_check("assign_fast(rows)");
 }
@@ -367,11 +374,15 @@ void Engine::launch_assign_kernel(bool accumulate) {
   const int64_t nv = slab_voxels();
   const double* hist = dist_mode_ ? nullptr : centers_;
   if (path_ == AssignPath::kFast && accumulate && !dist_mode_) {
-    launch_fast_assign(fast_params(), s);
+    FastParams P = fast_params();
+    if (rows_assigned_) P.first = 0;  // some rows may already hold labels
+    launch_fast_assign(P, s);
+    words_fresh_ = false;
     ++launches_;  // k_region_cand + k_assign_fast
     launch_check("assign_fast");
     return;
   }
+  words_fresh_ = false;
   launch_exact_kernel(accumulate, nv, hist);
 }
 
@@ -404,6 +415,7 @@ FastParams Engine::fast_params() {
     P.region_cand = region_cand_;
     P.max_cand = max_cand_;
     P.vmax = (float)vmax_;
+    P.first = words_fresh_ && iter_ == 0 ? 1 : 0;
     return P;
 }
 

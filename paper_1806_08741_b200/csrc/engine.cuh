@@ -143,6 +143,8 @@ class Engine {
   float* img32_ = nullptr;            // fast path over an fp64 image: f32 working copy
   double pix_err_ = 0.0;              // bound of its rounding (|v| 2^-24)
   bool acc_zero_ = false;            // deltas already zero (fused update)
+  bool words_fresh_ = false;         // every label word is undefined (constructor / reset)
+  bool rows_assigned_ = false;       // assign_rows ran since the last reset (pipelined start)
   double vmax_ = 0.0;
   float abs_margin_ = 0.f;
   std::vector<cudaEvent_t> ev_start_, ev_stop_;

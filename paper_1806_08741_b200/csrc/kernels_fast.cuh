@@ -74,6 +74,7 @@ struct FastParams {
   int aligned4;       // dims[0] % 4 == 0: 4-voxel runs are vector-aligned
   int max_cand;       // regions with more candidates take the exact crowded path
   int skip_full;      // k_assign_fast: full regions were done by k_assign_lean
+  int first;          // every label word of the slab is undefined (iteration 0 after a reset)
   float vmax;         // value range of the image (max |v|; dtype max for u8/u16)
   // TMA descriptors of the label words (dims0 x dims1 x slab planes, u32) and
   // the image (dims0*C x dims1 x data planes) for 8x4x4 box loads
@@ -208,6 +209,41 @@ constexpr uint32_t kSentKey = 0x1E800000u * 8u;        // fkey(2^-66, 0)
 constexpr float kSentinel = 1.3552527156068805e-20f;   // 2^-66
 __device__ __forceinline__ uint32_t min3u(uint32_t a, uint32_t b, uint32_t c) {
   return min(min(a, b), c);
+}
+
+// Upper bound, over every voxel of a box, of the (scaled) fp32 distance to
+// candidate j -- +inf unless j's window covers the whole box, so that every
+// voxel of the box really evaluates j. A box that holds undefined voxels
+// (d_old = +inf, slic.hpp:285-297 on a fresh DistanceMap) has no finite
+// "largest carried-over distance" to prune against; the smallest such bound
+// UB_r takes its place: a candidate k with LB_k > UB_r has D_k(v) > D_r(v) at
+// every voxel, so the strict-minimum scan never picks k (iteration 0: the 3^n
+// covering candidates drop to the ones that can win). crec = the record's
+// (c_hi, c_lo) pairs; b0/b1 = the box's inclusive region-local extent.
+template <int RANK, int C>
+__device__ __forceinline__ float box_upper_bound(const FastSmem& sm, const float* crec, int j,
+                                                 bool overlaps, const float* pmin,
+                                                 const float* pmax, const int* b0, const int* b1,
+                                                 const int* grid, const float* inv_grid,
+                                                 float msq_scaled) {
+  bool all = overlaps;
+  float sl = 0.f;
+#pragma unroll
+  for (int a = 0; a < RANK; ++a) {
+    const int an = sm.anc[j][a];
+    all &= (an - grid[a] <= b0[a]) & (an + grid[a] >= b1[a]);
+    const float cpl = sm.cpl[j][a];
+    const float t = (fmaxf(cpl - (float)b0[a], (float)b1[a] - cpl) + 1e-3f) * inv_grid[a];
+    sl = fmaf(t, t, sl);
+  }
+  float ub = sl * msq_scaled;
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    const float ch = crec[2 * c], cl = fabsf(crec[2 * c + 1]);
+    const float t = fmaxf(pmax[c] - ch, ch - pmin[c]) + cl;
+    ub = fmaf(t, t, ub);
+  }
+  return all ? ub : kInf;
 }
 
 // Exact per-voxel decision over the region's candidate list (fp64, the

@@ -210,7 +210,10 @@ __host__ __device__ constexpr int fast_queue_cap(int C) { return C == 3 ? 32 : 0
 // T is the caller's storage type; T = double sweeps an f32 working copy (TW)
 // with the pixel rounding folded into the margins, and takes the exact f64
 // values for the re-decisions and the fixed-point deltas.
-// VAR bits: 1 no spatial lower bound, 2 full regions only (clipping folded)
+// VAR bits: 1 no spatial lower bound, 2 full regions only (clipping folded),
+// 4 first iteration (every label word of the slab is undefined: no word loads, no
+// carried-over distances; candidates pruned by box_upper_bound), 16 TMA box
+// tiles, 32 L2 prefetch of the next box's unstaged pixel runs
 template <int RANK, int C, typename TS, int RXc, int RYc, int RZc, int CAPc = 0, int VAR = 0>
 __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fast(const __grid_constant__ FastParams P) {
   constexpr bool kF64 = std::is_same<TS, double>::value;
@@ -273,6 +276,7 @@ __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fas
   // box is whole, so the clipping below folds to constants
   constexpr bool kFull = (VAR & 2) != 0 && RANK == 3 && RXc > 0;
   if (kFull && !region_full(P, org, RX, RY, RZ)) return;
+  constexpr bool kFirst = (VAR & 4) != 0;
   const int64_t hi[3] = {min(org[0] + RX, g.dims[0]) - 1, min(org[1] + RY, g.dims[1]) - 1,
                          RANK == 3 ? min(org[2] + RZ, g.dims[2]) - 1 : 0};
   const int64_t zlo = RANK == 3 ? max(org[2], g.slab_begin) : 0;
@@ -407,7 +411,7 @@ __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fas
     }
     const BoxG q = box_geom(bn);
     if (!q.vec) return;
-    cp_async16(my_pfw + buf * 32, lab_r + q.rel);
+    if constexpr (!kFirst) cp_async16(my_pfw + buf * 32, lab_r + q.rel);
     if (kPW) {
       const unsigned char* src = reinterpret_cast<const unsigned char*>(img_r + q.rel * C);
       uint32_t* dst = my_pfp + buf * 32 * (kPW ? kPW : 1);
@@ -416,6 +420,13 @@ __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fas
       else
 #pragma unroll
         for (int i = 0; i < kPW; ++i) cp_async4(dst + i, src + 4 * i);
+    } else if constexpr ((VAR & 32) != 0) {
+      // runs wider than one 16-byte cp.async are not staged: pull the next
+      // box's pixel lines into L2 so the direct loads do not wait on DRAM
+      const unsigned char* src = reinterpret_cast<const unsigned char*>(img_r + q.rel * C);
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(src));
+      if constexpr (4 * C * (int)sizeof(T) > 128)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(src + 128));
     }
   };
 
@@ -595,7 +606,10 @@ __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fas
       tma_phase ^= 1u << buf;
     }
     const int toff = (zq * Box::Y + yq) * Box::X + 4 * xq;  // lane's run in the 8x4x4 tiles
-    if (kTma) {
+    if constexpr (kFirst) {
+#pragma unroll
+      for (int v = 0; v < 4; ++v) word[v] = kUndefined;
+    } else if (kTma) {
       const uint4 q = *reinterpret_cast<const uint4*>(my_tiles + buf * kTileBuf + 4 * toff);
       word[0] = q.x;
       word[1] = q.y;
@@ -645,7 +659,7 @@ __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fas
     for (int v = 0; v < 4; ++v) {
       rep[v] = v > 0 && word[v] == word[v - 1] ? rep[v - 1] : v;
       any_undef |= valid[v] & (word[v] == kUndefined);
-      {  // predicated copies (no branch per voxel)
+      if constexpr (!kFirst) {  // predicated copies (no branch per voxel)
         const bool need = (rep[v] == v) & valid[v] & (word[v] != kUndefined);
         const uint32_t L = word[v] & lmask, Tg = word[v] >> lbits;
         // (history rows < 2^32: tag mode caps the tables at 8 GB)
@@ -751,8 +765,25 @@ __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fas
       dold[v] = has ? d * P.key_scale2 : kInf;
       dmax = has ? fmaxf(dmax, dold[v]) : dmax;
     }
-    dmax = any_undef ? kInf : dmax * (1.0f + M) + A;
-    dmax = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(dmax)));
+    if constexpr (kFirst) {
+      // no finite d_old bounds undefined voxels; the smallest upper bound of
+      // a candidate that covers the whole box does (box_upper_bound)
+      const int b0[3] = {bx0, by0, bz0c}, b1[3] = {bx1, by1, bz1};
+      const int sg[3] = {(int)g.grid[0], (int)g.grid[1], RANK == 3 ? (int)g.grid[2] : 0};
+      float ub = kInf;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int j = lane + 32 * h;
+        ub = fminf(ub, box_upper_bound<RANK, C>(sm, rec + j * RS + HO, j, cov[h], pmin, pmax, b0,
+                                                b1, sg, P.inv_grid,
+                                                (float)g.m_sq * P.key_scale2));
+      }
+      ub = __uint_as_float(__reduce_min_sync(0xffffffffu, __float_as_uint(ub)));
+      dmax = (ub * (1.0f + 4.0f * M) + A) * (1.0f + M) + A;
+    } else {
+      dmax = any_undef ? kInf : dmax * (1.0f + M) + A;
+      dmax = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(dmax)));
+    }
 
     // candidates covering this box whose lower bound over the box can beat
     // some voxel's d_old -> compact warp list (padded to pairs). A candidate
@@ -1524,9 +1555,9 @@ namespace sslic_b200 {
 // k_assign_lean over the full regions (the compile-time shapes of configs 3
 // and 5); returns false when the geometry is not one of them. *all_full:
 // no clipped region exists (k_assign_fast then needs no launch).
-template <int C, typename T, int RXc, int RYc, int RZc, int CAPc, int MINB>
+template <int C, typename T, int RXc, int RYc, int RZc, int CAPc, int MINB, int FIRST = 0>
 void launch_lean_shape(const FastParams& P, int64_t nblocks, cudaStream_t s) {
-  auto kern = k_assign_lean<C, T, RXc, RYc, RZc, CAPc, MINB>;
+  auto kern = k_assign_lean<C, T, RXc, RYc, RZc, CAPc, MINB, FIRST>;
   static std::atomic<unsigned long long> configured{0};
   int dev = 0;
   SSLIC_CUDA_CHECK(cudaGetDevice(&dev));
@@ -1562,7 +1593,10 @@ inline bool launch_lean(const FastParams& P, int64_t nblocks, cudaStream_t s) {
       fast_cand_need(g, R) <= 40 && P.max_cand >= 40) {
     FastParams Q = P;
     Q.max_cand = 40;
-    launch_lean_shape<3, uint8_t, 32, 32, 32, 40, 4>(Q, nblocks, s);  // config 5
+    if (P.first && std::getenv("SSLIC_NO_FIRST") == nullptr)
+      launch_lean_shape<3, uint8_t, 32, 32, 32, 40, 4, 1>(Q, nblocks, s);  // iteration 0
+    else
+      launch_lean_shape<3, uint8_t, 32, 32, 32, 40, 4>(Q, nblocks, s);  // config 5
     return true;
   }
   return false;
@@ -1660,6 +1694,15 @@ void launch_fast_t(const FastParams& P, size_t smem, int64_t nblocks, cudaStream
       const double sp = P.g.m_sq * 3.0 * 4.0, cr = (double)P.vmax / 64.0;
       const bool no_slb = sp < cr * cr && std::getenv("SSLIC_KEEP_SPATIAL_LB") == nullptr;
       // full regions first (clipping folded away), then the clipped ones
+      const bool first = P.first && std::getenv("SSLIC_NO_FIRST") == nullptr;
+      if (first && P.aligned4) {  // iteration 0: no words, no d_old (VAR & 4)
+        if (no_slb) launch_fast_shape<RANK, C, T, 32, 16, 16, 0, 7>(P, smem, nblocks, s);
+        else launch_fast_shape<RANK, C, T, 32, 16, 16, 0, 6>(P, smem, nblocks, s);
+        if (all_regions_full(P)) return;
+        FastParams Q = P;
+        Q.skip_full = 1;
+        return launch_fast_shape<RANK, C, T, 32, 16, 16, 0, 4>(Q, smem, nblocks, s);
+      }
       if (P.aligned4 && std::getenv("SSLIC_NO_FULL") == nullptr) {
         FastParams T2 = P;
         // TMA box tiles: correct, but 7.8 % slower than the per-lane cp.async
@@ -1681,8 +1724,19 @@ void launch_fast_t(const FastParams& P, size_t smem, int64_t nblocks, cudaStream
   }
   if constexpr (RANK == 3 && C == 4 && sizeof(T) == 4) {
     if (R[0] == 16 && R[1] == 16 && R[2] == 8) {  // config 4
+      const bool first = P.first && std::getenv("SSLIC_NO_FIRST") == nullptr;
+      if (first && P.aligned4) {
+        launch_fast_shape<RANK, C, T, 16, 16, 8, 0, 38>(P, smem, nblocks, s);
+        if (all_regions_full(P)) return;
+        FastParams Q = P;
+        Q.skip_full = 1;
+        return launch_fast_shape<RANK, C, T, 16, 16, 8, 0, 4>(Q, smem, nblocks, s);
+      }
       if (P.aligned4 && std::getenv("SSLIC_NO_FULL") == nullptr) {
-        launch_fast_shape<RANK, C, T, 16, 16, 8, 0, 2>(P, smem, nblocks, s);
+        if (std::getenv("SSLIC_NO_PF_L2") == nullptr)
+          launch_fast_shape<RANK, C, T, 16, 16, 8, 0, 34>(P, smem, nblocks, s);
+        else
+          launch_fast_shape<RANK, C, T, 16, 16, 8, 0, 2>(P, smem, nblocks, s);
         if (all_regions_full(P)) return;
         FastParams Q = P;
         Q.skip_full = 1;
@@ -1698,6 +1752,9 @@ void launch_fast_t(const FastParams& P, size_t smem, int64_t nblocks, cudaStream
       if (fast_cand_need(P.g, R) <= 40) {
         FastParams Q = P;
         if (Q.max_cand > 40) Q.max_cand = 40;
+        if (P.first && std::getenv("SSLIC_NO_FIRST") == nullptr)
+          return launch_fast_shape<RANK, C, T, 32, 32, 32, 40, 4>(Q, fast_smem_bytes(P.g, R, 40),
+                                                                 nblocks, s);
         return launch_fast_shape<RANK, C, T, 32, 32, 32, 40>(Q, fast_smem_bytes(P.g, R, 40),
                                                             nblocks, s);
       }
@@ -1705,12 +1762,18 @@ void launch_fast_t(const FastParams& P, size_t smem, int64_t nblocks, cudaStream
     }
   }
   if constexpr (RANK == 2 && C == 3 && sizeof(T) == 4) {
-    if (R[0] == 64 && R[1] == 32)
-      return launch_fast_shape<RANK, C, T, 64, 32, 1>(P, smem, nblocks, s);  // config 2
+    if (R[0] == 64 && R[1] == 32) {  // config 2
+      if (P.first && std::getenv("SSLIC_NO_FIRST") == nullptr)
+        return launch_fast_shape<RANK, C, T, 64, 32, 1, 0, 4>(P, smem, nblocks, s);
+      return launch_fast_shape<RANK, C, T, 64, 32, 1>(P, smem, nblocks, s);
+    }
   }
   if constexpr (RANK == 2 && C == 3 && sizeof(T) == 1) {
-    if (R[0] == 16 && R[1] == 16)
-      return launch_fast_shape<RANK, C, T, 16, 16, 1>(P, smem, nblocks, s);  // config 1
+    if (R[0] == 16 && R[1] == 16) {  // config 1
+      if (P.first && std::getenv("SSLIC_NO_FIRST") == nullptr)
+        return launch_fast_shape<RANK, C, T, 16, 16, 1, 0, 4>(P, smem, nblocks, s);
+      return launch_fast_shape<RANK, C, T, 16, 16, 1>(P, smem, nblocks, s);
+    }
   }
   launch_fast_shape<RANK, C, T, 0, 0, 0>(P, smem, nblocks, s);
 }

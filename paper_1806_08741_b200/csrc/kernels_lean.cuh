@@ -114,9 +114,13 @@ inline size_t lean_smem_bytes(const Geom& g, const int* R, int cap, int ntags) {
   return (b + 15) & ~(size_t)15;
 }
 
-template <int C, typename T, int RXc, int RYc, int RZc, int CAPc, int MINB>
+// FIRST: every label word of the slab is undefined (iteration 0 after a
+// reset): no word loads, no history rows, no carried-over distances; the
+// candidates of a half box are pruned by box_upper_bound instead.
+template <int C, typename T, int RXc, int RYc, int RZc, int CAPc, int MINB, int FIRST = 0>
 __global__ void __launch_bounds__(kFastThreads, MINB) k_assign_lean(const __grid_constant__ FastParams P) {
   constexpr int RANK = 3;
+  constexpr bool kFirst = FIRST != 0;
   using Sh = LeanShape<RXc, RYc, RZc>;
   constexpr int RX = RXc, RY = RYc, RZ = RZc;
   constexpr int kStride = C + RANK;
@@ -180,7 +184,7 @@ __global__ void __launch_bounds__(kFastThreads, MINB) k_assign_lean(const __grid
   auto prefetch = [&](int bn, int r) {
     if (bn >= Sh::NBOX) return;
     const int q = box_rel(bn) + r * run_step;
-    cp_async16(my_pfw + r * 32, lab_r + q);
+    if constexpr (!kFirst) cp_async16(my_pfw + r * 32, lab_r + q);
     const unsigned char* src = reinterpret_cast<const unsigned char*>(img_r + (size_t)q * C);
     uint32_t* dst = my_pfp + (size_t)r * 32 * kPW;
     if constexpr (kPW == 4) cp_async16(dst, src);
@@ -307,7 +311,7 @@ __global__ void __launch_bounds__(kFastThreads, MINB) k_assign_lean(const __grid
   }
   __syncthreads();  // cxy scratch is read above; the history rows overwrite it
   // history rows of every candidate for every tag so far: hs[j * ntags + t]
-  {
+  if constexpr (!kFirst) {
     constexpr int kChunks = kS2 / 2;  // 16-byte pieces per row
     for (int i = tid; i < n * kChunks; i += kFastThreads) {
       const int j = i / kChunks, piece = i - j * kChunks;
@@ -359,11 +363,16 @@ __global__ void __launch_bounds__(kFastThreads, MINB) k_assign_lean(const __grid
       cp_async_wait_group1();  // this run's group (the other run's may stay in flight)
       __syncwarp();
       {
-        const uint4 q = my_pfw[r * 32];
-        word[0] = q.x;
-        word[1] = q.y;
-        word[2] = q.z;
-        word[3] = q.w;
+        if constexpr (kFirst) {
+#pragma unroll
+          for (int v = 0; v < 4; ++v) word[v] = kUndefined;
+        } else {
+          const uint4 q = my_pfw[r * 32];
+          word[0] = q.x;
+          word[1] = q.y;
+          word[2] = q.z;
+          word[3] = q.w;
+        }
         uint32_t w[kPW];
 #pragma unroll
         for (int i = 0; i < kPW; ++i) w[i] = my_pfp[(size_t)r * 32 * kPW + i];
@@ -387,6 +396,13 @@ __global__ void __launch_bounds__(kFastThreads, MINB) k_assign_lean(const __grid
       const float fzv = fz0 + (float)lz;
 #pragma unroll
       for (int v = 0; v < 4; ++v) {
+        if constexpr (kFirst) {
+          oldl[v] = lmask;
+          oslot[v] = -1;
+          dold[v] = kInf;
+          any_undef = true;
+          continue;
+        }
         const uint32_t w = word[v];
         const bool def = w != kUndefined;
         oldl[v] = w & lmask;  // undefined -> lmask (never a label)
@@ -423,8 +439,10 @@ __global__ void __launch_bounds__(kFastThreads, MINB) k_assign_lean(const __grid
       }
 #pragma unroll
       for (int v = 0; v < 4; ++v) dmax = fmaxf(dmax, dold[v]);
-      dmax = any_undef ? kInf : dmax * (1.0f + M) + A;
-      dmax = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(dmax)));
+      if constexpr (!kFirst) {
+        dmax = any_undef ? kInf : dmax * (1.0f + M) + A;
+        dmax = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(dmax)));
+      }
 
       // value range of the half box per channel (scaled) for the colour bounds
       float pmin[C], pmax[C];
@@ -442,6 +460,24 @@ __global__ void __launch_bounds__(kFastThreads, MINB) k_assign_lean(const __grid
       }
       // kept candidates: window overlaps the half box and LB <= max d_old
       const unsigned long long bmask = sm.bmask[0][bx] & sm.bmask[1][by] & sm.bmask[2][hz];
+      if constexpr (kFirst) {
+        // undefined voxels have no finite d_old: the smallest upper bound of a
+        // candidate covering the whole half box prunes instead (box_upper_bound)
+        const int b0[3] = {bx * Sh::BX, by * Sh::BY, hz * 4};
+        const int b1[3] = {b0[0] + Sh::BX - 1, b0[1] + Sh::BY - 1, b0[2] + 3};
+        const int sg[3] = {(int)g.grid[0], (int)g.grid[1], (int)g.grid[2]};
+        float ub = kInf;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int j = lane + 32 * h;
+          const bool c = (uint32_t)(bmask >> (32 * h)) >> lane & 1u;
+          if (j < kCap)
+            ub = fminf(ub, box_upper_bound<RANK, C>(sm, rec + j * RS + HO, j, c, pmin, pmax, b0, b1,
+                                                    sg, P.inv_grid, (float)g.m_sq * P.key_scale2));
+        }
+        ub = __uint_as_float(__reduce_min_sync(0xffffffffu, __float_as_uint(ub)));
+        dmax = (ub * (1.0f + 4.0f * M + kLeanTau) + A) * (1.0f + M) + A;
+      }
       const float* lbx = lbs + bx * kCap;
       const float* lby = lbs + (Sh::NBX + by) * kCap;
       const float* lbz = lbs + (Sh::NBX + Sh::NBY + hz) * kCap;
