@@ -1775,6 +1775,8 @@ void launch_fast_t(const FastParams& P, size_t smem, int64_t nblocks, cudaStream
       return launch_fast_shape<RANK, C, T, 16, 16, 1>(P, smem, nblocks, s);
     }
   }
+  if (P.first && std::getenv("SSLIC_NO_FIRST") == nullptr)
+    return launch_fast_shape<RANK, C, T, 0, 0, 0, 0, 4>(P, smem, nblocks, s);
   launch_fast_shape<RANK, C, T, 0, 0, 0>(P, smem, nblocks, s);
 }
 

@@ -545,11 +545,13 @@ def test_engine_reset_reruns_identically(sslic, exact):
     assert np.array_equal(l1, l2) and np.array_equal(c1, c2) and np.array_equal(r1, r2)
 
 
-@pytest.mark.parametrize("env", ["SSLIC_TMA", "SSLIC_NO_FULL", "SSLIC_KEEP_SPATIAL_LB"])
+@pytest.mark.parametrize("env", ["SSLIC_TMA", "SSLIC_NO_FULL", "SSLIC_KEEP_SPATIAL_LB",
+                                 "SSLIC_NO_FIRST"])
 def test_fast_variants_equal_exact(sslic, env, monkeypatch):
     """The kernel variants behind launch-time switches -- TMA box tiles
     (cp.async.bulk.tensor + mbarrier), the clipped-region kernel on full
-    regions, the spatial lower bound kept -- equal the exact kernel bit for
+    regions, the spatial lower bound kept, the general kernel instead of the
+    first-iteration one at iteration 0 -- equal the exact kernel bit for
     bit at every iteration (config-3 shape: 32x16x16 regions, full and
     clipped)."""
     import torch
@@ -573,3 +575,49 @@ def test_fast_variants_equal_exact(sslic, env, monkeypatch):
         torch.cuda.synchronize()
         assert int((la != lb).sum().item()) == 0, f"{env}: iteration {it}"
         assert np.array_equal(fast.centers(), exact.centers()), f"{env}: iteration {it}"
+
+
+@pytest.mark.parametrize("cfg,dims,ch,dtype,grid,m", [
+    (3, (168, 144, 120), 1, np.uint16, (16, 16, 16), 10.0),
+    (4, (80, 72, 40), 4, np.float32, (8, 8, 8), 20.0),
+    (5, (96, 96, 96), 3, np.uint8, (32, 32, 32), 10.0),
+    (1, (112, 80), 3, np.uint8, (16, 16), 10.0),
+])
+def test_first_iteration_kernel_only_on_fresh_words(sslic, cfg, dims, ch, dtype, grid, m):
+    """The first-iteration kernel (no label-word loads, no carried-over
+    distances) may only run while every word is undefined: a second assign at
+    iteration 0 (labels now defined, same centres) must take the general
+    kernel and, like the exact kernel, keep every label; after reset() the
+    first-iteration kernel applies again and reproduces the run."""
+    import torch
+    s = sslic
+    img, fast, exact = _engines(s, cfg, dims, ch, dtype, grid, m, 4, torch)
+    n = int(np.prod(dims))
+    la = torch.empty(n, dtype=torch.int32, device="cuda")
+    lb = torch.empty(n, dtype=torch.int32, device="cuda")
+
+    def clean_run():
+        fast.init()
+        fast.commit()
+        for _ in range(2):
+            fast.assign()
+            fast.update()
+        return fast.centers().copy()
+
+    c_clean = clean_run()
+    fast.reset()
+    for e in (fast, exact):
+        e.init()
+        e.commit()
+        e.assign()
+    fast.labels_to(la.data_ptr())
+    first = la.clone()
+    for e in (fast, exact):
+        e.assign()  # same centres: D* == d_old everywhere, nothing may change
+    fast.labels_to(la.data_ptr())
+    exact.labels_to(lb.data_ptr())
+    torch.cuda.synchronize()
+    assert int((la != lb).sum().item()) == 0
+    assert int((la != first).sum().item()) == 0
+    fast.reset()
+    assert np.array_equal(clean_run(), c_clean)
