@@ -1574,6 +1574,10 @@ void launch_lean_shape(const FastParams& P, int64_t nblocks, cudaStream_t s) {
   kern<<<(unsigned)nblocks, kFastThreads, smem, s>>>(P);
 }
 
+// Build split (SSLIC_FAST_SPLIT, csrc/Makefile): the kernel instantiations are
+// spread over fast_inst_*.cu so they compile in parallel; engine.cu only sees
+// declarations. Without the macro this header is self-contained.
+#if !defined(SSLIC_FAST_SPLIT)
 inline bool launch_lean(const FastParams& P, int64_t nblocks, cudaStream_t s) {
   const Geom& g = P.g;
   if (g.rank != 3 || !P.aligned4 || std::getenv("SSLIC_NO_LEAN") != nullptr) return false;
@@ -1601,6 +1605,37 @@ inline bool launch_lean(const FastParams& P, int64_t nblocks, cudaStream_t s) {
   }
   return false;
 }
+#elif defined(SSLIC_FAST_TU_LEAN)
+bool launch_lean(const FastParams& P, int64_t nblocks, cudaStream_t s) {
+  const Geom& g = P.g;
+  if (g.rank != 3 || !P.aligned4 || std::getenv("SSLIC_NO_LEAN") != nullptr) return false;
+  const int* R = P.R;
+  // config 3 (1 channel, 8.6 evaluations per voxel): measured slower than
+  // k_assign_fast (76.8 vs 83.2 Gvox/s, profiles/r2/lean_ab.txt) -- kept
+  // behind SSLIC_LEAN_C1=1 for experiments; config 5 gains 11 %
+  if (g.channels == 1 && g.dtype == SSLIC_U16 && R[0] == 32 && R[1] == 16 && R[2] == 16 &&
+      std::getenv("SSLIC_LEAN_C1") != nullptr && fast_cand_need(g, R) <= 56 &&
+      P.max_cand >= 56) {
+    FastParams Q = P;
+    Q.max_cand = 56;
+    launch_lean_shape<1, uint16_t, 32, 16, 16, 56, 5>(Q, nblocks, s);  // config 3
+    return true;
+  }
+  if (g.channels == 3 && g.dtype == SSLIC_U8 && R[0] == 32 && R[1] == 32 && R[2] == 32 &&
+      fast_cand_need(g, R) <= 40 && P.max_cand >= 40) {
+    FastParams Q = P;
+    Q.max_cand = 40;
+    if (P.first && std::getenv("SSLIC_NO_FIRST") == nullptr)
+      launch_lean_shape<3, uint8_t, 32, 32, 32, 40, 4, 1>(Q, nblocks, s);  // iteration 0
+    else
+      launch_lean_shape<3, uint8_t, 32, 32, 32, 40, 4>(Q, nblocks, s);  // config 5
+    return true;
+  }
+  return false;
+}
+#else
+bool launch_lean(const FastParams& P, int64_t nblocks, cudaStream_t s);
+#endif
 
 // TMA descriptors for the full-region box loads (k_assign_fast VAR & 16):
 // label words of the slab (u32) and the image's data planes (channels
@@ -1790,6 +1825,15 @@ void launch_fast_c(const FastParams& P, size_t smem, int64_t nb, cudaStream_t s)
   }
 }
 
+#if defined(SSLIC_FAST_SPLIT) && !defined(SSLIC_FAST_TU_INST)
+#define SSLIC_FAST_EXTERN(R, C) \
+  extern template void launch_fast_c<R, C>(const FastParams&, size_t, int64_t, cudaStream_t);
+SSLIC_FAST_EXTERN(2, 1) SSLIC_FAST_EXTERN(2, 2) SSLIC_FAST_EXTERN(2, 3) SSLIC_FAST_EXTERN(2, 4)
+SSLIC_FAST_EXTERN(3, 1) SSLIC_FAST_EXTERN(3, 2) SSLIC_FAST_EXTERN(3, 3) SSLIC_FAST_EXTERN(3, 4)
+#undef SSLIC_FAST_EXTERN
+#endif
+
+#if !defined(SSLIC_FAST_TU_INST)
 template <int RANK>
 void launch_fast_r(const FastParams& P, size_t smem, int64_t nb, cudaStream_t s) {
   switch (P.g.channels) {
@@ -1800,6 +1844,8 @@ void launch_fast_r(const FastParams& P, size_t smem, int64_t nb, cudaStream_t s)
   }
 }
 
+#endif  // !SSLIC_FAST_TU_INST
+
 // Relative fp32 decision margin: each fp32
 // distance is within (C + 14) u of the fp64 one (u = 2^-24; includes the
 // fp32 spatial tables and reciprocal multiplies; the key scaling is exact and
@@ -1809,6 +1855,7 @@ inline float fast_margin(int channels) {
   return (float)(1.5 * 2.0 * (channels + 14) * u);
 }
 
+#if !defined(SSLIC_FAST_TU_INST)
 // (row0 < row1: only region rows [row0, row1) of the slab, z-ordered)
 inline void launch_fast_assign(FastParams P, cudaStream_t s, int64_t row0 = 0,
                                int64_t row1 = -1) {
@@ -1864,5 +1911,7 @@ inline void launch_fast_assign(FastParams P, cudaStream_t s, int64_t row0 = 0,
     launch_fast_r<2>(P, smem, nb, s);
   }
 }
+
+#endif  // !SSLIC_FAST_TU_INST
 
 }  // namespace sslic_b200
