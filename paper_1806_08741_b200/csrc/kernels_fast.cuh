@@ -109,6 +109,7 @@ struct BoxShape<3> {
 struct alignas(16) FastSmem {
   unsigned long long tma_bar[kFastThreads / 32][2];  // per warp, per box buffer (TMA loads)
   int n_cand;
+  unsigned stats[3];  // k_assign_lean diagnostics (P.eval_count): fp64 re-decisions, label changes, evaluations
   int id[kFastMaxCand];
   short anc[kFastMaxCand][3];  // region-local anchors
   alignas(8) uint32_t wl[kFastThreads / 32][kFastMaxCand + 8];  // record offsets (floats)

@@ -203,7 +203,10 @@ __global__ void __launch_bounds__(kFastThreads, MINB) k_assign_lean(const __grid
   const int total = __ldg(rc);
   const int n = total < P.max_cand ? total : P.max_cand;
   for (int j = tid; j < n; j += kFastThreads) sm.id[j] = __ldg(rc + 1 + j);
-  if (tid == 0) sm.n_cand = n;
+  if (tid == 0) {
+    sm.n_cand = n;
+    sm.stats[0] = sm.stats[1] = sm.stats[2] = 0u;
+  }
   if (total > P.max_cand) {  // uniform
     cp_async_wait_all();
     if (tid == 0) atomicAdd(P.counters + 6, 1ull);
@@ -328,12 +331,16 @@ __global__ void __launch_bounds__(kFastThreads, MINB) k_assign_lean(const __grid
   // ---- per-warp sweep over the region's boxes ----
   uint2* const queue = queues + (size_t)warp * (kLeanQCap + 2);
   int qn = 0;
-  unsigned n_changed = 0, n_redecided = 0, n_evals = 0;
+  // (diagnostics are counted in shared memory, only when asked for)
+  const bool stats = P.eval_count != nullptr;
   const int64_t org0 = org[0], org1 = org[1], org2 = org[2];
   auto redecide = [&](uint2 e) {
-    n_changed += redecide_queued<RANK, C, T>(P, sm, accs, org, lab_r, img_r, nullptr, s1, s2,
-                                             false, e);
-    ++n_redecided;
+    const unsigned ch = redecide_queued<RANK, C, T>(P, sm, accs, org, lab_r, img_r, nullptr, s1,
+                                                    s2, false, e);
+    if (stats) {
+      atomicAdd(&sm.stats[0], 1u);
+      if (ch) atomicAdd(&sm.stats[1], ch);
+    }
   };
   auto drain = [&]() {
     __syncwarp();
@@ -512,7 +519,7 @@ __global__ void __launch_bounds__(kFastThreads, MINB) k_assign_lean(const __grid
         __syncwarp();
       }
       const int nlp = (nl + 1) & ~1;
-      n_evals += 4u * (unsigned)nl;
+      if (stats && lane == 0) atomicAdd(&sm.stats[2], 128u * (unsigned)nl);
 
       // fp32 argmin with runner-up; keys carry the record slot
       f2 p01[C], p23[C];
@@ -598,7 +605,10 @@ __global__ void __launch_bounds__(kFastThreads, MINB) k_assign_lean(const __grid
       unsigned chm = 0;
 #pragma unroll
       for (int v = 0; v < 4; ++v) chm |= (unsigned)(newl[v] != oldl[v]) << v;
-      n_changed += (unsigned)__popc(chm);
+      if (stats) {  // uniform
+        const unsigned c = __reduce_add_sync(0xffffffffu, (unsigned)__popc(chm));
+        if (lane == 0 && c) atomicAdd(&sm.stats[1], c);
+      }
       unsigned pending = chm | chm << 4;
       if (__any_sync(0xffffffffu, any_undef)) {
         unsigned undef = 0, olddef = 0;
@@ -774,17 +784,12 @@ __global__ void __launch_bounds__(kFastThreads, MINB) k_assign_lean(const __grid
   }
   if (qn > 0) drain();
   cp_async_wait_all();
-  if (P.eval_count) {
-    const unsigned a = __reduce_add_sync(0xffffffffu, n_redecided);
-    const unsigned c = __reduce_add_sync(0xffffffffu, n_changed);
-    const unsigned e = __reduce_add_sync(0xffffffffu, n_evals);
-    if (lane == 0) {
-      atomicAdd(P.counters + 5, (unsigned long long)a);
-      atomicAdd(P.counters + 7, (unsigned long long)c);
-      atomicAdd(P.eval_count, (unsigned long long)e);
-    }
-  }
   __syncthreads();
+  if (stats && tid == 0) {
+    atomicAdd(P.counters + 5, (unsigned long long)sm.stats[0]);
+    atomicAdd(P.counters + 7, (unsigned long long)sm.stats[1]);
+    atomicAdd(P.eval_count, (unsigned long long)sm.stats[2]);
+  }
   // ---- flush CTA slots (one global atomic per non-zero component) ----
   for (int t = tid; t < n * kComp; t += kFastThreads) {
     const int j = t / kComp, cp = t - j * kComp;
