@@ -125,7 +125,10 @@ __device__ __forceinline__ void load_run(const T* src, bool vec, const bool* val
 // CTAs per SM the register budget targets: 5 (96 registers) where the
 // shared-memory footprint allows it (1-2 channels; measured +2% on config 3),
 // else 4 (128 registers; 5 costs config 4 7% through spills)
-__host__ __device__ constexpr int fast_min_blocks(int C) { return C <= 2 ? 5 : 4; }
+__host__ __device__ constexpr int fast_min_blocks(int C, int VAR = 0) {
+  // (the first-iteration kernel, VAR & 4, spills 28 B at 96 registers: 4 CTAs there)
+  return C <= 2 && !(VAR & 4) ? 5 : 4;
+}
 
 // fp64 re-decision of one queued voxel of the fast kernel (entry: old label
 // word, region-local coordinates | amb | winner slot): writes the label word
@@ -215,7 +218,7 @@ __host__ __device__ constexpr int fast_queue_cap(int C) { return C == 3 ? 32 : 0
 // carried-over distances; candidates pruned by box_upper_bound), 16 TMA box
 // tiles, 32 L2 prefetch of the next box's unstaged pixel runs
 template <int RANK, int C, typename TS, int RXc, int RYc, int RZc, int CAPc = 0, int VAR = 0>
-__global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fast(const __grid_constant__ FastParams P) {
+__global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C, VAR)) k_assign_fast(const __grid_constant__ FastParams P) {
   constexpr bool kF64 = std::is_same<TS, double>::value;
   using T = typename std::conditional<kF64, float, TS>::type;  // working pixel type
   using Box = BoxShape<RANK>;
@@ -1338,7 +1341,7 @@ __global__ void __launch_bounds__(kFastThreads, fast_min_blocks(C)) k_assign_fas
   // 128-register kernels: one (candidate, component) pair per thread (every
   // lane busy; config 4 -4 %); the 96-register ones keep one warp per
   // candidate (the pair loop costs them spills)
-  if constexpr (fast_min_blocks(C) == 4) {
+  if constexpr (fast_min_blocks(C, VAR) == 4) {
     for (int t = tid; t < n * kComp; t += kFastThreads) {
       const int j = t / kComp, cp = t - j * kComp;
       long long v = (long long)accs[j * kCompA + cp];
