@@ -414,7 +414,11 @@ __global__ void __launch_bounds__(kFastThreads, MINB) k_assign_lean(const __grid
         const bool def = w != kUndefined;
         oldl[v] = w & lmask;  // undefined -> lmask (never a label)
         const uint32_t tg = def ? (w >> lbits) : 0u;
-        const int sl = def ? lean_slot(htab2, oldl[v]) : -1;
+        // (the lookup runs once per run of equal labels: most 4-voxel runs
+        // of a coherent label map hold one label)
+        int sl;
+        if (v > 0 && oldl[v] == oldl[v - 1]) sl = oslot[v - 1];
+        else sl = def ? lean_slot(htab2, oldl[v]) : -1;
         oslot[v] = sl;
         fb |= (unsigned)(def & (sl < 0)) << v;
         const float2* hr = hs + ((sl >= 0 ? sl : 0) * ntags + (sl >= 0 ? (int)tg : 0)) * kS2;
