@@ -65,3 +65,29 @@ def test_no_cpu_fallback_without_device():
     import paper_1806_08741_b200 as s
     with pytest.raises(s.CudaError):
         s.run_slic(s.NDImage.zeros((8, 8), 1), s.SlicParams(grid=[4, 4]))
+
+
+def test_library_holds_sm100a_kernels_only():
+    """The product library is built for sm_100a alone (no other targets, no
+    PTX-JIT fallback) and holds the hot kernels: the general and the
+    first-iteration variants of k_assign_fast / k_assign_lean, the fused
+    update and the connectivity kernels (cuobjdump, no GPU needed)."""
+    import shutil
+    import subprocess
+    import paper_1806_08741_b200 as s
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(tool):
+        pytest.skip("cuobjdump not available")
+    out = subprocess.run([tool, "-lelf", s.LIB_PATH], capture_output=True, text=True).stdout
+    elfs = [l for l in out.splitlines() if ".cubin" in l]
+    assert elfs and all("sm_100a" in l for l in elfs), elfs[:4]
+    ptx = subprocess.run([tool, "-lptx", s.LIB_PATH], capture_output=True, text=True).stdout
+    assert ".ptx" not in ptx or "sm_100a" in ptx
+    syms = subprocess.run(["nm", "-C", s.LIB_PATH], capture_output=True, text=True).stdout
+    for kernel in ("k_assign_fast<3, 1, unsigned short, 32, 16, 16, 0, 3>",   # config 3, general
+                   "k_assign_fast<3, 1, unsigned short, 32, 16, 16, 0, 7>",   # config 3, iteration 0
+                   "k_assign_fast<3, 4, float, 16, 16, 8, 0, 34>",            # config 4
+                   "k_assign_lean<3, unsigned char, 32, 32, 32, 40, 4, 0>",   # config 5
+                   "k_assign_lean<3, unsigned char, 32, 32, 32, 40, 4, 1>",
+                   "k_update_fused", "k_init_perturb", "k_region_cand<3>"):
+        assert kernel in syms, kernel
