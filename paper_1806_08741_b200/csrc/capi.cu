@@ -166,7 +166,9 @@ std::unique_ptr<DeviceBuf> upload_image(const sslic_image* img, Stream& st) {
   const int64_t nvals = pixel_count(*img) * img->channels;
   const size_t bytes = (size_t)nvals * dtype_size(img->dtype);
   auto buf = std::make_unique<DeviceBuf>(bytes, st.s);
-  SSLIC_CUDA_CHECK(cudaMemcpyAsync(buf->p, img->data, bytes, cudaMemcpyHostToDevice, st.s));
+  int dev = 0;
+  SSLIC_CUDA_CHECK(cudaGetDevice(&dev));
+  copy_to_device(buf->p, img->data, bytes, dev, st.s);  // (pageable callers: striped)
   if (img->dtype == SSLIC_F32 || img->dtype == SSLIC_F64) {
     DeviceBuf cnt(sizeof(unsigned long long), st.s);
     SSLIC_CUDA_CHECK(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), st.s));
@@ -741,8 +743,7 @@ int sslic_run_slic(const sslic_image* img, const sslic_params* params, int devic
       dimg.reset();
       uint32_t* lab = e.label_words();
       e.unpack_labels(lab);
-      SSLIC_CUDA_CHECK(cudaMemcpyAsync(labels_out, lab, n * sizeof(uint32_t),
-                                       cudaMemcpyDeviceToHost, st.s));
+      copy_to_host(labels_out, lab, n * sizeof(uint32_t), device, st.s);
       st.sync();
       pt.mark(st, "labels D2H");
     }
@@ -779,8 +780,7 @@ int sslic_segment(const sslic_image* img, const sslic_params* params, int device
       next = enforce_connectivity_device(e.geom(), lab, e.current_centers(), lab, st.s);
       pt.mark(st, "connectivity");
     }
-    SSLIC_CUDA_CHECK(cudaMemcpyAsync(labels_out, lab, n * sizeof(uint32_t),
-                                     cudaMemcpyDeviceToHost, st.s));
+    copy_to_host(labels_out, lab, n * sizeof(uint32_t), device, st.s);
     st.sync();
     pt.mark(st, "labels D2H");
     e.copy_centers_to_host(centers_out);
@@ -827,8 +827,7 @@ int sslic_segment_write(const sslic_image* img, const sslic_params* params, int 
     std::vector<uint32_t> host((size_t)n);
     std::vector<uint32_t> bits(contour_path ? (size_t)words : 0);
     unsigned mx = 0;
-    SSLIC_CUDA_CHECK(
-        cudaMemcpyAsync(host.data(), lab, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, st.s));
+    copy_to_host(host.data(), lab, n * sizeof(uint32_t), device, st.s);
     if (contour_path)
       SSLIC_CUDA_CHECK(
           cudaMemcpyAsync(bits.data(), dbits.p, words * 4, cudaMemcpyDeviceToHost, st.s));

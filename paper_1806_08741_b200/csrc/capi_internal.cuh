@@ -45,6 +45,11 @@ inline void slab_bounds(int64_t last, int world, int rank, int64_t align, int64_
   *hi = std::min(units * (rank + 1) / world * align, last);
 }
 
+// Host <-> device copies that stripe large PAGEABLE buffers over host threads
+// and pinned staging (hostcopy.cu); small or pinned buffers: cudaMemcpyAsync.
+void copy_to_device(void* dev, const void* host, size_t bytes, int device, cudaStream_t s);
+void copy_to_host(void* host, const void* dev, size_t bytes, int device, cudaStream_t s);
+
 // Keep freed device memory in the stream-ordered pool across calls (capi.cu).
 void keep_pool_memory(int device);
 

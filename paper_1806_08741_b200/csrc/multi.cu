@@ -193,8 +193,9 @@ void run_rank(const sslic_image* img, const sslic_params* p, int rank, int world
   if (d0 < data_first_plane)
     throw Error(SSLIC_EINVAL, "run_slic_rank: host planes must cover the slab plus its halo");
   DevMem dimg((size_t)(d1 - d0) * plane_bytes, st.s);
-  SSLIC_CUDA_CHECK(cudaMemcpyAsync(dimg.p, static_cast<const char*>(img->data) + (d0 - data_first_plane) * plane_bytes,
-                                   (size_t)(d1 - d0) * plane_bytes, cudaMemcpyHostToDevice, st.s));
+  copy_to_device(dimg.p,
+                 static_cast<const char*>(img->data) + (d0 - data_first_plane) * plane_bytes,
+                 (size_t)(d1 - d0) * plane_bytes, device, st.s);
   if (img->dtype == SSLIC_F32 || img->dtype == SSLIC_F64) {  // NDImage checks (image.hpp:238-249)
     DevMem cnt(sizeof(unsigned long long), st.s);
     SSLIC_CUDA_CHECK(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), st.s));
@@ -234,8 +235,7 @@ void run_rank(const sslic_image* img, const sslic_params* p, int rank, int world
   const int64_t nv = (s1 - s0) * plane;
   DevMem lab((size_t)nv * sizeof(uint32_t), st.s);
   e.unpack_labels(static_cast<uint32_t*>(lab.p));
-  SSLIC_CUDA_CHECK(cudaMemcpyAsync(labels_out, lab.p, (size_t)nv * sizeof(uint32_t),
-                                   cudaMemcpyDeviceToHost, st.s));
+  copy_to_host(labels_out, lab.p, (size_t)nv * sizeof(uint32_t), device, st.s);
   SSLIC_CUDA_CHECK(cudaStreamSynchronize(st.s));
   if (centers_out) e.copy_centers_to_host(centers_out);
   if (residuals_out) e.residuals_to_host(residuals_out, e.iterations_done());

@@ -621,3 +621,29 @@ def test_first_iteration_kernel_only_on_fresh_words(sslic, cfg, dims, ch, dtype,
     assert int((la != first).sum().item()) == 0
     fast.reset()
     assert np.array_equal(clean_run(), c_clean)
+
+
+def test_striped_pageable_copies_equal_plain_copies(sslic, monkeypatch):
+    """Large pageable host buffers travel in stripes over host threads and
+    pinned staging (csrc/hostcopy.cu); the result must equal the driver's
+    plain cudaMemcpy path (SSLIC_NO_STRIPED_COPY) byte for byte -- odd sizes:
+    36 MB of pixels and 72 MB of labels, not multiples of the 8 MiB stage or
+    of the stripe unit."""
+    import torch
+    s = sslic
+    dims, ch, dtype, grid, m = (301, 299, 201), 1, np.uint16, (16, 16, 16), 10.0
+    n = int(np.prod(dims))
+    dev = torch.empty(n, dtype=torch.int16, device="cuda")
+    s.synth_generate(3, dims, dtype, ch, 4321, 0, dims[2], dev.data_ptr())
+    host = dev.cpu().numpy().view(np.uint16).copy()  # pageable
+    del dev
+    p = s.SlicParams(grid=list(grid), weight_m=m, max_iterations=3, enforce_connectivity=True)
+
+    def run():
+        res, nxt = s.segment(s.NDImage(dims, ch, host), p)
+        return res.labels.copy(), res.centers.data.copy(), nxt
+
+    l1, c1, n1 = run()
+    monkeypatch.setenv("SSLIC_NO_STRIPED_COPY", "1")
+    l2, c2, n2 = run()
+    assert n1 == n2 and np.array_equal(l1, l2) and np.array_equal(c1, c2)
