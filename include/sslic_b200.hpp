@@ -89,6 +89,17 @@ inline NativeImage narrow(const NDImage& img) {
   return out;
 }
 
+// The NDImage's own fp64 storage as an image descriptor (no copy).
+inline NativeImage view_f64(const NDImage& img) {
+  NativeImage out;
+  out.desc.rank = img.rank();
+  for (int a = 0; a < 4; ++a) out.desc.dims[a] = a < img.rank() ? img.dims()[a] : 1;
+  out.desc.channels = img.channels();
+  out.desc.dtype = SSLIC_F64;
+  out.desc.data = img.data().data();
+  return out;
+}
+
 inline sslic_params params_of(const SlicParams& p) {
   sslic_params c{};
   for (int a = 0; a < 4; ++a) c.grid[a] = a < p.grid.size() ? p.grid[a] : 1;
@@ -105,7 +116,9 @@ inline sslic_params params_of(const SlicParams& p) {
 /// run_slic (slic.hpp:384-415) on ONE given device.
 inline SlicResult run_slic_on_device(const NDImage& img, const SlicParams& params, int device) {
   params.validate(img.dims());  // same exceptions as the reference, before any copy
-  detail::NativeImage nimg = detail::narrow(img);
+  // the fp64 storage goes to the library as is: it narrows uint8 / uint16 /
+  // float32 data losslessly on the device (no host pass over the volume)
+  detail::NativeImage nimg = detail::view_f64(img);
   const sslic_params p = detail::params_of(params);
   const int iters = params.iterations_for(img.rank());
   std::vector<int64_t> dims(img.dims().begin(), img.dims().end());

@@ -162,13 +162,73 @@ struct PhaseTimer {
   }
 };
 
-std::unique_ptr<DeviceBuf> upload_image(const sslic_image* img, Stream& st) {
+// fp64 images are the reference's storage (NDImage holds doubles,
+// image.hpp:236-285) whatever the data really is. When every value is a
+// uint8 / uint16 / float32 number the volume is narrowed to that type ON THE
+// DEVICE, losslessly, and takes the native-dtype kernels: flags[0] non-finite
+// values, [1] not uint8, [2] not uint16, [3] not float32.
+__global__ void k_narrow_probe(const double* v, int64_t n, unsigned* flags) {
+  unsigned f = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double x = v[i];
+    const bool integral = x == trunc(x);
+    f |= isfinite(x) ? 0u : 1u;
+    f |= (integral && x >= 0.0 && x <= 255.0) ? 0u : 2u;
+    f |= (integral && x >= 0.0 && x <= 65535.0) ? 0u : 4u;
+    f |= ((double)(float)x == x) ? 0u : 8u;
+  }
+  f = __reduce_or_sync(0xffffffffu, f);
+  if ((threadIdx.x & 31) == 0 && f) {
+    if (f & 1u) atomicOr(flags, 1u);
+    if (f & 2u) atomicOr(flags + 1, 1u);
+    if (f & 4u) atomicOr(flags + 2, 1u);
+    if (f & 8u) atomicOr(flags + 3, 1u);
+  }
+}
+template <typename T>
+__global__ void k_narrow_convert(const double* v, int64_t n, T* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (T)v[i];
+}
+
+// narrowed_dtype (optional): fp64 input may come back as a uint8 / uint16 /
+// float32 device image (see k_narrow_probe); *narrowed_dtype is its type.
+std::unique_ptr<DeviceBuf> upload_image(const sslic_image* img, Stream& st,
+                                        int* narrowed_dtype = nullptr) {
   const int64_t nvals = pixel_count(*img) * img->channels;
   const size_t bytes = (size_t)nvals * dtype_size(img->dtype);
   auto buf = std::make_unique<DeviceBuf>(bytes, st.s);
   int dev = 0;
   SSLIC_CUDA_CHECK(cudaGetDevice(&dev));
   copy_to_device(buf->p, img->data, bytes, dev, st.s);  // (pageable callers: striped)
+  if (narrowed_dtype) *narrowed_dtype = img->dtype;
+  if (narrowed_dtype && img->dtype == SSLIC_F64 && std::getenv("SSLIC_NO_NARROW") == nullptr) {
+    DeviceBuf flags(4 * sizeof(unsigned), st.s);
+    SSLIC_CUDA_CHECK(cudaMemsetAsync(flags.p, 0, 4 * sizeof(unsigned), st.s));
+    k_narrow_probe<<<148 * 8, 256, 0, st.s>>>(buf->as<double>(), nvals, flags.as<unsigned>());
+    SSLIC_CUDA_CHECK(cudaGetLastError());
+    unsigned f[4] = {0, 0, 0, 0};
+    SSLIC_CUDA_CHECK(cudaMemcpyAsync(f, flags.p, sizeof f, cudaMemcpyDeviceToHost, st.s));
+    st.sync();
+    if (f[0]) throw Error(SSLIC_EINVAL, "NDImage: non-finite value");
+    const int dt = !f[1] ? SSLIC_U8 : !f[2] ? SSLIC_U16 : !f[3] ? SSLIC_F32 : SSLIC_F64;
+    if (dt == SSLIC_F64) return buf;  // genuinely fp64 data (checked finite above)
+    auto out = std::make_unique<DeviceBuf>((size_t)nvals * dtype_size(dt), st.s);
+    if (dt == SSLIC_U8)
+      k_narrow_convert<uint8_t><<<148 * 8, 256, 0, st.s>>>(buf->as<double>(), nvals,
+                                                          out->as<uint8_t>());
+    else if (dt == SSLIC_U16)
+      k_narrow_convert<uint16_t><<<148 * 8, 256, 0, st.s>>>(buf->as<double>(), nvals,
+                                                           out->as<uint16_t>());
+    else
+      k_narrow_convert<float><<<148 * 8, 256, 0, st.s>>>(buf->as<double>(), nvals,
+                                                        out->as<float>());
+    SSLIC_CUDA_CHECK(cudaGetLastError());
+    *narrowed_dtype = dt;
+    return out;  // (the fp64 copy is released in stream order)
+  }
   if (img->dtype == SSLIC_F32 || img->dtype == SSLIC_F64) {
     DeviceBuf cnt(sizeof(unsigned long long), st.s);
     SSLIC_CUDA_CHECK(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), st.s));
@@ -714,16 +774,18 @@ int sslic_run_slic(const sslic_image* img, const sslic_params* params, int devic
     // pipelined upload (u8/u16 volumes: no image-wide pre-pass before init)
     const size_t img_bytes = (size_t)n * img->channels * dtype_size(img->dtype);
     std::unique_ptr<DeviceBuf> dimg;
+    int dtype_dev = img->dtype;
     bool pipelined = false;
     if (overlapped && img->rank == 3 && (img->dtype == SSLIC_U8 || img->dtype == SSLIC_U16) &&
         std::getenv("SSLIC_NO_PIPELINED_UPLOAD") == nullptr) {
       dimg = std::make_unique<DeviceBuf>(img_bytes, st.s);
       pipelined = true;
     } else {
-      dimg = upload_image(img, st);
+      dimg = upload_image(img, st, &dtype_dev);  // (fp64 storage of narrower data: narrowed)
       pt.mark(st, "upload");
     }
-    const sslic_image v = device_view(img, dimg->p);
+    sslic_image v = device_view(img, dimg->p);
+    v.dtype = dtype_dev;
     Engine e(v, *params, device, 0, last, 0, last, st.s);
     if (pipelined && !(e.pipeline_ok() && !e.dist_mode() && e.max_iterations() >= 4)) {
       SSLIC_CUDA_CHECK(
@@ -762,8 +824,10 @@ int sslic_segment(const sslic_image* img, const sslic_params* params, int device
     validate_params(params, img);
     Stream st(device);
     PhaseTimer pt("segment");
-    auto dimg = upload_image(img, st);
-    const sslic_image v = device_view(img, dimg->p);
+    int dtype_dev = img->dtype;
+    auto dimg = upload_image(img, st, &dtype_dev);
+    sslic_image v = device_view(img, dimg->p);
+    v.dtype = dtype_dev;
     const int64_t last = img->dims[img->rank - 1];
     Engine e(v, *params, device, 0, last, 0, last, st.s);
     const int done = run_loop(e, params, st);
@@ -800,8 +864,10 @@ int sslic_segment_write(const sslic_image* img, const sslic_params* params, int 
     if (!labels_path) throw Error(SSLIC_EINVAL, "segment_write: null labels path");
     Stream st(device);
     PhaseTimer pt("segment_write");
-    auto dimg = upload_image(img, st);
-    const sslic_image v = device_view(img, dimg->p);
+    int dtype_dev = img->dtype;
+    auto dimg = upload_image(img, st, &dtype_dev);
+    sslic_image v = device_view(img, dimg->p);
+    v.dtype = dtype_dev;
     const int64_t last = img->dims[img->rank - 1];
     Engine e(v, *params, device, 0, last, 0, last, st.s);
     const int done = run_loop(e, params, st);

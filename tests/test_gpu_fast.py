@@ -647,3 +647,33 @@ def test_striped_pageable_copies_equal_plain_copies(sslic, monkeypatch):
     monkeypatch.setenv("SSLIC_NO_STRIPED_COPY", "1")
     l2, c2, n2 = run()
     assert n1 == n2 and np.array_equal(l1, l2) and np.array_equal(c1, c2)
+
+
+@pytest.mark.parametrize("dtype,ch", [(np.uint8, 3), (np.uint16, 1), (np.float32, 2)])
+def test_fp64_storage_of_narrower_data_is_narrowed_on_the_device(sslic, dtype, ch, monkeypatch):
+    """The reference's NDImage stores doubles whatever the data is
+    (image.hpp:236-285). An fp64 image whose values are all uint8 / uint16 /
+    float32 numbers is narrowed losslessly on the device and must give the
+    native-dtype run bit for bit -- and the same as the fp64 kernels
+    (SSLIC_NO_NARROW), which compute in the reference's own storage type."""
+    s = sslic
+    rng = np.random.default_rng(77)
+    dims, grid = (96, 80, 40), [8, 8, 8]
+    n = int(np.prod(dims)) * ch
+    if dtype == np.float32:
+        native = rng.random(n, dtype=np.float32)
+    else:
+        native = rng.integers(0, np.iinfo(dtype).max, n, endpoint=True).astype(dtype)
+    p = s.SlicParams(grid=grid, weight_m=10.0, max_iterations=4)
+    a = s.run_slic(s.NDImage(dims, ch, native), p)
+    b = s.run_slic(s.NDImage(dims, ch, native.astype(np.float64)), p)
+    assert np.array_equal(a.labels, b.labels)
+    assert np.array_equal(a.centers.data, b.centers.data)
+    assert np.array_equal(a.residuals, b.residuals)
+    monkeypatch.setenv("SSLIC_NO_NARROW", "1")
+    c = s.run_slic(s.NDImage(dims, ch, native.astype(np.float64)), p)
+    assert np.array_equal(a.labels, c.labels)
+    if dtype != np.float32:  # (float sums: fixed-point scale differs between the paths)
+        assert np.array_equal(a.centers.data, c.centers.data)
+    else:
+        assert np.allclose(a.centers.data, c.centers.data, rtol=1e-12, atol=0)
