@@ -79,7 +79,13 @@ int sslic_iterations_for(const sslic_params* p, int rank); /* SlicParams::iterat
 
 /* run_slic (slic.hpp:384-415). img->data is HOST memory. Outputs (host):
  *   labels_out[N] (uint32), centers_out[k*(c+rank)], residuals_out[iterations],
- *   *iterations_done. The reference's `workers` maps to nothing: one device. */
+ *   *iterations_done. The reference's `workers` maps to nothing: one device.
+ * Host buffers may be pageable or pinned: large pageable buffers travel in
+ * stripes over host threads and pinned staging (csrc/hostcopy.cu); pinned,
+ * device-mapped label buffers of >= 2^24 voxels get the overlapped download.
+ * An SSLIC_F64 image whose values are all uint8 / uint16 / float32 numbers (the
+ * reference's NDImage stores doubles, image.hpp:236-285) is narrowed
+ * losslessly on the device and runs the native-dtype kernels. */
 int sslic_run_slic(const sslic_image* img, const sslic_params* params, int device,
                    uint32_t* labels_out, double* centers_out, double* residuals_out,
                    int* iterations_done);

@@ -16,7 +16,9 @@
 // (std::invalid_argument / std::logic_error / std::out_of_range), CUDA
 // failures as std::runtime_error. The fp64 NDImage is narrowed losslessly to
 // uint8 / uint16 / float32 when every value is representable (so the fast
-// fp32-filter kernel applies); otherwise it is passed as fp64.
+// fp32-filter kernel applies); otherwise it is passed as fp64. run_slic hands
+// the NDImage's storage to the library, which narrows on the device; the
+// small helpers (perturb_centers, assign_labels, ...) narrow on the host.
 #pragma once
 
 #include <cstdint>
