@@ -1217,14 +1217,12 @@ int sslic_enforce_connectivity(int rank, const int64_t* dims, const uint32_t* la
     const int64_t n = acc;
     // relabelled in place on the device (4 bytes per voxel + the node ids)
     DeviceBuf din(n * sizeof(uint32_t), st.s), dc(k * g.stride * sizeof(double), st.s);
-    SSLIC_CUDA_CHECK(cudaMemcpyAsync(din.p, labels_in, n * sizeof(uint32_t),
-                                     cudaMemcpyHostToDevice, st.s));
+    copy_to_device(din.p, labels_in, n * sizeof(uint32_t), device, st.s);  // (pageable: striped)
     SSLIC_CUDA_CHECK(cudaMemcpyAsync(dc.p, centers, k * g.stride * sizeof(double),
                                      cudaMemcpyHostToDevice, st.s));
     const uint32_t next = enforce_connectivity_device(g, din.as<uint32_t>(), dc.as<double>(),
                                                       din.as<uint32_t>(), st.s);
-    SSLIC_CUDA_CHECK(cudaMemcpyAsync(labels_out, din.p, n * sizeof(uint32_t),
-                                     cudaMemcpyDeviceToHost, st.s));
+    copy_to_host(labels_out, din.p, n * sizeof(uint32_t), device, st.s);
     st.sync();
     if (next_label_out) *next_label_out = next;
     return SSLIC_OK;
