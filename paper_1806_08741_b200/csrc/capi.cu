@@ -976,8 +976,7 @@ int sslic_convert_image_to_lab(const sslic_image* img, int device, double* lab_o
     sslic_b200::srgb_to_lab_device(dimg->p, img->dtype, npix, dt.as<double>(),
                                    dout.as<double>(), st.s);
     SSLIC_CUDA_CHECK(cudaGetLastError());
-    SSLIC_CUDA_CHECK(cudaMemcpyAsync(lab_out, dout.p, npix * 3 * sizeof(double),
-                                     cudaMemcpyDeviceToHost, st.s));
+    copy_to_host(lab_out, dout.p, npix * 3 * sizeof(double), device, st.s);
     st.sync();
     return SSLIC_OK;
   });
@@ -1004,13 +1003,11 @@ int sslic_mask_label_contour(const sslic_image* img, int label_rank, const int64
       acc *= g.dims[a];
     }
     DeviceBuf dl(n * sizeof(uint32_t), st.s), dout(n * img->channels * sizeof(double), st.s);
-    SSLIC_CUDA_CHECK(cudaMemcpyAsync(dl.p, labels, n * sizeof(uint32_t), cudaMemcpyHostToDevice,
-                                     st.s));
+    copy_to_device(dl.p, labels, n * sizeof(uint32_t), device, st.s);
     sslic_b200::mask_label_contour_device(g, dimg->p, dl.as<uint32_t>(),
                                           dout.as<double>(), st.s);
     SSLIC_CUDA_CHECK(cudaGetLastError());
-    SSLIC_CUDA_CHECK(cudaMemcpyAsync(out, dout.p, n * img->channels * sizeof(double),
-                                     cudaMemcpyDeviceToHost, st.s));
+    copy_to_host(out, dout.p, n * img->channels * sizeof(double), device, st.s);
     st.sync();
     return SSLIC_OK;
   });
@@ -1031,15 +1028,13 @@ int sslic_gradient_sq(const sslic_image* img, const int64_t* coords, int64_t n, 
     const int64_t last = img->dims[img->rank - 1];
     Engine e(v, p, device, 0, last, 0, last, st.s, true);
     DeviceBuf dc(n * img->rank * sizeof(int64_t), st.s), dout(n * sizeof(double), st.s);
-    SSLIC_CUDA_CHECK(cudaMemcpyAsync(dc.p, coords, n * img->rank * sizeof(int64_t),
-                                     cudaMemcpyHostToDevice, st.s));
+    copy_to_device(dc.p, coords, n * img->rank * sizeof(int64_t), device, st.s);
     if (n > 0) {
       k_gradient_points<<<(unsigned)((n + 127) / 128), 128, 0, st.s>>>(
           e.geom(), dimg->p, dc.as<int64_t>(), n, dout.as<double>());
       SSLIC_CUDA_CHECK(cudaGetLastError());
     }
-    SSLIC_CUDA_CHECK(cudaMemcpyAsync(out, dout.p, n * sizeof(double), cudaMemcpyDeviceToHost,
-                                     st.s));
+    copy_to_host(out, dout.p, n * sizeof(double), device, st.s);
     st.sync();
     return SSLIC_OK;
   });
@@ -1060,19 +1055,15 @@ int sslic_squared_distance(int channels, int rank, const int64_t* grid, double w
     g.m_sq = weight_m * weight_m;
     DeviceBuf dc(n * g.stride * sizeof(double), st.s), dp(n * channels * sizeof(double), st.s),
         dx(n * rank * sizeof(int64_t), st.s), dout(n * sizeof(double), st.s);
-    SSLIC_CUDA_CHECK(cudaMemcpyAsync(dc.p, centers, n * g.stride * sizeof(double),
-                                     cudaMemcpyHostToDevice, st.s));
-    SSLIC_CUDA_CHECK(cudaMemcpyAsync(dp.p, pixels, n * channels * sizeof(double),
-                                     cudaMemcpyHostToDevice, st.s));
-    SSLIC_CUDA_CHECK(cudaMemcpyAsync(dx.p, coords, n * rank * sizeof(int64_t),
-                                     cudaMemcpyHostToDevice, st.s));
+    copy_to_device(dc.p, centers, n * g.stride * sizeof(double), device, st.s);
+    copy_to_device(dp.p, pixels, n * channels * sizeof(double), device, st.s);
+    copy_to_device(dx.p, coords, n * rank * sizeof(int64_t), device, st.s);
     if (n > 0) {
       k_distance_points<<<(unsigned)((n + 127) / 128), 128, 0, st.s>>>(
           g, n, dc.as<double>(), dp.as<double>(), dx.as<int64_t>(), dout.as<double>());
       SSLIC_CUDA_CHECK(cudaGetLastError());
     }
-    SSLIC_CUDA_CHECK(cudaMemcpyAsync(out, dout.p, n * sizeof(double), cudaMemcpyDeviceToHost,
-                                     st.s));
+    copy_to_host(out, dout.p, n * sizeof(double), device, st.s);
     st.sync();
     return SSLIC_OK;
   });
@@ -1096,15 +1087,11 @@ int sslic_assign_pass(const sslic_image* img, const sslic_params* params, const 
     e.set_centers_host(centers);
     e.commit();
     const int64_t n = pixel_count(*img);
-    SSLIC_CUDA_CHECK(cudaMemcpyAsync(e.label_words(), labels, n * sizeof(uint32_t),
-                                     cudaMemcpyHostToDevice, st.s));
-    SSLIC_CUDA_CHECK(cudaMemcpyAsync(e.dists(), dists, n * sizeof(double),
-                                     cudaMemcpyHostToDevice, st.s));
+    copy_to_device(e.label_words(), labels, n * sizeof(uint32_t), device, st.s);
+    copy_to_device(e.dists(), dists, n * sizeof(double), device, st.s);
     e.assign(false);
-    SSLIC_CUDA_CHECK(cudaMemcpyAsync(labels, e.label_words(), n * sizeof(uint32_t),
-                                     cudaMemcpyDeviceToHost, st.s));
-    SSLIC_CUDA_CHECK(cudaMemcpyAsync(dists, e.dists(), n * sizeof(double),
-                                     cudaMemcpyDeviceToHost, st.s));
+    copy_to_host(labels, e.label_words(), n * sizeof(uint32_t), device, st.s);
+    copy_to_host(dists, e.dists(), n * sizeof(double), device, st.s);
     st.sync();
     return SSLIC_OK;
   });
@@ -1129,8 +1116,7 @@ int sslic_accumulate(const sslic_image* img, const uint32_t* labels, int64_t k, 
     const int64_t n = pixel_count(*img);
     DeviceBuf acc((k * (g.stride + 1) + 2) * sizeof(unsigned long long), st.s);
     DeviceBuf dl(n * sizeof(uint32_t), st.s);
-    SSLIC_CUDA_CHECK(cudaMemcpyAsync(dl.p, labels, n * sizeof(uint32_t), cudaMemcpyHostToDevice,
-                                     st.s));
+    copy_to_device(dl.p, labels, n * sizeof(uint32_t), device, st.s);
     SSLIC_CUDA_CHECK(cudaMemsetAsync(acc.p, 0, (k * (g.stride + 1) + 2) * sizeof(unsigned long long),
                                      st.s));
     unsigned long long* a = acc.as<unsigned long long>();
