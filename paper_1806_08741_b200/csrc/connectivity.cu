@@ -150,6 +150,124 @@ __global__ void k_cc_union(CG<uint32_t> g, const uint32_t* labels, uint32_t* par
   }
 }
 
+// ---- tiled CCL for ranks 1-3 (the whole-slab k_cc_union above stays for rank 4)
+// A CTA labels one 32x8x8 tile in shared memory (runs along x by ballot, then
+// shared-memory atomicMin hooking along y and z) and writes each voxel's tile
+// root as a slab offset; k_cc_seams then unites equal labels across the tile
+// faces in global memory. A union is skipped when the pair one step back along
+// another in-tile axis carries the same label on both sides: that pair (or,
+// by induction, one further back) makes the same connection. Hooking always
+// points the larger root at the smaller one and a tile's local order is the
+// raster order, so a component's root is its smallest offset, as before.
+constexpr uint32_t kTX = 32, kTY = 8, kTZ = 8, kTileVox = kTX * kTY * kTZ;
+
+__device__ __forceinline__ void unite_tile(uint32_t* par, uint32_t a, uint32_t b) {
+  for (;;) {
+    uint32_t p = par[a];
+    while (p != a) {
+      a = p;
+      p = par[a];
+    }
+    p = par[b];
+    while (p != b) {
+      b = p;
+      p = par[b];
+    }
+    if (a == b) return;
+    if (a < b) {
+      const uint32_t t = a;
+      a = b;
+      b = t;
+    }
+    const uint32_t old = atomicMin(par + a, b);
+    if (old == a) return;
+    a = old;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_cc_tile(uint32_t X, uint32_t Y, uint32_t Z, uint32_t ntx,
+                                                 uint32_t nty, const uint32_t* __restrict__ labels,
+                                                 uint32_t* __restrict__ parent) {
+  __shared__ uint32_t lab[kTileVox];
+  __shared__ uint32_t par[kTileVox];
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t t = blockIdx.x;
+  const uint32_t tx = t % ntx;
+  t /= ntx;
+  const uint32_t ty = t % nty, tz = t / nty;
+  const uint32_t x0 = tx * kTX, y0 = ty * kTY, z0 = tz * kTZ;
+  const uint32_t x = x0 + lane, y = y0 + w;
+  const bool vxy = x < X && y < Y;
+  const uint32_t nz = min(kTZ, Z - z0);
+  const uint32_t pbase = x + X * (y + Y * z0), zs = X * Y;
+  const uint32_t li0 = lane + kTX * w;
+  // labels into shared memory; parents start at the head of the voxel's x-run
+#pragma unroll
+  for (uint32_t z = 0; z < kTZ; ++z) {
+    const bool v = vxy && z < nz;
+    const uint32_t l = v ? labels[pbase + z * zs] : 0u;
+    const uint32_t left = __shfl_up_sync(0xffffffffu, l, 1);
+    const unsigned same = __ballot_sync(0xffffffffu, v && lane > 0 && l == left);
+    const unsigned heads = ~same & ((2u << lane) - 1u);  // bit 0 is always a head
+    const uint32_t li = li0 + kTX * kTY * z;
+    lab[li] = l;
+    par[li] = li - lane + (31u - (uint32_t)__clz(heads));
+  }
+  __syncthreads();
+  if (vxy) {
+#pragma unroll
+    for (uint32_t z = 0; z < kTZ; ++z) {
+      if (z >= nz) break;
+      const uint32_t li = li0 + kTX * kTY * z, l = lab[li];
+      const bool back = lane > 0 && lab[li - 1] == l;
+      if (w + 1 < kTY && y + 1 < Y) {
+        const uint32_t lj = li + kTX;
+        if (lab[lj] == l && !(back && lab[lj - 1] == l)) unite_tile(par, li, lj);
+      }
+      if (z + 1 < nz) {
+        const uint32_t lj = li + kTX * kTY;
+        if (lab[lj] == l && !(back && lab[lj - 1] == l)) unite_tile(par, li, lj);
+      }
+    }
+  }
+  __syncthreads();
+  if (vxy) {
+#pragma unroll
+    for (uint32_t z = 0; z < kTZ; ++z) {
+      if (z >= nz) break;
+      uint32_t r = li0 + kTX * kTY * z, p = par[r];
+      while (p != r) {
+        r = p;
+        p = par[r];
+      }
+      parent[pbase + z * zs] =
+          (x0 + (r & (kTX - 1))) + X * ((y0 + ((r / kTX) & (kTY - 1))) + Y * (z0 + r / (kTX * kTY)));
+    }
+  }
+}
+
+// unions across the tile faces (the voxels with x % 32 == 31, y % 8 == 7 or
+// z % 8 == 7 and their +1 neighbours)
+__global__ void k_cc_seams(uint32_t X, uint32_t Y, uint32_t Z, const uint32_t* __restrict__ labels,
+                           uint32_t* parent) {
+  const uint32_t n = X * Y * Z, zs = X * Y;
+  GRID_STRIDE(uint32_t, p, n) {
+    const uint32_t z = p / zs, i = p - z * zs, y = i / X, x = i - y * X;
+    const bool fx = (x & (kTX - 1)) == kTX - 1 && x + 1 < X;
+    const bool fy = (y & (kTY - 1)) == kTY - 1 && y + 1 < Y;
+    const bool fz = (z & (kTZ - 1)) == kTZ - 1 && z + 1 < Z;
+    if (!(fx | fy | fz)) continue;
+    const uint32_t l = labels[p];
+    const bool backx = (x & (kTX - 1)) != 0 && labels[p - 1] == l;
+    if (fx && labels[p + 1] == l) {
+      const bool backy = (y & (kTY - 1)) != 0 && labels[p - X] == l && labels[p + 1 - X] == l;
+      if (!backy) unite(parent, p, p + 1);
+    }
+    if (fy && labels[p + X] == l && !(backx && labels[p + X - 1] == l)) unite(parent, p, p + X);
+    if (fz && labels[p + zs] == l && !(backx && labels[p + zs - 1] == l)) unite(parent, p, p + zs);
+  }
+}
+
 // parent -> root; idx[p] = 1 for roots (scanned into dense node ids)
 __global__ void k_cc_flatten(uint32_t* parent, uint32_t* idx, uint32_t n) {
   GRID_STRIDE(uint32_t, i, n) {
@@ -486,6 +604,24 @@ __global__ void k_jump(uint32_t m, uint32_t* T, unsigned* changed) {
 // One pass over the face edges: extension candidates (te_new) and absorbed
 // components (against the previous round's te).
 template <class Off>
+__device__ __forceinline__ void edge_body(const CG<Off>& g, Off p, uint32_t d, uint32_t l,
+                                          uint32_t f, const uint32_t* nid, const uint8_t* flags,
+                                          const uint32_t* T, const uint32_t* te, uint32_t* te_new,
+                                          uint8_t* absn) {
+  const uint32_t t0 = te[l];
+  bool cand = false, ab = false;
+  for_neighbours(g, p, [&](Off q) {
+    const uint32_t x = nid[q];
+    if (x == d || T[x] != f) return;
+    const bool proc = flags[x] & kProc;
+    if (x < d || proc) cand = true;
+    if (t0 != kNone && d > t0 && (x < t0 || proc)) ab = true;
+  });
+  if (cand) atomicMin(te_new + l, d);
+  if (ab) absn[d] = 1;
+}
+
+template <class Off>
 __global__ void k_edges(CG<Off> g, const uint32_t* nid, const uint8_t* flags,
                         const uint32_t* nlab, const uint32_t* fcomp, const uint8_t* factive,
                         const uint32_t* T, const uint32_t* te, uint32_t* te_new, uint8_t* absn) {
@@ -496,17 +632,50 @@ __global__ void k_edges(CG<Off> g, const uint32_t* nid, const uint8_t* flags,
     if (!factive[l]) continue;
     const uint32_t f = fcomp[l];
     if (f == kNone) continue;
-    const uint32_t t0 = te[l];
-    bool cand = false, ab = false;
-    for_neighbours(g, p, [&](Off q) {
-      const uint32_t x = nid[q];
-      if (x == d || T[x] != f) return;
-      const bool proc = flags[x] & kProc;
-      if (x < d || proc) cand = true;
-      if (t0 != kNone && d > t0 && (x < t0 || proc)) ab = true;
-    });
-    if (cand) atomicMin(te_new + l, d);
-    if (ab) absn[d] = 1;
+    edge_body(g, p, d, l, f, nid, flags, T, te, te_new, absn);
+  }
+}
+
+// The voxels k_edges does not skip (components that are neither final nor
+// decided by the prefix, of a label with an active finalized component) are
+// the same in every round: they are listed once (any order: k_edges only
+// takes minima and sets flags) and the rounds walk the list. *count may pass
+// cap; the caller then keeps the whole-map pass.
+template <class Off>
+__global__ void k_active_list(Off n, const uint32_t* nid, const uint8_t* flags,
+                              const uint32_t* nlab, const uint32_t* fcomp, const uint8_t* factive,
+                              Off* list, unsigned long long cap, unsigned long long* count) {
+  const unsigned lane = threadIdx.x & 31;
+  const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t base = ((uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32;
+       base < (uint64_t)n; base += warps * 32) {
+    const uint64_t p = base + lane;
+    bool act = false;
+    if (p < (uint64_t)n) {
+      const uint32_t d = nid[p];
+      if (!(flags[d] & (kFin | kProc))) {
+        const uint32_t l = nlab[d];
+        act = factive[l] && fcomp[l] != kNone;
+      }
+    }
+    const unsigned am = __ballot_sync(0xffffffffu, act);
+    if (am == 0) continue;
+    unsigned long long pos = 0;
+    if (lane == 0) pos = atomicAdd(count, (unsigned long long)__popc(am));
+    pos = __shfl_sync(0xffffffffu, pos, 0) + __popc(am & ((1u << lane) - 1u));
+    if (act && pos < cap) list[pos] = (Off)p;
+  }
+}
+
+template <class Off>
+__global__ void k_edges_list(CG<Off> g, const Off* list, unsigned long long count,
+                             const uint32_t* nid, const uint8_t* flags, const uint32_t* nlab,
+                             const uint32_t* fcomp, const uint32_t* T, const uint32_t* te,
+                             uint32_t* te_new, uint8_t* absn) {
+  GRID_STRIDE(uint64_t, i, count) {
+    const Off p = list[i];
+    const uint32_t d = nid[p], l = nlab[d];
+    edge_body(g, p, d, l, fcomp[l], nid, flags, T, te, te_new, absn);
   }
 }
 
@@ -629,8 +798,20 @@ __global__ void k_label_outputs(CG<Off> g, const uint32_t* labels, unsigned* max
 struct Scratch {
   void* p = nullptr;
   cudaStream_t s;
+  Scratch() : s(nullptr) {}
   Scratch(size_t bytes, cudaStream_t st) : s(st) {
     SSLIC_CUDA_CHECK(cudaMallocAsync(&p, bytes ? bytes : 1, st));
+  }
+  // optional buffers: false (and no sticky error) when the memory is not there
+  bool try_alloc(size_t bytes, cudaStream_t st) {
+    release();
+    s = st;
+    if (cudaMallocAsync(&p, bytes ? bytes : 1, st) != cudaSuccess) {
+      p = nullptr;
+      (void)cudaGetLastError();
+      return false;
+    }
+    return true;
   }
   ~Scratch() { release(); }
   void release() {
@@ -709,9 +890,10 @@ uint32_t connectivity_impl(const Geom& g, const uint32_t* labels_in, const doubl
   Scratch ctl(8 * sizeof(unsigned), s);
   unsigned* c = ctl.as<unsigned>();
   SSLIC_CUDA_CHECK(cudaMemsetAsync(c, 0, 8 * sizeof(unsigned), s));
-  Scratch ull(4 * sizeof(unsigned long long), s);  // [0] best_after of node 0, [1..3] serial
+  // [0] best_after of node 0, [1..3] serial, [4] listed edge-pass voxels
+  Scratch ull(5 * sizeof(unsigned long long), s);
   unsigned long long* cu = ull.as<unsigned long long>();
-  SSLIC_CUDA_CHECK(cudaMemsetAsync(cu, 0, 4 * sizeof(unsigned long long), s));
+  SSLIC_CUDA_CHECK(cudaMemsetAsync(cu, 0, 5 * sizeof(unsigned long long), s));
   SSLIC_CUDA_CHECK(cudaMemsetAsync(cu, 0xff, sizeof(unsigned long long), s));
   k_max_label<Off><<<148 * 8, 256, 0, s>>>(labels_in, n, c + 0);
 
@@ -725,13 +907,24 @@ uint32_t connectivity_impl(const Geom& g, const uint32_t* labels_in, const doubl
   size_t tmp_bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, idx, idx, slab_max + 1, s);
   std::vector<uint32_t> slab_m(nslabs);
-  auto slab_ccl = [&](int si) {  // -> nid[slab] = local roots, idx = scanned root flags
+  // tiled shared-memory CCL for ranks 1-3 with rows of at least half a tile
+  // (SSLIC_CC_NO_TILES=1: the whole-slab union-find, kept for rank 4 and for
+  // the equality test)
+  const bool tiled = g.rank <= 3 && g.dims[0] >= 16 && std::getenv("SSLIC_CC_NO_TILES") == nullptr;
+  auto slab_ccl =[&](int si) {  // -> nid[slab] = local roots, idx = scanned root flags
     const int64_t z0 = si * sp, z1 = std::min(last, z0 + sp);
     const CG<uint32_t> sg = make_cg<uint32_t>(g, z0, z1);
     uint32_t* par = nid + z0 * plane;
     const uint32_t* lab = labels_in + z0 * plane;
-    k_cc_init<<<blocks(sg.n), 256, 0, s>>>(par, sg.n);
-    k_cc_union<<<blocks(sg.n), 256, 0, s>>>(sg, lab, par);
+    if (tiled) {
+      const uint32_t X = sg.dims[0], Y = g.rank > 1 ? sg.dims[1] : 1, Z = g.rank > 2 ? sg.dims[2] : 1;
+      const uint32_t ntx = (X + kTX - 1) / kTX, nty = (Y + kTY - 1) / kTY, ntz = (Z + kTZ - 1) / kTZ;
+      k_cc_tile<<<ntx * nty * ntz, 256, 0, s>>>(X, Y, Z, ntx, nty, lab, par);
+      k_cc_seams<<<blocks(sg.n), 256, 0, s>>>(X, Y, Z, lab, par);
+    } else {
+      k_cc_init<<<blocks(sg.n), 256, 0, s>>>(par, sg.n);
+      k_cc_union<<<blocks(sg.n), 256, 0, s>>>(sg, lab, par);
+    }
     k_cc_flatten<<<blocks(sg.n), 256, 0, s>>>(par, idx, sg.n);
     return sg.n;
   };
@@ -892,6 +1085,16 @@ uint32_t connectivity_impl(const Geom& g, const uint32_t* labels_in, const doubl
     }
   }
   int rounds = 0, jumps = 0;
+  // list of the edge pass's voxels: up to a quarter of the map and 2 GB
+  // (beyond that, or if the allocation fails, every round scans the map)
+  unsigned long long list_cap =
+      std::min<unsigned long long>((unsigned long long)n64 / 4 + 1, (2ull << 30) / sizeof(Off));
+  unsigned long long n_active = 0;
+  Scratch alist_b;
+  bool use_list = !done && list_cap >= (unsigned long long)n64 / 16 &&
+                  std::getenv("SSLIC_CC_NO_LIST") == nullptr &&
+                  alist_b.try_alloc((size_t)list_cap * sizeof(Off), s);
+  Off* alist = alist_b.as<Off>();
   if (!done) {
     for (;;) {
       ++rounds;
@@ -903,8 +1106,20 @@ uint32_t connectivity_impl(const Geom& g, const uint32_t* labels_in, const doubl
         SSLIC_CUDA_CHECK(cudaGetLastError());
         if (read_scalar(c + 2, s) == 0) break;
       }
-      k_edges<Off><<<blocks(n64), 256, 0, s>>>(cg, nid, flags, nlab, fcomp, factive, T, te,
-                                               te_new, absn);
+      if (rounds == 1 && use_list) {
+        // (first round: list the voxels the edge pass works on)
+        k_active_list<Off><<<blocks(n64), 256, 0, s>>>(n, nid, flags, nlab, fcomp, factive,
+                                                       alist, list_cap, cu + 4);
+        SSLIC_CUDA_CHECK(cudaGetLastError());
+        n_active = read_scalar(cu + 4, s);
+        if (n_active > list_cap) use_list = false;
+      }
+      if (use_list)
+        k_edges_list<Off><<<blocks((int64_t)n_active), 256, 0, s>>>(cg, alist, n_active, nid, flags,
+                                                                    nlab, fcomp, T, te, te_new, absn);
+      else
+        k_edges<Off><<<blocks(n64), 256, 0, s>>>(cg, nid, flags, nlab, fcomp, factive, T, te,
+                                                 te_new, absn);
       SSLIC_CUDA_CHECK(cudaMemsetAsync(c + 2, 0, sizeof(unsigned), s));
       k_swap_te<<<blocks(kk), 256, 0, s>>>(k, te, te_new, c + 2);
       k_swap_abs<<<blocks(m), 256, 0, s>>>(m, flags, absn, c + 2);

@@ -192,3 +192,30 @@ def test_slab_stitched_noisy_volume(sslic, oracle_lib):
     cen = res.centers.data.reshape(-1, 4)
     with _env(SSLIC_CC_SLAB_PLANES=15, SSLIC_CC_FORCE64=1):
         _check(sslic, oracle_lib, dims, res.labels, cen, 1, grid)
+
+
+@pytest.mark.parametrize("seed,dims,blob", [
+    (0, (70, 21, 19), 3), (1, (33, 9, 9), 2), (2, (64, 16, 16), 5), (3, (32, 8, 8), 1),
+    (4, (97, 40, 23), 9), (5, (16, 70, 33), 4), (6, (129, 37), 6), (7, (40, 300), 2),
+    (8, (5000,), 7), (9, (65, 17, 41), 30), (10, (200, 9, 17), 12), (11, (31, 64, 64), 8),
+])
+def test_tiled_ccl_and_edge_list_equal_whole_slab_union_find(sslic, oracle_lib, seed, dims, blob):
+    """The CCL labels 32x8x8 tiles in shared memory and unites the tile faces
+    afterwards (k_cc_tile / k_cc_seams), and the fixpoint rounds walk a list
+    of the voxels the edge pass works on (k_active_list / k_edges_list). On
+    volumes that cut tiles on every axis, with components from specks to
+    blobs spanning many tiles: equal to the oracle's raster sweep, and equal
+    to the whole-slab union-find with whole-map edge passes
+    (SSLIC_CC_NO_TILES, SSLIC_CC_NO_LIST), also with slabs and 64-bit offsets."""
+    rng = np.random.default_rng(9100 + seed)
+    k = int(rng.integers(2, 30))
+    grid = tuple(int(rng.integers(1, min(d, 6) + 1)) for d in dims)
+    lab = _random_field(rng, dims, k, blob)
+    cen = _random_centres(rng, dims, k, 1)
+    out = _check(sslic, oracle_lib, dims, lab, cen, 1, grid)
+    with _env(SSLIC_CC_NO_TILES=1, SSLIC_CC_NO_LIST=1):
+        plain = _check(sslic, oracle_lib, dims, lab, cen, 1, grid)
+    assert np.array_equal(out, plain)
+    with _env(SSLIC_CC_SLAB_PLANES=max(1, dims[-1] // 3), SSLIC_CC_FORCE64=1):
+        slabs = _check(sslic, oracle_lib, dims, lab, cen, 1, grid)
+    assert np.array_equal(out, slabs)
