@@ -636,46 +636,76 @@ __global__ void k_edges(CG<Off> g, const uint32_t* nid, const uint8_t* flags,
   }
 }
 
-// The voxels k_edges does not skip (components that are neither final nor
-// decided by the prefix, of a label with an active finalized component) are
-// the same in every round: they are listed once (any order: k_edges only
-// takes minima and sets flags) and the rounds walk the list. *count may pass
-// cap; the caller then keeps the whole-map pass.
+// The rounds' edge pass as a list. Only a neighbour component x that is not
+// final can satisfy T[x] == f for x != f (a final component's T is itself,
+// always), and the voxels the pass skips are the same in every round, so the
+// candidate edges (d, x, label of d | kProc(x) << 31) are listed once, in any
+// order (the pass only takes minima and sets flags), and every round walks
+// the list with ONE gather (T[x]) per edge instead of the node ids and flags
+// of six neighbours per voxel. *count may pass cap; the caller then keeps the
+// whole-map pass.
 template <class Off>
-__global__ void k_active_list(Off n, const uint32_t* nid, const uint8_t* flags,
-                              const uint32_t* nlab, const uint32_t* fcomp, const uint8_t* factive,
-                              Off* list, unsigned long long cap, unsigned long long* count) {
+__global__ void k_edge_list(CG<Off> g, const uint32_t* nid, const uint8_t* flags,
+                            const uint32_t* nlab, const uint32_t* fcomp, const uint8_t* factive,
+                            uint32_t* ed, uint32_t* ex, uint32_t* el, unsigned long long cap,
+                            unsigned long long* count) {
   const unsigned lane = threadIdx.x & 31;
   const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
   for (uint64_t base = ((uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32;
-       base < (uint64_t)n; base += warps * 32) {
+       base < (uint64_t)g.n; base += warps * 32) {
     const uint64_t p = base + lane;
     bool act = false;
-    if (p < (uint64_t)n) {
-      const uint32_t d = nid[p];
+    uint32_t d = 0, l = 0, f = 0;
+    if (p < (uint64_t)g.n) {
+      d = nid[p];
       if (!(flags[d] & (kFin | kProc))) {
-        const uint32_t l = nlab[d];
-        act = factive[l] && fcomp[l] != kNone;
+        l = nlab[d];
+        f = fcomp[l];
+        act = factive[l] && f != kNone;
       }
     }
-    const unsigned am = __ballot_sync(0xffffffffu, act);
-    if (am == 0) continue;
+    if (!__any_sync(0xffffffffu, act)) continue;
+    unsigned cnt = 0;
+    if (act)
+      for_neighbours(g, (Off)p, [&](Off q) {
+        const uint32_t x = nid[q];
+        if (x != d && (!(flags[x] & kFin) || x == f)) ++cnt;
+      });
+    unsigned incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= (unsigned)o) incl += v;
+    }
+    const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
+    if (total == 0) continue;
     unsigned long long pos = 0;
-    if (lane == 0) pos = atomicAdd(count, (unsigned long long)__popc(am));
-    pos = __shfl_sync(0xffffffffu, pos, 0) + __popc(am & ((1u << lane) - 1u));
-    if (act && pos < cap) list[pos] = (Off)p;
+    if (lane == 0) pos = atomicAdd(count, (unsigned long long)total);
+    pos = __shfl_sync(0xffffffffu, pos, 0) + (incl - cnt);
+    if (cnt && pos + cnt <= cap)
+      for_neighbours(g, (Off)p, [&](Off q) {
+        const uint32_t x = nid[q];
+        const uint8_t fx = flags[x];
+        if (x != d && (!(fx & kFin) || x == f)) {
+          ed[pos] = d;
+          ex[pos] = x;
+          el[pos] = l | (fx & kProc ? 0x80000000u : 0u);
+          ++pos;
+        }
+      });
   }
 }
 
-template <class Off>
-__global__ void k_edges_list(CG<Off> g, const Off* list, unsigned long long count,
-                             const uint32_t* nid, const uint8_t* flags, const uint32_t* nlab,
-                             const uint32_t* fcomp, const uint32_t* T, const uint32_t* te,
-                             uint32_t* te_new, uint8_t* absn) {
+__global__ void k_edges_list(const uint32_t* ed, const uint32_t* ex, const uint32_t* el,
+                             unsigned long long count, const uint32_t* fcomp, const uint32_t* T,
+                             const uint32_t* te, uint32_t* te_new, uint8_t* absn) {
   GRID_STRIDE(uint64_t, i, count) {
-    const Off p = list[i];
-    const uint32_t d = nid[p], l = nlab[d];
-    edge_body(g, p, d, l, fcomp[l], nid, flags, T, te, te_new, absn);
+    const uint32_t x = ex[i], lp = el[i], l = lp & 0x7fffffffu;
+    if (T[x] != fcomp[l]) continue;
+    const uint32_t d = ed[i], t0 = te[l];
+    const bool proc = lp >> 31;
+    if (x < d || proc) atomicMin(te_new + l, d);
+    if (t0 != kNone && d > t0 && (x < t0 || proc)) absn[d] = 1;
   }
 }
 
@@ -1085,16 +1115,24 @@ uint32_t connectivity_impl(const Geom& g, const uint32_t* labels_in, const doubl
     }
   }
   int rounds = 0, jumps = 0;
-  // list of the edge pass's voxels: up to a quarter of the map and 2 GB
-  // (beyond that, or if the allocation fails, every round scans the map)
-  unsigned long long list_cap =
-      std::min<unsigned long long>((unsigned long long)n64 / 4 + 1, (2ull << 30) / sizeof(Off));
-  unsigned long long n_active = 0;
-  Scratch alist_b;
-  bool use_list = !done && list_cap >= (unsigned long long)n64 / 16 &&
+  // list of the edge pass's candidate edges (12 bytes each): room for one per
+  // voxel if the device has it free (beyond a 4 GB reserve for what follows);
+  // with room for fewer than one per 16 voxels, or labels >= 2^31, every
+  // round scans the map
+  size_t mem_free = 0, mem_total = 0;
+  SSLIC_CUDA_CHECK(cudaStreamSynchronize(s));  // (the pool returns what was freed so far)
+  if (cudaMemGetInfo(&mem_free, &mem_total) != cudaSuccess) mem_free = 0;
+  const unsigned long long reserve = 4ull << 30;
+  const unsigned long long list_cap = std::min<unsigned long long>(
+      (unsigned long long)n64 + 64, mem_free > reserve ? (mem_free - reserve) / 12 : 0);
+  unsigned long long n_edges = 0;
+  Scratch elist_b;
+  bool use_list = !done && list_cap >= (unsigned long long)n64 / 16 && k < 0x80000000u &&
                   std::getenv("SSLIC_CC_NO_LIST") == nullptr &&
-                  alist_b.try_alloc((size_t)list_cap * sizeof(Off), s);
-  Off* alist = alist_b.as<Off>();
+                  elist_b.try_alloc((size_t)list_cap * 12, s);
+  uint32_t* ed = elist_b.as<uint32_t>();
+  uint32_t* ex = ed + list_cap;
+  uint32_t* el = ex + list_cap;
   if (!done) {
     for (;;) {
       ++rounds;
@@ -1107,16 +1145,16 @@ uint32_t connectivity_impl(const Geom& g, const uint32_t* labels_in, const doubl
         if (read_scalar(c + 2, s) == 0) break;
       }
       if (rounds == 1 && use_list) {
-        // (first round: list the voxels the edge pass works on)
-        k_active_list<Off><<<blocks(n64), 256, 0, s>>>(n, nid, flags, nlab, fcomp, factive,
-                                                       alist, list_cap, cu + 4);
+        // (first round: list the candidate edges)
+        k_edge_list<Off><<<blocks(n64), 256, 0, s>>>(cg, nid, flags, nlab, fcomp, factive, ed, ex,
+                                                     el, list_cap, cu + 4);
         SSLIC_CUDA_CHECK(cudaGetLastError());
-        n_active = read_scalar(cu + 4, s);
-        if (n_active > list_cap) use_list = false;
+        n_edges = read_scalar(cu + 4, s);
+        if (n_edges > list_cap) use_list = false;
       }
       if (use_list)
-        k_edges_list<Off><<<blocks((int64_t)n_active), 256, 0, s>>>(cg, alist, n_active, nid, flags,
-                                                                    nlab, fcomp, T, te, te_new, absn);
+        k_edges_list<<<blocks((int64_t)n_edges), 256, 0, s>>>(ed, ex, el, n_edges, fcomp, T, te,
+                                                              te_new, absn);
       else
         k_edges<Off><<<blocks(n64), 256, 0, s>>>(cg, nid, flags, nlab, fcomp, factive, T, te,
                                                  te_new, absn);
@@ -1154,10 +1192,11 @@ uint32_t connectivity_impl(const Geom& g, const uint32_t* labels_in, const doubl
     const auto t1 = std::chrono::steady_clock::now();
     std::fprintf(stderr,
                  "[sslic] connectivity: %lld voxels, %u components, %d CCL slab(s), %s, %d "
-                 "rounds, %d jump passes, %.2f ms\n",
+                 "rounds (%s, %llu edges), %d jump passes, %.2f ms\n",
                  (long long)n64, m, nslabs,
                  full_serial ? "serial (ids >= k)" : (serial ? "serial prefix" : "no prefix"),
-                 rounds, jumps, std::chrono::duration<double, std::milli>(t1 - t0).count());
+                 rounds, use_list ? "edge list" : "map scans", n_edges, jumps,
+                 std::chrono::duration<double, std::milli>(t1 - t0).count());
   }
   return next;
 }
