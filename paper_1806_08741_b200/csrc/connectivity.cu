@@ -941,12 +941,15 @@ uint32_t connectivity_impl(const Geom& g, const uint32_t* labels_in, const doubl
   // (SSLIC_CC_NO_TILES=1: the whole-slab union-find, kept for rank 4 and for
   // the equality test)
   const bool tiled = g.rank <= 3 && g.dims[0] >= 16 && std::getenv("SSLIC_CC_NO_TILES") == nullptr;
-  auto slab_ccl =[&](int si) {  // -> nid[slab] = local roots, idx = scanned root flags
+  // -> nid[slab] = local roots, idx = root flags; `again`: the roots are
+  // still in nid from the first pass (only idx was reused), so just the flags
+  auto slab_ccl = [&](int si, bool again = false) {
     const int64_t z0 = si * sp, z1 = std::min(last, z0 + sp);
     const CG<uint32_t> sg = make_cg<uint32_t>(g, z0, z1);
     uint32_t* par = nid + z0 * plane;
     const uint32_t* lab = labels_in + z0 * plane;
-    if (tiled) {
+    if (again) {
+    } else if (tiled) {
       const uint32_t X = sg.dims[0], Y = g.rank > 1 ? sg.dims[1] : 1, Z = g.rank > 2 ? sg.dims[2] : 1;
       const uint32_t ntx = (X + kTX - 1) / kTX, nty = (Y + kTY - 1) / kTY, ntz = (Z + kTZ - 1) / kTZ;
       k_cc_tile<<<ntx * nty * ntz, 256, 0, s>>>(X, Y, Z, ntx, nty, lab, par);
@@ -984,8 +987,8 @@ uint32_t connectivity_impl(const Geom& g, const uint32_t* labels_in, const doubl
     for (int si = 0; si < nslabs; ++si) {
       const int64_t z0 = si * sp;
       uint32_t ns;
-      if (nslabs > 1) {  // the first pass's roots were overwritten by the next slab's scan
-        ns = slab_ccl(si);
+      if (nslabs > 1) {  // the first pass's root flags were overwritten by the next slab's
+        ns = slab_ccl(si, true);
         SSLIC_CUDA_CHECK(
             cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, idx, idx, (int64_t)ns + 1, s));
       } else {
