@@ -109,10 +109,24 @@ __device__ __forceinline__ uint32_t find_root(const uint32_t* parent, uint32_t i
   return i;
 }
 
+// find with path halving: a node that is not a root never becomes one again
+// and only ever points at an ancestor, so the plain store of the grandparent
+// is safe next to the hooking atomics (and keeps parent[i] <= i)
+__device__ __forceinline__ uint32_t find_root_halving(uint32_t* parent, uint32_t i) {
+  for (;;) {
+    const uint32_t p = parent[i];
+    if (p == i) return i;
+    const uint32_t gp = parent[p];
+    if (gp == p) return p;
+    parent[i] = gp;
+    i = gp;
+  }
+}
+
 __device__ __forceinline__ void unite(uint32_t* parent, uint32_t a, uint32_t b) {
   for (;;) {
-    a = find_root(parent, a);
-    b = find_root(parent, b);
+    a = find_root_halving(parent, a);
+    b = find_root_halving(parent, b);
     if (a == b) return;
     if (a < b) {
       const uint32_t t = a;
@@ -1118,22 +1132,30 @@ uint32_t connectivity_impl(const Geom& g, const uint32_t* labels_in, const doubl
     }
   }
   int rounds = 0, jumps = 0;
-  // list of the edge pass's candidate edges (12 bytes each): room for one per
-  // voxel if the device has it free (beyond a 4 GB reserve for what follows);
-  // with room for fewer than one per 16 voxels, or labels >= 2^31, every
-  // round scans the map
+  // List of the edge pass's candidate edges (12 bytes each). It lives in a
+  // buffer of its own when the device has room for one edge per voxel beyond
+  // a 4 GB reserve; otherwise in the OUTPUT map, which nothing reads between
+  // here and k_output (which rewrites all of it, also when it aliases the
+  // input): room for one edge per three voxels. If the edges outnumber the
+  // room (or labels need 32 bits), every round scans the map.
   size_t mem_free = 0, mem_total = 0;
   SSLIC_CUDA_CHECK(cudaStreamSynchronize(s));  // (the pool returns what was freed so far)
   if (cudaMemGetInfo(&mem_free, &mem_total) != cudaSuccess) mem_free = 0;
   const unsigned long long reserve = 4ull << 30;
-  const unsigned long long list_cap = std::min<unsigned long long>(
-      (unsigned long long)n64 + 64, mem_free > reserve ? (mem_free - reserve) / 12 : 0);
+  unsigned long long list_cap = (unsigned long long)n64 + 64;
   unsigned long long n_edges = 0;
   Scratch elist_b;
-  bool use_list = !done && list_cap >= (unsigned long long)n64 / 16 && k < 0x80000000u &&
-                  std::getenv("SSLIC_CC_NO_LIST") == nullptr &&
-                  elist_b.try_alloc((size_t)list_cap * 12, s);
-  uint32_t* ed = elist_b.as<uint32_t>();
+  uint32_t* ed = nullptr;
+  bool use_list = !done && k < 0x80000000u && std::getenv("SSLIC_CC_NO_LIST") == nullptr;
+  if (use_list) {
+    if (std::getenv("SSLIC_CC_LIST_IN_OUTPUT") == nullptr && mem_free > reserve &&
+        (mem_free - reserve) / 12 >= list_cap && elist_b.try_alloc((size_t)list_cap * 12, s)) {
+      ed = elist_b.as<uint32_t>();
+    } else {
+      ed = labels_out;
+      list_cap = (unsigned long long)n64 / 3;
+    }
+  }
   uint32_t* ex = ed + list_cap;
   uint32_t* el = ex + list_cap;
   if (!done) {

@@ -202,7 +202,7 @@ def test_slab_stitched_noisy_volume(sslic, oracle_lib):
 def test_tiled_ccl_and_edge_list_equal_whole_slab_union_find(sslic, oracle_lib, seed, dims, blob):
     """The CCL labels 32x8x8 tiles in shared memory and unites the tile faces
     afterwards (k_cc_tile / k_cc_seams), and the fixpoint rounds walk a list
-    of the voxels the edge pass works on (k_active_list / k_edges_list). On
+    of candidate edges (k_edge_list / k_edges_list). On
     volumes that cut tiles on every axis, with components from specks to
     blobs spanning many tiles: equal to the oracle's raster sweep, and equal
     to the whole-slab union-find with whole-map edge passes
@@ -219,3 +219,13 @@ def test_tiled_ccl_and_edge_list_equal_whole_slab_union_find(sslic, oracle_lib, 
     with _env(SSLIC_CC_SLAB_PLANES=max(1, dims[-1] // 3), SSLIC_CC_FORCE64=1):
         slabs = _check(sslic, oracle_lib, dims, lab, cen, 1, grid)
     assert np.array_equal(out, slabs)
+    # the edge list kept in the output map (what a volume that fills the
+    # device does), whole and in slabs; fields with more edges than room fall
+    # back to the map scans after the list was started
+    with _env(SSLIC_CC_LIST_IN_OUTPUT=1):
+        inout = _check(sslic, oracle_lib, dims, lab, cen, 1, grid)
+    assert np.array_equal(out, inout)
+    with _env(SSLIC_CC_LIST_IN_OUTPUT=1, SSLIC_CC_SLAB_PLANES=max(1, dims[-1] // 2),
+              SSLIC_CC_FORCE64=1):
+        inout = _check(sslic, oracle_lib, dims, lab, cen, 1, grid)
+    assert np.array_equal(out, inout)
