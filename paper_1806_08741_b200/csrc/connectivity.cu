@@ -2,7 +2,9 @@
 //
 // 1. Face-connected component labelling of the label map, slab by slab along
 //    the last axis (32-bit local offsets per slab): lock-free union-find
-//    (atomicMin hooking; a component's root is its smallest flat offset),
+//    (atomicMin hooking; a component's root is its smallest flat offset) --
+//    32x8x8 tiles in shared memory first, then the tile faces in global
+//    memory with path halving (k_cc_tile, k_cc_seams) --
 //    then the components are numbered densely in root order, so a node id
 //    orders components exactly like the raster sweep reaches them. Volumes of
 //    2^32 voxels or more take several slabs: their components are stitched
@@ -25,7 +27,9 @@
 //      adjacent to F_L's merged region ("absorbed");
 //    * te(L) and the absorbed sets depend only on earlier events, so Jacobi
 //      rounds (pointer jumping, one pass over the face edges) converge to the
-//      unique fixpoint, which equals the sequential sweep's outcome;
+//      unique fixpoint, which equals the sequential sweep's outcome; the
+//      edges that can matter are listed once (k_edge_list) and the rounds
+//      walk that list;
 //    * fresh ids are numbered by a prefix sum over events in root order.
 //    A pending adoption (no finalized neighbour at all) can only start at
 //    offset 0; the cascade it opens is emulated exactly by one device thread
@@ -35,7 +39,9 @@
 //
 // Voxel offsets are `Off` (uint32_t below 2^32 voxels, uint64_t above);
 // component (node) ids are 32-bit. Per voxel the pass needs the label map and
-// one node id (8 bytes); labels_out may alias labels_in.
+// one node id (8 bytes); labels_out may alias labels_in. labels_out doubles
+// as scratch (the edge list on a full device) until the final labels are
+// written: after a failed call its content is undefined.
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
 
