@@ -685,12 +685,33 @@ __global__ void k_edge_list(CG<Off> g, const uint32_t* nid, const uint8_t* flags
       }
     }
     if (!__any_sync(0xffffffffu, act)) continue;
-    unsigned cnt = 0;
-    if (act)
-      for_neighbours(g, (Off)p, [&](Off q) {
-        const uint32_t x = nid[q];
-        if (x != d && (!(flags[x] & kFin) || x == f)) ++cnt;
-      });
+    // the qualifying neighbour components, one register per face (static
+    // slots: the loops are unrolled), so the neighbours are gathered once
+    uint32_t xs[2 * kMaxRank];
+    unsigned vm = 0;
+    if (act) {
+      Off c[kMaxRank];
+      decode(g, (Off)p, c);
+#pragma unroll
+      for (int a = 0; a < kMaxRank; ++a) {
+        if (a < g.rank) {
+          if (c[a] > 0) {
+            const uint32_t x = nid[(Off)p - g.strides[a]];
+            const uint8_t fx = x != d ? flags[x] : kFin;
+            xs[2 * a] = x | 0u;
+            if (x != d && (!(fx & kFin) || x == f)) vm |= (1u | (fx & kProc ? 2u : 0u)) << (4 * a);
+          }
+          if (c[a] + 1 < g.dims[a]) {
+            const uint32_t x = nid[(Off)p + g.strides[a]];
+            const uint8_t fx = x != d ? flags[x] : kFin;
+            xs[2 * a + 1] = x;
+            if (x != d && (!(fx & kFin) || x == f)) vm |= (4u | (fx & kProc ? 8u : 0u)) << (4 * a);
+          }
+        }
+      }
+    }
+    // bits 0/2 of each nibble: slot 2a / 2a+1 holds an edge; bits 1/3: x is kProc
+    const unsigned cnt = __popc(vm & 0x5555u);
     unsigned incl = cnt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -702,17 +723,17 @@ __global__ void k_edge_list(CG<Off> g, const uint32_t* nid, const uint8_t* flags
     unsigned long long pos = 0;
     if (lane == 0) pos = atomicAdd(count, (unsigned long long)total);
     pos = __shfl_sync(0xffffffffu, pos, 0) + (incl - cnt);
-    if (cnt && pos + cnt <= cap)
-      for_neighbours(g, (Off)p, [&](Off q) {
-        const uint32_t x = nid[q];
-        const uint8_t fx = flags[x];
-        if (x != d && (!(fx & kFin) || x == f)) {
+    if (cnt && pos + cnt <= cap) {
+#pragma unroll
+      for (int j = 0; j < 2 * kMaxRank; ++j) {
+        if (vm >> (2 * j) & 1u) {
           ed[pos] = d;
-          ex[pos] = x;
-          el[pos] = l | (fx & kProc ? 0x80000000u : 0u);
+          ex[pos] = xs[j];
+          el[pos] = l | (vm >> (2 * j + 1) & 1u ? 0x80000000u : 0u);
           ++pos;
         }
-      });
+      }
+    }
   }
 }
 
@@ -930,6 +951,12 @@ uint32_t connectivity_impl(const Geom& g, const uint32_t* labels_in, const doubl
   const uint32_t k = (uint32_t)g.k;
   const bool timing = std::getenv("SSLIC_TIMING") != nullptr;
   const auto t0 = std::chrono::steady_clock::now();
+  double ph[5] = {0, 0, 0, 0, 0};  // CCL, node ids + stitching, finalize + pointers, list, rounds
+  auto stamp = [&](int i) {
+    if (!timing) return;
+    cudaStreamSynchronize(s);
+    ph[i] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  };
   const int last_axis = g.rank - 1;
   const int64_t last = g.dims[last_axis];
   int64_t plane = 1;
@@ -991,6 +1018,7 @@ uint32_t connectivity_impl(const Geom& g, const uint32_t* labels_in, const doubl
       m_total += slab_m[si];
     }
   }
+  stamp(0);
   if (m_total >= kNone) throw Error(SSLIC_EINVAL, "enforce_connectivity: >= 2^32 components");
   uint32_t m = (uint32_t)m_total;
   const unsigned max_label = read_scalar(c + 0, s);
@@ -1068,6 +1096,7 @@ uint32_t connectivity_impl(const Geom& g, const uint32_t* labels_in, const doubl
   }
   if (read_scalar(c + 4, s) != 0)
     throw Error(SSLIC_EINVAL, "enforce_connectivity: a component holds >= 2^32 voxels");
+  stamp(1);
   const Off* node_off = node_off_b.as<Off>();
   const uint32_t* nlab = nlab_b.as<uint32_t>();
   uint32_t* size = size_b.as<uint32_t>();
@@ -1137,6 +1166,7 @@ uint32_t connectivity_impl(const Geom& g, const uint32_t* labels_in, const doubl
         throw Error(SSLIC_ELOGIC, "enforce_connectivity: inconsistent prefix state");
     }
   }
+  stamp(2);
   int rounds = 0, jumps = 0;
   // List of the edge pass's candidate edges (12 bytes each). It lives in a
   // buffer of its own when the device has room for one edge per voxel beyond
@@ -1181,6 +1211,7 @@ uint32_t connectivity_impl(const Geom& g, const uint32_t* labels_in, const doubl
                                                      el, list_cap, cu + 4);
         SSLIC_CUDA_CHECK(cudaGetLastError());
         n_edges = read_scalar(cu + 4, s);
+        stamp(3);
         if (n_edges > list_cap) use_list = false;
       }
       if (use_list)
@@ -1197,6 +1228,7 @@ uint32_t connectivity_impl(const Geom& g, const uint32_t* labels_in, const doubl
     }
     // the last round left T consistent with the converged te / absorbed sets;
     // the event flags and their ranks reuse the (now dead) size array
+    stamp(4);
     uint32_t* ev = size;  // m + 1 entries
     k_events<<<blocks(m), 256, 0, s>>>(m, flags, nlab, fcomp, factive, te, ev);
     {
@@ -1223,11 +1255,13 @@ uint32_t connectivity_impl(const Geom& g, const uint32_t* labels_in, const doubl
     const auto t1 = std::chrono::steady_clock::now();
     std::fprintf(stderr,
                  "[sslic] connectivity: %lld voxels, %u components, %d CCL slab(s), %s, %d "
-                 "rounds (%s, %llu edges), %d jump passes, %.2f ms\n",
+                 "rounds (%s, %llu edges), %d jump passes, %.2f ms (ms from start: CCL %.1f, "
+                 "node ids %.1f, pointers %.1f, edge list %.1f, rounds %.1f)\n",
                  (long long)n64, m, nslabs,
                  full_serial ? "serial (ids >= k)" : (serial ? "serial prefix" : "no prefix"),
                  rounds, use_list ? "edge list" : "map scans", n_edges, jumps,
-                 std::chrono::duration<double, std::milli>(t1 - t0).count());
+                 std::chrono::duration<double, std::milli>(t1 - t0).count(), ph[0], ph[1], ph[2],
+                 ph[3], ph[4]);
   }
   return next;
 }
