@@ -170,7 +170,7 @@ __global__ void k_cc_union(CG<uint32_t> g, const uint32_t* labels, uint32_t* par
   }
 }
 
-// ---- tiled CCL for ranks 1-3 (the whole-slab k_cc_union above stays for rank 4)
+// ---- tiled CCL for ranks 2-3 (the whole-slab k_cc_union above stays for ranks 1 and 4)
 // A CTA labels one 32x8x8 tile in shared memory (runs along x by ballot, then
 // shared-memory atomicMin hooking along y and z) and writes each voxel's tile
 // root as a slab offset; k_cc_seams then unites equal labels across the tile
@@ -984,10 +984,11 @@ uint32_t connectivity_impl(const Geom& g, const uint32_t* labels_in, const doubl
   size_t tmp_bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, idx, idx, slab_max + 1, s);
   std::vector<uint32_t> slab_m(nslabs);
-  // tiled shared-memory CCL for ranks 1-3 with rows of at least half a tile
-  // (SSLIC_CC_NO_TILES=1: the whole-slab union-find, kept for rank 4 and for
-  // the equality test)
-  const bool tiled = g.rank <= 3 && g.dims[0] >= 16 && std::getenv("SSLIC_CC_NO_TILES") == nullptr;
+  // tiled shared-memory CCL for ranks 2-3 with rows of at least half a tile
+  // (a 1-D image would fill 1/64 of each tile; SSLIC_CC_NO_TILES=1: the
+  // whole-slab union-find, kept for ranks 1 and 4 and for the equality test)
+  const bool tiled = g.rank >= 2 && g.rank <= 3 && g.dims[0] >= 16 &&
+                     std::getenv("SSLIC_CC_NO_TILES") == nullptr;
   // -> nid[slab] = local roots, idx = root flags; `again`: the roots are
   // still in nid from the first pass (only idx was reused), so just the flags
   auto slab_ccl = [&](int si, bool again = false) {
